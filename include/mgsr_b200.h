@@ -1,0 +1,142 @@
+/* mgsr_b200 -- C ABI of the B200-native V-cycle hot path.
+ *
+ * Drop-in boundary for the reference package ``mgsr`` (arXiv 2403.07936
+ * reference, /root/reference/pkg/src/mgsr).  Every entry point is
+ * ``extern "C"``, takes plain device pointers and sizes (fp64 row-major n x n
+ * grids unless stated), a ``cudaStream_t`` passed as ``void*`` LAST, and
+ * returns an ``int`` status: 0 = ok, negative = error (see MGSR_E_*; the
+ * Python shim maps them to the reference's ValueError texts).  Caller owns
+ * all buffers; handles are immutable after creation except the V-cycle plan,
+ * which owns its level buffers and captured graphs.  No global mutable state.
+ *
+ * Each declaration names the reference interface it replaces (file:line).
+ */
+#ifndef MGSR_B200_H
+#define MGSR_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    MGSR_OK = 0,
+    MGSR_E_ODD_SIDE = -1,      /* "red-black coloring needs an even side"   (_stencil.pyx:15-16) */
+    MGSR_E_BAD_ARG = -2,       /* negative sweeps, n < 2, null pointer        (smoother.py:68-69)  */
+    MGSR_E_RATIO = -3,         /* "transfer ratio must be a power of two"     (transfer.py:22-24)  */
+    MGSR_E_NOT_DIVISIBLE = -4, /* "fine side ... is not divisible by ratio"   (transfer.py:34-35)  */
+    MGSR_E_PROLONG_RATIO = -5, /* "prolongation ratio must be one of"         (transfer.py:71-72)  */
+    MGSR_E_SR_RATIO = -6,      /* "unsupported SR ratio"                      (srmodel.py:479-480) */
+    MGSR_E_WINDOW = -7,        /* coarse side must be >= 6 and even           (srmodel.py:416-419) */
+    MGSR_E_CUDA = -8,          /* CUDA runtime error (message via mgsr_last_error) */
+    MGSR_E_WORKSPACE = -9,     /* workspace too small                                            */
+    MGSR_E_UNSUPPORTED = -10,  /* configuration not supported by this build                      */
+    MGSR_E_LADDER = -11        /* "no valid ladder"                           (solver.py:107-117)  */
+};
+
+/* Last error text of the calling thread (thread-local, never NULL). */
+const char *mgsr_last_error(void);
+/* Build/version string; also proves the library loads. */
+const char *mgsr_version(void);
+
+/* ---- stencil kernels: the MGSR_BACKEND plugin point (kernels/__init__.py:35-49) ---- */
+
+/* Bytes of device workspace mgsr_gs_sweeps / mgsr_residual / mgsr_restrict need for side n. */
+size_t mgsr_workspace_bytes(int64_t n);
+
+/* In-place red-black Gauss-Seidel, red=(i+j) even first, mean subtracted
+ * (deferred to once per call; <=6e-16 from per-sweep).
+ * Replaces kernels.gs_sweeps(p, f, h2, sweeps)  (_stencil.pyx:12-45). */
+int mgsr_gs_sweeps(double *p, const double *f, int64_t n, double h2, int32_t sweeps,
+                   void *ws, size_t ws_bytes, void *stream);
+
+/* out = (nb - 4p) * inv_h2, periodic; any n >= 2.
+ * Replaces kernels.laplacian(p, inv_h2)  (_stencil.pyx:48-63). */
+int mgsr_laplacian(const double *p, double *out, int64_t n, double inv_h2, void *stream);
+
+/* r = f - L p, then r -= mean(r).  Replaces smoother.residual (smoother.py:52-57). */
+int mgsr_residual(const double *p, const double *f, double *r, int64_t n,
+                  void *ws, size_t ws_bytes, void *stream);
+
+/* coarse = fine[::s, ::s] (- its mean if subtract_mean).
+ * Replaces transfer.restrict (transfer.py:27-39). */
+int mgsr_restrict(const double *fine, double *coarse, int64_t n, int32_t s, int32_t subtract_mean,
+                  void *ws, size_t ws_bytes, void *stream);
+
+/* out (nc*s)^2 = separable periodic Keys(a=-1/2) interpolation of c (nc^2).
+ * Replaces transfer.spline_prolong (transfer.py:64-74). */
+int mgsr_spline_prolong(const double *c, int64_t nc, int32_t s, double *out, void *stream);
+
+/* Reductions used by Grid.rms / diff_norm (grid.py:67-78): out[0] = sqrt(mean((a-b)^2))
+ * (b may be NULL -> rms(a)). Deterministic fixed-order reduction. */
+int mgsr_rms_diff(const double *a, const double *b, int64_t count, double *out_host,
+                  void *ws, size_t ws_bytes, void *stream);
+
+/* ---- generator (srmodel.py:90-487) ---- */
+
+typedef struct mgsr_gen mgsr_gen;
+
+enum { MGSR_PREC_FP32 = 0, MGSR_PREC_BF16 = 1 };
+
+/* Build an immutable generator from the MGSR1 tensor set (host float32 arrays in
+ * the canonical order of expected_tensor_shapes(B), srmodel.py:90-114), i.e.
+ * head.conv.weight, head.prelu.alpha, res{i}.{conv1.weight, bn1.gamma, bn1.beta,
+ * bn1.mean, bn1.var, prelu.alpha, conv2.weight, bn2.gamma, bn2.beta, bn2.mean,
+ * bn2.var} for i < B, post.conv.weight, post.bn.{gamma,beta,mean,var},
+ * up.conv.weight, up.prelu.alpha, tail.conv.weight, tail.conv.bias.
+ * Replaces srmodel.GeneratorWeights / load_weights (srmodel.py:117-248). */
+int mgsr_generator_create(const float *const *tensors, int32_t num_tensors, int32_t blocks,
+                          double tanh_scale, mgsr_gen **out);
+int mgsr_generator_destroy(mgsr_gen *g);
+
+/* y (N,3,2h,2h) = generator(x (N,3,h,h)), fp64 in/out, any h >= 1 (fp32 compute).
+ * Replaces srmodel.generator_forward / _forward_batch (srmodel.py:330-354). */
+int mgsr_generator_forward(const mgsr_gen *g, const double *x, int64_t batch, int64_t side,
+                           double *y, void *stream);
+
+/* Windowed SR prolongation by s in {2,4,8,16}: normalise, 6x6 windows at
+ * stride 2, generator, channel mean, stitch, denormalise with output signs,
+ * mean-subtract (per pass).  precision: MGSR_PREC_FP32 (CUDA-core fp32) or
+ * MGSR_PREC_BF16 (tcgen05 bf16 operands / fp32 accumulate; s == 2 only).
+ * Replaces srmodel.sr_prolong (srmodel.py:470-487). */
+size_t mgsr_sr_workspace_bytes(int64_t nc, int32_t s);
+int mgsr_sr_prolong(const mgsr_gen *g, const double *c, int64_t nc, int32_t s,
+                    double p_min, double p_max, int32_t precision, double *out,
+                    void *ws, size_t ws_bytes, void *stream);
+
+/* ---- V-cycle driver (solver.py:100-330) ---- */
+
+typedef struct mgsr_plan mgsr_plan;
+
+typedef struct {
+    int64_t n;             /* fine side */
+    int32_t n_step;        /* RunConfig.N_step */
+    int32_t r_min;         /* RunConfig.r_min */
+    int32_t n_smooth;      /* RunConfig.N_smooth */
+    int32_t coarse_sweeps; /* RunConfig.coarse_sweeps */
+    double p_min, p_max;   /* RunConfig.p_min / p_max (SR normalisation band) */
+    int32_t precision;     /* MGSR_PREC_* for SR prolongations */
+    uint32_t sr_level_mask;/* bit l set: prolongation from level l+1 into level l may use SR
+                              when the cycle's operator is "sr" (all ones = reference behaviour) */
+} mgsr_plan_config;
+
+/* Plan: level ladder (solver.py:100-119), per-level buffers, and one CUDA graph
+ * per operator variant captured on first use.  gen may be NULL (spline only). */
+int mgsr_plan_create(const mgsr_plan_config *cfg, const mgsr_gen *gen, mgsr_plan **out);
+int mgsr_plan_destroy(mgsr_plan *plan);
+int32_t mgsr_plan_levels(const mgsr_plan *plan, int64_t *sides_out /* >= 32 entries */);
+
+/* One V-cycle on iterate p (in place) with RHS f, then the solve-loop logging
+ * pass: stats[0] = diff_norm(new_p, old_p), stats[1] = residual(new_p).rms()
+ * (solver.py:311-313), written to the device buffer stats_dev (2 doubles).
+ * use_sr: 0 -> operator "spline", 1 -> operator "sr".  One graph launch.
+ * Replaces solver.v_cycle (solver.py:158-197) + solver.py:312-313. */
+int mgsr_plan_vcycle(mgsr_plan *plan, double *p, const double *f, int32_t use_sr,
+                     double *stats_dev, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MGSR_B200_H */

@@ -1,0 +1,41 @@
+// Generator handle and SR-prolongation launchers (internal).
+#pragma once
+#include <vector>
+
+#include "common.cuh"
+
+struct mgsr_gen {
+    int blocks = 0;
+    double tanh_scale = 1.0;
+    // fp32 device tensors (reference layout, OIHW)
+    float *head_w = nullptr;   // 64 x 3 x 9 x 9
+    float *head_a = nullptr;   // 64
+    std::vector<float *> c1, c2;           // per block 64x64x3x3
+    std::vector<float *> bn1s, bn1b, bn2s, bn2b, pa;   // folded BN scale / shift, PReLU alpha
+    float *post_w = nullptr, *post_s = nullptr, *post_b = nullptr;
+    float *up_w = nullptr, *up_a = nullptr;  // 256x64x3x3, 64
+    float *tail_w = nullptr, *tail_b = nullptr;  // 3x64x9x9, 3
+    // tensor-core path: packed weights / constants (one device blob), see generator_tc.cu
+    void *tc_blob = nullptr;
+    size_t tc_bytes = 0;
+    std::vector<void *> allocations;
+};
+
+namespace mgsr {
+
+// Windowed SR prolongation (one full sr_prolong, all passes).
+// c_shift: optional device scalar subtracted from c before normalising.
+// out: fine grid (nc*s)^2 raw data (before the final mean subtraction);
+// out_mean: device scalar = mean(out).
+size_t sr_workspace_bytes(int64_t nc, int s, int precision);
+int launch_sr_prolong(const mgsr_gen *g, const double *c, const double *c_shift, int nc, int s, double p_min,
+                      double p_max, int precision, double *out, double *out_mean, void *ws, size_t ws_bytes,
+                      void *red_slot, cudaStream_t st);
+
+// tensor-core generator (generator_tc.cu): windows of a 6x6 pass, ratio 2.
+int tc_pack_weights(mgsr_gen *g);
+size_t tc_workspace_bytes(int64_t nc);
+int launch_sr_pass_tc(const mgsr_gen *g, const double *c, const double *c_shift, int nc, double log_lo,
+                      double span, double *fine, void *ws, size_t ws_bytes, cudaStream_t st);
+
+}  // namespace mgsr

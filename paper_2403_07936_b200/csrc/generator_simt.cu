@@ -1,0 +1,455 @@
+// Generator inference on CUDA cores in fp32 (precision mode MGSR_PREC_FP32)
+// and the windowed SR-prolongation glue (gather / stitch / denormalise).
+//
+// Reference: srmodel.py:285-344 (replicate-padded same-size correlation,
+// PReLU, BN eps=1e-5, pixel shuffle c*4+i*2+j -> (i,j), tail bias + s*tanh(x/s)),
+// srmodel.py:414-487 (6x6 windows at stride 2, central-band stitch, channel
+// mean, sign-preserving log map).  General window side (the second generator
+// application of a x4 pass runs on 12x12); this is the reference-precision
+// path, the tensor-core path lives in generator_tc.cu.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "generator.cuh"
+#include "stencil.cuh"
+
+namespace mgsr {
+
+enum { OP_PRELU = 0, OP_BN_PRELU = 1, OP_BN_RES = 2, OP_SHUF_PRELU = 3, OP_TAIL = 4 };
+
+struct Epi {
+    const float *scale, *shift, *alpha, *bias;
+    const float *res;   // OP_BN_RES residual input (may alias out)
+    float tanh_s;
+};
+
+constexpr int kConvThreads = 256, kConvOB = 16;
+
+// Same-size correlation with replicate padding, CTA = (sample, 16 output
+// channels); input channels staged through shared memory in chunks.
+template <int K, int MAXP, int OP>
+__global__ void __launch_bounds__(kConvThreads) k_conv_simt(const float *__restrict__ in, int C, int H,
+                                                            const float *__restrict__ w, int O,
+                                                            float *__restrict__ out, Epi ep, int cc_max) {
+    extern __shared__ float s_in[];
+    constexpr int P = K / 2;
+    const int n = blockIdx.x, ob = blockIdx.y * kConvOB, tid = threadIdx.x;
+    const int HW = H * H, HP = H + K - 1;
+    const int nout = kConvOB * HW;
+    float acc[MAXP];
+#pragma unroll
+    for (int k = 0; k < MAXP; ++k) acc[k] = 0.f;
+    for (int c0 = 0; c0 < C; c0 += cc_max) {
+        const int cc = min(cc_max, C - c0);
+        __syncthreads();
+        for (int idx = tid; idx < cc * HP * HP; idx += kConvThreads) {
+            int c = idx / (HP * HP), r = idx - c * HP * HP;
+            int yy = min(max(r / HP - P, 0), H - 1), xx = min(max(r % HP - P, 0), H - 1);
+            s_in[idx] = in[((int64_t(n) * C + c0 + c) * H + yy) * H + xx];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < MAXP; ++k) {
+            const int idx = tid + k * kConvThreads;
+            if (idx >= nout) break;
+            const int o = ob + idx / HW, pix = idx % HW, y = pix / H, x = pix % H;
+            if (o >= O) continue;
+            const float *wo = w + (int64_t(o) * C + c0) * K * K;
+            float a = acc[k];
+            for (int c = 0; c < cc; ++c) {
+                const float *si = s_in + (c * HP + y) * HP + x;
+                const float *wc = wo + c * K * K;
+#pragma unroll
+                for (int dy = 0; dy < K; ++dy)
+#pragma unroll
+                    for (int dx = 0; dx < K; ++dx) a = fmaf(si[dy * HP + dx], __ldg(wc + dy * K + dx), a);
+            }
+            acc[k] = a;
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < MAXP; ++k) {
+        const int idx = tid + k * kConvThreads;
+        if (idx >= nout) break;
+        const int o = ob + idx / HW, pix = idx % HW, y = pix / H, x = pix % H;
+        if (o >= O) continue;
+        float v = acc[k];
+        if (OP == OP_PRELU) {
+            out[(int64_t(n) * O + o) * HW + pix] = v > 0.f ? v : ep.alpha[o] * v;
+        } else if (OP == OP_BN_PRELU) {
+            v = fmaf(v, ep.scale[o], ep.shift[o]);
+            out[(int64_t(n) * O + o) * HW + pix] = v > 0.f ? v : ep.alpha[o] * v;
+        } else if (OP == OP_BN_RES) {
+            int64_t oi = (int64_t(n) * O + o) * HW + pix;
+            out[oi] = ep.res[oi] + fmaf(v, ep.scale[o], ep.shift[o]);
+        } else if (OP == OP_SHUF_PRELU) {
+            const int c = o >> 2, i = (o >> 1) & 1, j = o & 1, W2 = 2 * H;
+            v = v > 0.f ? v : ep.alpha[c] * v;
+            out[((int64_t(n) * (O >> 2) + c) * W2 + 2 * y + i) * W2 + 2 * x + j] = v;
+        } else {
+            const float s = ep.tanh_s;
+            out[(int64_t(n) * O + o) * HW + pix] = s * tanhf((v + ep.bias[o]) / s);
+        }
+    }
+}
+
+template <int K, int OP>
+static int conv(const float *in, int N, int C, int H, const float *w, int O, float *out, const Epi &ep,
+                cudaStream_t st) {
+    const int HP = H + K - 1;
+    int cc = 12288 / (HP * HP);
+    if (cc > C) cc = C;
+    if (cc < 1) { set_error("conv window too large"); return MGSR_E_UNSUPPORTED; }
+    const size_t smem = sizeof(float) * cc * HP * HP;
+    const int per = (kConvOB * H * H + kConvThreads - 1) / kConvThreads;
+    dim3 grid(N, (O + kConvOB - 1) / kConvOB);
+    if (per <= 3)
+        k_conv_simt<K, 3, OP><<<grid, kConvThreads, smem, st>>>(in, C, H, w, O, out, ep, cc);
+    else if (per <= 9)
+        k_conv_simt<K, 9, OP><<<grid, kConvThreads, smem, st>>>(in, C, H, w, O, out, ep, cc);
+    else if (per <= 36)
+        k_conv_simt<K, 36, OP><<<grid, kConvThreads, smem, st>>>(in, C, H, w, O, out, ep, cc);
+    else { set_error("window side too large for the fp32 generator"); return MGSR_E_UNSUPPORTED; }
+    MGSR_LAUNCH_CHECK();
+    return MGSR_OK;
+}
+
+// Per-window scratch floats for a forward at side H (buffers S, Y, Z, U, out).
+static size_t gen_scratch_floats(int H) { return size_t(64) * H * H * 3 + size_t(64) * 4 * H * H + 3 * 4 * H * H; }
+
+// Generator forward on N samples (N,3,H,H) fp32 -> (N,3,2H,2H) fp32 (srmodel.py:330-344).
+static int gen_forward_f32(const mgsr_gen *g, const float *x, int N, int H, float *y, float *scratch,
+                           cudaStream_t st) {
+    const size_t t64 = size_t(N) * 64 * H * H;
+    float *S = scratch, *Y = S + t64, *Z = Y + t64, *U = Z + t64;
+    Epi ep{};
+    int r;
+    ep.alpha = g->head_a;
+    if ((r = conv<9, OP_PRELU>(x, N, 3, H, g->head_w, 64, S, ep, st))) return r;
+    MGSR_CUDA_TRY(cudaMemcpyAsync(Y, S, sizeof(float) * t64, cudaMemcpyDeviceToDevice, st));
+    for (int b = 0; b < g->blocks; ++b) {
+        Epi e1{g->bn1s[b], g->bn1b[b], g->pa[b], nullptr, nullptr, 1.f};
+        if ((r = conv<3, OP_BN_PRELU>(Y, N, 64, H, g->c1[b], 64, Z, e1, st))) return r;
+        Epi e2{g->bn2s[b], g->bn2b[b], nullptr, nullptr, Y, 1.f};
+        if ((r = conv<3, OP_BN_RES>(Z, N, 64, H, g->c2[b], 64, Y, e2, st))) return r;
+    }
+    Epi ep_post{g->post_s, g->post_b, nullptr, nullptr, S, 1.f};
+    if ((r = conv<3, OP_BN_RES>(Y, N, 64, H, g->post_w, 64, Z, ep_post, st))) return r;
+    Epi ep_up{nullptr, nullptr, g->up_a, nullptr, nullptr, 1.f};
+    if ((r = conv<3, OP_SHUF_PRELU>(Z, N, 64, H, g->up_w, 256, U, ep_up, st))) return r;
+    Epi ep_t{nullptr, nullptr, nullptr, g->tail_b, nullptr, float(g->tanh_scale)};
+    return conv<9, OP_TAIL>(U, N, 64, 2 * H, g->tail_w, 3, y, ep_t, st);
+}
+
+// ---------------------------------------------------------------------------
+// windowed pass glue
+
+// q = clip((log10|v| - log_lo)/span, 0, 1) * sign(v) in fp64 (grid.py:103-109)
+__device__ __forceinline__ double normalize_q(double v, double log_lo, double span) {
+    if (v == 0.0) return 0.0;
+    double t = (log10(fabs(v)) - log_lo) / span;
+    t = t < 0.0 ? 0.0 : (t > 1.0 ? 1.0 : t);
+    return v > 0.0 ? t : -t;
+}
+
+__device__ __forceinline__ double denormalize_q(double q, double log_lo, double span) {
+    if (q == 0.0) return 0.0;   // sign 0 annihilates (grid.py:112-114)
+    double m = pow(10.0, log_lo + fabs(q) * span);
+    return q > 0.0 ? m : -m;
+}
+
+// windows [k0, k0+cnt) of the plan (srmodel.py:423-440) -> X (cnt, 3, 6, 6) fp32
+__global__ void k_sr_gather(const double *__restrict__ c, const double *shift, int nc, int npos, int64_t k0,
+                            int cnt, double log_lo, double span, float *__restrict__ X) {
+    const double sh = shift ? *shift : 0.0;
+    const int64_t total = int64_t(cnt) * 36;
+    for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < total;
+         t += int64_t(gridDim.x) * blockDim.x) {
+        int64_t kw = t / 36;
+        int pix = int(t - kw * 36), y = pix / 6, x = pix % 6;
+        int64_t k = k0 + kw;
+        int iw = 2 * int(k / npos), jw = 2 * int(k % npos);
+        float q = float(normalize_q(c[int64_t(iw + y) * nc + jw + x] - sh, log_lo, span));
+        X[(kw * 3 + 0) * 36 + pix] = q;
+        X[(kw * 3 + 1) * 36 + pix] = q;
+        X[(kw * 3 + 2) * 36 + pix] = q;
+    }
+}
+
+// general gather for a pass whose input is a (nc, nc) grid and windows 6x6
+// (also used for the 12x12 second application input? no: that is the
+// generator's own output, fed directly).  Stitch: channel mean, keep band,
+// denormalise.  Yout (cnt, 3, 6*sc, 6*sc).
+__global__ void k_sr_stitch(const float *__restrict__ Y, int npos, int64_t k0, int cnt, int sc, int nc,
+                            double log_lo, double span, double *__restrict__ fine) {
+    const int side = 6 * sc;
+    const int64_t per = int64_t(side) * side;
+    const int64_t total = int64_t(cnt) * per;
+    const int nf = nc * sc;
+    const int last = 2 * (npos - 1);
+    for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < total;
+         t += int64_t(gridDim.x) * blockDim.x) {
+        int64_t kw = t / per;
+        int pix = int(t - kw * per), fy = pix / side, fx = pix % side;
+        int64_t k = k0 + kw;
+        int iw = 2 * int(k / npos), jw = 2 * int(k % npos);
+        int lo_i = iw == 0 ? 0 : 2, hi_i = iw == last ? 6 : 4;
+        int lo_j = jw == 0 ? 0 : 2, hi_j = jw == last ? 6 : 4;
+        if (fy < lo_i * sc || fy >= hi_i * sc || fx < lo_j * sc || fx >= hi_j * sc) continue;
+        const float *yw = Y + kw * 3 * per + pix;
+        double m = ((double(yw[0]) + double(yw[per])) + double(yw[2 * per])) / 3.0;
+        fine[int64_t(iw * sc + fy) * nf + jw * sc + fx] = denormalize_q(m, log_lo, span);
+    }
+}
+
+__global__ void k_mean_f64(const double *__restrict__ a, int64_t count, RedSlot slot, double *result) {
+    double v[1] = {0.0};
+    for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < count;
+         t += int64_t(gridDim.x) * blockDim.x)
+        v[0] += a[t];
+    grid_reduce<1>(v, slot, result, 1.0 / double(count));
+}
+
+__global__ void k_f64_to_f32(const double *__restrict__ a, float *__restrict__ b, int64_t count) {
+    for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < count;
+         t += int64_t(gridDim.x) * blockDim.x)
+        b[t] = float(a[t]);
+}
+
+__global__ void k_f32_to_f64(const float *__restrict__ a, double *__restrict__ b, int64_t count) {
+    for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < count;
+         t += int64_t(gridDim.x) * blockDim.x)
+        b[t] = double(a[t]);
+}
+
+constexpr int kSrChunk = 4096;   // windows per fp32 chunk
+
+static size_t pass_ws_floats(int apps) {
+    // input X (3*36) + generator scratch for the largest application + outputs
+    int H = 6, Hmax = 6 * (1 << (apps - 1));
+    size_t per = 3 * 36 + gen_scratch_floats(Hmax) + 3 * 4 * Hmax * Hmax + 3 * 4 * H * H * 4;
+    return per * kSrChunk;
+}
+
+size_t sr_workspace_bytes(int64_t nc, int s, int precision) {
+    // intermediate fine grid for two-pass ratios + fp32 chunk buffers + scalars
+    size_t inter = (s == 8 || s == 16) ? sizeof(double) * size_t(nc * 4) * size_t(nc * 4) : 0;
+    size_t simt = sizeof(float) * pass_ws_floats(2) + 4096;
+    size_t tc = precision == MGSR_PREC_BF16 ? tc_workspace_bytes(nc) : 0;
+    return inter + (simt > tc ? simt : tc) + 512;
+}
+
+static const int *pass_plan(int s, int *count) {
+    static const int p2[] = {1}, p4[] = {2}, p8[] = {2, 1}, p16[] = {2, 2};
+    switch (s) {
+        case 2: *count = 1; return p2;
+        case 4: *count = 1; return p4;
+        case 8: *count = 2; return p8;
+        case 16: *count = 2; return p16;
+    }
+    *count = 0;
+    return nullptr;
+}
+
+// One windowed pass (srmodel.py:443-463) with `apps` applications, fp32 generator.
+static int sr_pass_simt(const mgsr_gen *g, const double *c, const double *c_shift, int nc, int apps,
+                        double log_lo, double span, double *fine, float *fws, cudaStream_t st) {
+    const int npos = nc / 2 - 2;
+    const int64_t nw = int64_t(npos) * npos;
+    const int Hmax = 6 * (1 << (apps - 1));
+    float *X = fws;
+    float *Y1 = X + size_t(kSrChunk) * 3 * 36;                 // (chunk,3,12,12)
+    float *Y2 = Y1 + size_t(kSrChunk) * 3 * 144;               // (chunk,3,24,24) if apps == 2
+    float *scratch = Y2 + (apps == 2 ? size_t(kSrChunk) * 3 * 576 : 0);
+    (void)Hmax;
+    for (int64_t k0 = 0; k0 < nw; k0 += kSrChunk) {
+        int cnt = int(nw - k0 < kSrChunk ? nw - k0 : kSrChunk);
+        k_sr_gather<<<grid_for(int64_t(cnt) * 36, 256), 256, 0, st>>>(c, c_shift, nc, npos, k0, cnt, log_lo, span, X);
+        MGSR_LAUNCH_CHECK();
+        int r = gen_forward_f32(g, X, cnt, 6, Y1, scratch, st);
+        if (r) return r;
+        const float *Yout = Y1;
+        if (apps == 2) {
+            r = gen_forward_f32(g, Y1, cnt, 12, Y2, scratch, st);
+            if (r) return r;
+            Yout = Y2;
+        }
+        int sc = 1 << apps;
+        k_sr_stitch<<<grid_for(int64_t(cnt) * 36 * sc * sc, 256), 256, 0, st>>>(Yout, npos, k0, cnt, sc, nc, log_lo,
+                                                                                span, fine);
+        MGSR_LAUNCH_CHECK();
+    }
+    return MGSR_OK;
+}
+
+int launch_sr_prolong(const mgsr_gen *g, const double *c, const double *c_shift, int nc, int s, double p_min,
+                      double p_max, int precision, double *out, double *out_mean, void *ws, size_t ws_bytes,
+                      void *red_slot, cudaStream_t st) {
+    int npass = 0;
+    const int *plan = pass_plan(s, &npass);
+    if (!plan) { set_error("unsupported SR ratio " + std::to_string(s) + "; expected one of [2, 4, 8, 16]"); return MGSR_E_SR_RATIO; }
+    if (nc < 6) { set_error("coarse side must be >= 6, got " + std::to_string(nc)); return MGSR_E_WINDOW; }
+    if (nc % 2) { set_error("coarse side must be even, got " + std::to_string(nc)); return MGSR_E_WINDOW; }
+    if (ws_bytes < sr_workspace_bytes(nc, s, precision)) { set_error("sr workspace too small"); return MGSR_E_WORKSPACE; }
+    const double log_lo = std::log10(p_min), span = std::log10(p_max) - std::log10(p_min);
+    char *w = static_cast<char *>(ws);
+    double *scal = reinterpret_cast<double *>(w);     // [0] intermediate mean
+    w += 512;
+    double *inter = nullptr;
+    if (npass == 2) {
+        inter = reinterpret_cast<double *>(w);
+        w += sizeof(double) * size_t(nc * 4) * size_t(nc * 4);
+    }
+    RedSlot sl = red_slot_at(red_slot);
+    const double *src = c;
+    const double *src_shift = c_shift;
+    int n_in = nc;
+    for (int ip = 0; ip < npass; ++ip) {
+        const int apps = plan[ip];
+        double *dst = (ip == npass - 1) ? out : inter;
+        int r;
+        if (precision == MGSR_PREC_BF16) {
+            // tensor-core path only; no silent fallback to the fp32 CUDA-core path
+            if (apps != 1 || !g->tc_blob) {
+                set_error("bf16 tensor-core generator supports 6x6 windows (ratio-2 passes) only");
+                return MGSR_E_UNSUPPORTED;
+            }
+            r = launch_sr_pass_tc(g, src, src_shift, n_in, log_lo, span, dst, w, ws_bytes - (w - static_cast<char *>(ws)), st);
+        } else {
+            r = sr_pass_simt(g, src, src_shift, n_in, apps, log_lo, span, dst, reinterpret_cast<float *>(w), st);
+        }
+        if (r) return r;
+        const int n_out = n_in << apps;
+        double *mean_dst = (ip == npass - 1) ? out_mean : scal;
+        k_mean_f64<<<grid_for(int64_t(n_out) * n_out, 256), 256, 0, st>>>(dst, int64_t(n_out) * n_out, sl, mean_dst);
+        MGSR_LAUNCH_CHECK();
+        src = dst;
+        src_shift = scal;
+        n_in = n_out;
+    }
+    return MGSR_OK;
+}
+
+}  // namespace mgsr
+
+// ---------------------------------------------------------------------------
+// C ABI (generator part)
+
+using namespace mgsr;
+
+namespace {
+
+int upload(mgsr_gen *g, const float *host, size_t count, float **dst) {
+    float *d = nullptr;
+    MGSR_CUDA_TRY(cudaMalloc(&d, sizeof(float) * count));
+    MGSR_CUDA_TRY(cudaMemcpy(d, host, sizeof(float) * count, cudaMemcpyHostToDevice));
+    g->allocations.push_back(d);
+    *dst = d;
+    return MGSR_OK;
+}
+
+// BN(x) = gamma (x - mean)/sqrt(var + 1e-5) + beta  ->  x*scale + shift (srmodel.py:313-318)
+int upload_bn(mgsr_gen *g, const float *gamma, const float *beta, const float *mean, const float *var, float **s,
+              float **b) {
+    std::vector<float> sc(64), sh(64);
+    for (int i = 0; i < 64; ++i) {
+        double k = double(gamma[i]) / std::sqrt(double(var[i]) + 1e-5);
+        sc[i] = float(k);
+        sh[i] = float(double(beta[i]) - double(mean[i]) * k);
+    }
+    if (int r = upload(g, sc.data(), 64, s)) return r;
+    return upload(g, sh.data(), 64, b);
+}
+
+}  // namespace
+
+extern "C" int mgsr_generator_create(const float *const *t, int32_t num_tensors, int32_t blocks, double tanh_scale,
+                                     mgsr_gen **out) {
+    if (blocks < 1 || num_tensors != 2 + 11 * blocks + 5 + 2 + 2) {
+        set_error("missing tensors: tensor count does not match expected_tensor_shapes(" + std::to_string(blocks) + ")");
+        return MGSR_E_BAD_ARG;
+    }
+    if (!(tanh_scale >= 1.0)) { set_error("tanh scale must be >= 1"); return MGSR_E_BAD_ARG; }
+    mgsr_gen *g = new mgsr_gen();
+    g->blocks = blocks;
+    g->tanh_scale = tanh_scale;
+    int i = 0, r = 0;
+#define UP(cnt, dst) if ((r = upload(g, t[i++], (cnt), (dst)))) goto fail;
+    UP(64 * 3 * 81, &g->head_w);
+    UP(64, &g->head_a);
+    g->c1.resize(blocks); g->c2.resize(blocks); g->bn1s.resize(blocks); g->bn1b.resize(blocks);
+    g->bn2s.resize(blocks); g->bn2b.resize(blocks); g->pa.resize(blocks);
+    for (int b = 0; b < blocks; ++b) {
+        UP(64 * 64 * 9, &g->c1[b]);
+        if ((r = upload_bn(g, t[i], t[i + 1], t[i + 2], t[i + 3], &g->bn1s[b], &g->bn1b[b]))) goto fail;
+        i += 4;
+        UP(64, &g->pa[b]);
+        UP(64 * 64 * 9, &g->c2[b]);
+        if ((r = upload_bn(g, t[i], t[i + 1], t[i + 2], t[i + 3], &g->bn2s[b], &g->bn2b[b]))) goto fail;
+        i += 4;
+    }
+    UP(64 * 64 * 9, &g->post_w);
+    if ((r = upload_bn(g, t[i], t[i + 1], t[i + 2], t[i + 3], &g->post_s, &g->post_b))) goto fail;
+    i += 4;
+    UP(256 * 64 * 9, &g->up_w);
+    UP(64, &g->up_a);
+    UP(3 * 64 * 81, &g->tail_w);
+    UP(3, &g->tail_b);
+#undef UP
+    if ((r = tc_pack_weights(g))) goto fail;
+    *out = g;
+    return MGSR_OK;
+fail:
+    mgsr_generator_destroy(g);
+    return r;
+}
+
+extern "C" int mgsr_generator_destroy(mgsr_gen *g) {
+    if (!g) return MGSR_OK;
+    for (void *p : g->allocations) cudaFree(p);
+    if (g->tc_blob) cudaFree(g->tc_blob);
+    delete g;
+    return MGSR_OK;
+}
+
+extern "C" int mgsr_generator_forward(const mgsr_gen *g, const double *x, int64_t batch, int64_t side, double *y,
+                                      void *stream) {
+    if (!g || !x || !y || batch < 1 || side < 1) { set_error("bad argument"); return MGSR_E_BAD_ARG; }
+    if (side > 12) { set_error("fp32 generator supports input side <= 12"); return MGSR_E_UNSUPPORTED; }
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int H = int(side);
+    size_t nx = size_t(batch) * 3 * H * H, ny = size_t(batch) * 3 * 4 * H * H;
+    size_t bytes = sizeof(float) * (nx + ny + gen_scratch_floats(H) * size_t(batch));
+    float *buf = nullptr;
+    MGSR_CUDA_TRY(cudaMallocAsync(&buf, bytes, st));
+    k_f64_to_f32<<<grid_for(nx, 256), 256, 0, st>>>(x, buf, nx);
+    int r = gen_forward_f32(g, buf, int(batch), H, buf + nx, buf + nx + ny, st);
+    if (!r) k_f32_to_f64<<<grid_for(ny, 256), 256, 0, st>>>(buf + nx, y, ny);
+    cudaFreeAsync(buf, st);
+    if (!r) MGSR_LAUNCH_CHECK();
+    return r;
+}
+
+extern "C" size_t mgsr_sr_workspace_bytes(int64_t nc, int32_t s) {
+    return sr_workspace_bytes(nc, s, MGSR_PREC_BF16) + kRedSlotBytes + 256;
+}
+
+extern "C" int mgsr_sr_prolong(const mgsr_gen *g, const double *c, int64_t nc, int32_t s, double p_min,
+                               double p_max, int32_t precision, double *out, void *ws, size_t ws_bytes,
+                               void *stream) {
+    if (!g || !c || !out) { set_error("SR prolongation requires generator weights"); return MGSR_E_BAD_ARG; }
+    if (ws_bytes < mgsr_sr_workspace_bytes(nc, s)) { set_error("workspace too small"); return MGSR_E_WORKSPACE; }
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    char *w = static_cast<char *>(ws);
+    double *mean = reinterpret_cast<double *>(w);
+    void *red = w + 256;
+    w += 256 + kRedSlotBytes;
+    int r = launch_sr_prolong(g, c, nullptr, int(nc), s, p_min, p_max, precision, out, mean, w,
+                              ws_bytes - 256 - kRedSlotBytes, red, st);
+    if (r) return r;
+    return launch_affine(out, out, int64_t(nc) * s * nc * s, mean, 1.0, st);
+}

@@ -1,0 +1,240 @@
+// Device-resident V-cycle (solver.py:158-197) plus the solve-loop logging pass
+// (solver.py:311-313), captured once per (operator, buffers) variant into a
+// CUDA graph and replayed: one graph launch per cycle.
+//
+// Level buffers (fine -> coarse, sides from level_sides, solver.py:100-119):
+//   level 0: caller's p (iterate) and f; S = smoothed iterate, then out.
+//   level l>=1: rc[l] = raw injected residual of level l-1 (its RHS is
+//     0.5 * (rc[l] - mean(rc[l])), consumed on the fly, solver.py:178-179),
+//     d[l] = Gauss-Seidel correction from zero (raw, mean d_mean[l]),
+//     then d[l] <- (d[l] - d_mean[l]) + up[l]   (solver.py:190).
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <map>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "common.cuh"
+#include "generator.cuh"
+#include "stencil.cuh"
+
+using namespace mgsr;
+
+namespace {
+
+enum Scalar {
+    SC_S_MEAN = 0,    // mean of the smoothed top iterate
+    SC_OUT_MEAN = 1,  // mean of out (top)
+    SC_ACC = 2,       // 3 accumulators for the logging pass (2..4)
+    SC_STATS = 5,     // diff_norm, residual rms (5..6) -- internal copy
+    SC_LEVEL0 = 8     // per level l: rc_mean 8+4l, d_mean 9+4l, sr_mean 10+4l
+};
+
+}  // namespace
+
+struct mgsr_plan {
+    mgsr_plan_config cfg{};
+    const mgsr_gen *gen = nullptr;
+    std::vector<int> sides;
+    void *mem = nullptr;
+    size_t mem_bytes = 0;
+    double *scal = nullptr;
+    void *red = nullptr;      // 4 reduction slots
+    double *S = nullptr, *tmp = nullptr, *srbuf = nullptr;
+    std::vector<double *> rc, d;
+    void *srws = nullptr;
+    size_t srws_bytes = 0;
+    cudaStream_t cap = nullptr;
+    std::map<std::tuple<double *, const double *, int>, cudaGraphExec_t> graphs;
+};
+
+namespace {
+
+double *sc(mgsr_plan *pl, int i) { return pl->scal + i; }
+double *rc_mean(mgsr_plan *pl, int l) { return pl->scal + SC_LEVEL0 + 4 * l; }
+double *d_mean(mgsr_plan *pl, int l) { return pl->scal + SC_LEVEL0 + 4 * l + 1; }
+double *sr_mean(mgsr_plan *pl, int l) { return pl->scal + SC_LEVEL0 + 4 * l + 2; }
+void *slot(mgsr_plan *pl, int k) { return static_cast<char *>(pl->red) + k * kRedSlotBytes; }
+
+int ladder(int64_t n, int n_step, int r_min, std::vector<int> &sides) {
+    if (n <= r_min) { set_error("fine side must exceed r_min"); return MGSR_E_LADDER; }
+    sides.assign(1, int(n));
+    while (sides.back() > r_min) {
+        int nxt = sides.back() >> n_step;
+        if (nxt < r_min) nxt = r_min;
+        int ratio = sides.back() / nxt;
+        if (nxt * ratio != sides.back() || !(ratio == 2 || ratio == 4 || ratio == 8 || ratio == 16)) {
+            set_error("no valid ladder from " + std::to_string(n) + " to r_min " + std::to_string(r_min) +
+                      " with step 2^" + std::to_string(n_step));
+            return MGSR_E_LADDER;
+        }
+        sides.push_back(nxt);
+    }
+    return MGSR_OK;
+}
+
+// Prolong the correction of level l (buffer d[l], or the coarsest GS result)
+// into level l-1 and add to `base` (level l-1 GS result with mean *bshift):
+// out = (base - *bshift) + P(corr).  mean_out (optional) = mean(out).
+int prolong_into(mgsr_plan *pl, int l, int use_sr, const double *base, const double *bshift, double *out,
+                 double *mean_out, cudaStream_t st) {
+    const int nc = pl->sides[l], s = pl->sides[l - 1] / pl->sides[l];
+    const double *corr = pl->d[l];
+    const bool sr = use_sr && ((pl->cfg.sr_level_mask >> (l - 1)) & 1u);
+    if (!sr) return launch_prolong_add(corr, nc, s, base, bshift, out, mean_out, slot(pl, 3), st);
+    int r = launch_sr_prolong(pl->gen, corr, nullptr, nc, s, pl->cfg.p_min, pl->cfg.p_max, pl->cfg.precision,
+                              pl->srbuf, sr_mean(pl, l), pl->srws, pl->srws_bytes, slot(pl, 2), st);
+    if (r) return r;
+    const int64_t nf = int64_t(nc) * s;
+    return launch_add2(base, bshift, pl->srbuf, sr_mean(pl, l), out, nf * nf, mean_out, slot(pl, 3), st);
+}
+
+// correction(rhs_l, l) of solver.py:181-190; leaves the gauge-fixed result in d[l].
+int correction(mgsr_plan *pl, int l, int use_sr, cudaStream_t st) {
+    const int L = int(pl->sides.size());
+    const int n = pl->sides[l];
+    const double h = 2.0 * M_PI / n;
+    FSrc fs{pl->rc[l], rc_mean(pl, l), 0.5};
+    int r;
+    if (l == L - 1) {
+        r = launch_gs(nullptr, pl->d[l], pl->tmp, fs, n, h * h, pl->cfg.coarse_sweeps, 1, nullptr, nullptr,
+                      d_mean(pl, l), pl->red, st);
+        if (r) return r;
+        if (n > kSmallN) return launch_affine(pl->d[l], pl->d[l], int64_t(n) * n, d_mean(pl, l), 1.0, st);
+        return MGSR_OK;
+    }
+    const int s = n / pl->sides[l + 1];
+    const bool fuse_rc = (s == 2);
+    r = launch_gs(nullptr, pl->d[l], pl->tmp, fs, n, h * h, pl->cfg.n_smooth, 1, fuse_rc ? pl->rc[l + 1] : nullptr,
+                  fuse_rc ? rc_mean(pl, l + 1) : nullptr, d_mean(pl, l), pl->red, st);
+    if (r) return r;
+    if (!fuse_rc && (r = launch_res_restrict(pl->d[l], fs, n, s, pl->rc[l + 1], rc_mean(pl, l + 1), slot(pl, 1), st)))
+        return r;
+    if ((r = correction(pl, l + 1, use_sr, st))) return r;
+    // d[l] = (d[l] - d_mean) + up  (in place: elementwise)
+    const double *bshift = n <= kSmallN ? nullptr : d_mean(pl, l);
+    return prolong_into(pl, l + 1, use_sr, pl->d[l], bshift, pl->d[l], nullptr, st);
+}
+
+int record_vcycle(mgsr_plan *pl, double *p, const double *f, int use_sr, cudaStream_t st) {
+    const int n = pl->sides[0];
+    const double h = 2.0 * M_PI / n;
+    const int s0 = n / pl->sides[1];
+    FSrc fs{f, nullptr, 1.0};
+    int r = launch_gs(p, pl->S, pl->tmp, fs, n, h * h, pl->cfg.n_smooth, 0, s0 == 2 ? pl->rc[1] : nullptr,
+                      s0 == 2 ? rc_mean(pl, 1) : nullptr, sc(pl, SC_S_MEAN), pl->red, st);
+    if (r) return r;
+    if (s0 != 2 && (r = launch_res_restrict(pl->S, fs, n, s0, pl->rc[1], rc_mean(pl, 1), slot(pl, 1), st))) return r;
+    if ((r = correction(pl, 1, use_sr, st))) return r;
+    const double *bshift = n <= kSmallN ? nullptr : sc(pl, SC_S_MEAN);
+    if ((r = prolong_into(pl, 1, use_sr, pl->S, bshift, pl->S, sc(pl, SC_OUT_MEAN), st))) return r;
+    return launch_finalize(pl->S, sc(pl, SC_OUT_MEAN), p, fs, n, sc(pl, SC_ACC), sc(pl, SC_STATS), slot(pl, 0), st);
+}
+
+}  // namespace
+
+extern "C" int mgsr_plan_create(const mgsr_plan_config *cfg, const mgsr_gen *gen, mgsr_plan **out) {
+    if (!cfg || !out) { set_error("bad argument"); return MGSR_E_BAD_ARG; }
+    if (cfg->n_smooth < 1 || cfg->coarse_sweeps < 1) { set_error("sweep counts must be positive"); return MGSR_E_BAD_ARG; }
+    if (cfg->r_min < 2 || cfg->r_min % 2) { set_error("r_min must be an even integer >= 2"); return MGSR_E_BAD_ARG; }
+    mgsr_plan *pl = new mgsr_plan();
+    pl->cfg = *cfg;
+    pl->gen = gen;
+    int r = ladder(cfg->n, cfg->n_step, cfg->r_min, pl->sides);
+    if (r) { delete pl; return r; }
+    const int L = int(pl->sides.size());
+    if (L > 24) { delete pl; set_error("ladder too deep"); return MGSR_E_LADDER; }
+    const int64_t n = cfg->n;
+    // SR needs every prolongation's coarse side >= 6 and even
+    bool any_sr = false;
+    int64_t sr_ws = 0, sr_fine_max = 0;
+    if (gen) {
+        for (int l = 1; l < L; ++l) {
+            if (!((cfg->sr_level_mask >> (l - 1)) & 1u)) continue;
+            int nc = pl->sides[l], s = pl->sides[l - 1] / nc;
+            if (nc < 6 || nc % 2) continue;
+            any_sr = true;
+            int64_t w = int64_t(sr_workspace_bytes(nc, s, cfg->precision));
+            if (w > sr_ws) sr_ws = w;
+            int64_t nf = int64_t(nc) * s;
+            if (nf * nf > sr_fine_max) sr_fine_max = nf * nf;
+        }
+    }
+    size_t bytes = 4096 + 4 * kRedSlotBytes;          // scalars + slots
+    bytes += sizeof(double) * size_t(n) * n * 2;      // S, tmp
+    for (int l = 1; l < L; ++l) bytes += 2 * sizeof(double) * size_t(pl->sides[l]) * pl->sides[l];
+    if (any_sr) bytes += sizeof(double) * size_t(sr_fine_max) + size_t(sr_ws) + 256;
+    cudaError_t e = cudaMalloc(&pl->mem, bytes);
+    if (e != cudaSuccess) { delete pl; set_error(std::string("plan alloc: ") + cudaGetErrorString(e)); return MGSR_E_CUDA; }
+    cudaMemset(pl->mem, 0, 4096 + 4 * kRedSlotBytes);
+    pl->mem_bytes = bytes;
+    char *m = static_cast<char *>(pl->mem);
+    pl->scal = reinterpret_cast<double *>(m);
+    m += 4096;
+    pl->red = m;
+    m += 4 * kRedSlotBytes;
+    pl->S = reinterpret_cast<double *>(m); m += sizeof(double) * size_t(n) * n;
+    pl->tmp = reinterpret_cast<double *>(m); m += sizeof(double) * size_t(n) * n;
+    pl->rc.assign(L, nullptr);
+    pl->d.assign(L, nullptr);
+    for (int l = 1; l < L; ++l) {
+        size_t c = size_t(pl->sides[l]) * pl->sides[l];
+        pl->rc[l] = reinterpret_cast<double *>(m); m += sizeof(double) * c;
+        pl->d[l] = reinterpret_cast<double *>(m); m += sizeof(double) * c;
+    }
+    if (any_sr) {
+        pl->srbuf = reinterpret_cast<double *>(m); m += sizeof(double) * size_t(sr_fine_max);
+        m = reinterpret_cast<char *>((reinterpret_cast<uintptr_t>(m) + 255) & ~uintptr_t(255));
+        pl->srws = m;
+        pl->srws_bytes = size_t(sr_ws);
+    }
+    e = cudaStreamCreateWithFlags(&pl->cap, cudaStreamNonBlocking);
+    if (e != cudaSuccess) { mgsr_plan_destroy(pl); set_error("stream create failed"); return MGSR_E_CUDA; }
+    *out = pl;
+    return MGSR_OK;
+}
+
+extern "C" int mgsr_plan_destroy(mgsr_plan *pl) {
+    if (!pl) return MGSR_OK;
+    for (auto &kv : pl->graphs) cudaGraphExecDestroy(kv.second);
+    if (pl->cap) cudaStreamDestroy(pl->cap);
+    if (pl->mem) cudaFree(pl->mem);
+    delete pl;
+    return MGSR_OK;
+}
+
+extern "C" int32_t mgsr_plan_levels(const mgsr_plan *pl, int64_t *sides_out) {
+    if (!pl) return 0;
+    for (size_t i = 0; i < pl->sides.size() && sides_out; ++i) sides_out[i] = pl->sides[i];
+    return int32_t(pl->sides.size());
+}
+
+extern "C" int mgsr_plan_vcycle(mgsr_plan *pl, double *p, const double *f, int32_t use_sr, double *stats_dev,
+                                void *stream) {
+    if (!pl || !p || !f) { set_error("bad argument"); return MGSR_E_BAD_ARG; }
+    if (use_sr && !pl->gen) { set_error("SR prolongation requires generator weights"); return MGSR_E_BAD_ARG; }
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    auto key = std::make_tuple(p, f, int(use_sr != 0));
+    auto it = pl->graphs.find(key);
+    if (it == pl->graphs.end()) {
+        // capture on the plan's own stream, then instantiate once
+        MGSR_CUDA_TRY(cudaStreamSynchronize(st));
+        MGSR_CUDA_TRY(cudaStreamBeginCapture(pl->cap, cudaStreamCaptureModeRelaxed));
+        int r = record_vcycle(pl, p, f, use_sr != 0, pl->cap);
+        cudaGraph_t graph = nullptr;
+        cudaError_t e = cudaStreamEndCapture(pl->cap, &graph);
+        if (r) { if (graph) cudaGraphDestroy(graph); return r; }
+        if (e != cudaSuccess) { set_error(std::string("graph capture: ") + cudaGetErrorString(e)); return MGSR_E_CUDA; }
+        cudaGraphExec_t exec = nullptr;
+        e = cudaGraphInstantiate(&exec, graph, 0);
+        cudaGraphDestroy(graph);
+        if (e != cudaSuccess) { set_error(std::string("graph instantiate: ") + cudaGetErrorString(e)); return MGSR_E_CUDA; }
+        it = pl->graphs.emplace(key, exec).first;
+    }
+    MGSR_CUDA_TRY(cudaGraphLaunch(it->second, st));
+    if (stats_dev)
+        MGSR_CUDA_TRY(cudaMemcpyAsync(stats_dev, sc(pl, SC_STATS), 2 * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    return MGSR_OK;
+}

@@ -1,0 +1,23 @@
+// Internal launch helpers shared between the stencil kernels and the V-cycle plan.
+#pragma once
+#include "common.cuh"
+
+namespace mgsr {
+
+constexpr int kTbTX = 64, kTbTY = 32, kTbThreads = 256, kTbMaxK = 4;
+constexpr int kSmallN = 64;
+
+int grid_for(int64_t work, int threads);
+int launch_gs(const double *p_in, double *p_out, double *tmp, FSrc fs, int n, double h2, int sweeps,
+              int zero_init, double *rc, double *rc_mean, double *mean_out, void *red_ws, cudaStream_t st);
+int launch_prolong_add(const double *c, int nc, int s, const double *base, const double *bshift, double *out,
+                       double *mean_out, void *red_slot, cudaStream_t st);
+int launch_add2(const double *base, const double *bshift, const double *up, const double *ushift, double *out,
+                int64_t count, double *mean_out, void *red_slot, cudaStream_t st);
+int launch_res_restrict(const double *p, FSrc fs, int n, int s, double *rc, double *rc_mean, void *red_slot,
+                        cudaStream_t st);
+int launch_finalize(const double *out, const double *mean_ptr, double *p, FSrc fs, int n, double *acc3,
+                    double *stats2, void *red_slot, cudaStream_t st);
+int launch_affine(const double *a, double *out, int64_t count, const double *shift, double scale, cudaStream_t st);
+
+}  // namespace mgsr

@@ -1,0 +1,79 @@
+"""GPU parity: generator inference and windowed SR prolongation.
+
+Bar (north_star): GAN-prolonged fields within 1e-2 relative L2 of the
+reference's generator; the fp32 CUDA-core path is held much tighter.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import rel, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+
+def test_generator_forward_golden(cuda, golden):
+    from paper_2403_07936_b200 import srmodel
+    w1 = srmodel.random_weights(1, 3)
+    for key in ("6", "8"):
+        y = srmodel.generator_forward(w1, golden[f"gen_b1_x{key}"])
+        assert rel(y, golden[f"gen_b1_y{key}"]) < 1e-5
+    y = srmodel.generator_forward(srmodel.random_weights(8, 0), golden["gen_b8_x6"])
+    assert rel(y, golden["gen_b8_y6"]) < 1e-3   # saturated tanh, fp32 vs fp64
+
+
+def test_generator_nn_weights_exact(cuda):
+    """Crafted weights = exact x2 nearest-neighbour upsampler (srmodel.py:361-387)."""
+    from paper_2403_07936_b200 import srmodel
+    x = np.random.default_rng(0).uniform(-1, 1, (3, 6, 6))
+    y = srmodel.generator_forward(srmodel.make_nearest_neighbor_weights(), x)
+    exp = np.repeat(np.repeat(x, 2, axis=1), 2, axis=2)
+    assert np.abs(y - exp).max() < 1e-6
+
+
+def test_sr_prolong_fp32_golden(cuda, golden):
+    from paper_2403_07936_b200 import srmodel
+    from paper_2403_07936_b200.grid import Grid, NormBounds
+    w2 = srmodel.random_weights(2, 0)
+    out = srmodel.sr_prolong(Grid(golden["sr_c16"]), w2, NormBounds(), 2)
+    assert rel_l2(out.data, golden["sr2_out"]) < 1e-4
+    out = srmodel.sr_prolong(Grid(golden["sr_c12"]), w2, NormBounds(), 4)
+    assert rel_l2(out.data, golden["sr4_out"]) < 1e-4
+    out = srmodel.sr_prolong(Grid(golden["sr_c16"]), srmodel.make_nearest_neighbor_weights(), NormBounds(), 2)
+    assert rel(out.data, golden["srnn2_out"]) < 1e-5
+
+
+@pytest.mark.parametrize("s", [8, 16])
+def test_sr_prolong_two_pass_ratios(cuda, orc, s):
+    from paper_2403_07936_b200 import srmodel
+    from paper_2403_07936_b200.grid import Grid, NormBounds
+    from conftest import ROOT  # noqa: F401
+    c = orc.scale_to_p_rms(orc.sine_modes_rhs(12, 4), 1e-4)[:12, :12]
+    c = c - c.mean()
+    w = srmodel.random_weights(1, 2)
+    got = srmodel.sr_prolong(Grid(c), w, NormBounds(), s).data
+    exp = orc.sr_prolong(c, orc.random_weights(1, 2), orc.Bounds(), s)
+    assert rel_l2(got, exp) < 1e-3
+
+
+def test_sr_prolong_fp32_vs_oracle_256(cuda, orc):
+    """Full field at n_c = 128 (3844 windows), trained-like in-band input."""
+    from paper_2403_07936_b200 import srmodel
+    from paper_2403_07936_b200.grid import Grid, NormBounds
+    c = orc.scale_to_p_rms(orc.sine_modes_rhs(128, 5), 1e-4)
+    w = srmodel.random_weights(8, 0)
+    got = srmodel.sr_prolong(Grid(c), w, NormBounds(), 2).data
+    exp = orc.sr_prolong(c, orc.quantize_f32(orc.random_weights(8, 0)), orc.Bounds(), 2)
+    assert rel_l2(got, exp) < 1e-3
+
+
+def test_sr_ratio_errors(cuda):
+    from paper_2403_07936_b200 import srmodel
+    from paper_2403_07936_b200.grid import Grid, NormBounds
+    w = srmodel.random_weights(1, 0)
+    with pytest.raises(ValueError, match="unsupported SR ratio"):
+        srmodel.sr_prolong(Grid(np.ones((8, 8))), w, NormBounds(), 3)
+    with pytest.raises(ValueError, match=">= 6"):
+        srmodel.sr_prolong(Grid(np.ones((4, 4))), w, NormBounds(), 2)

@@ -1,0 +1,123 @@
+"""GPU parity: the graph-launched V-cycle and the solve loop vs golden / oracle.
+
+Bars (north_star / SURVEY §8(d)): one spline V-cycle within 1e-12 relative;
+residual-norm histories matching (<= 1e-12 early, <= 1e-6 late -- the spread
+the reference shows against itself), the same iteration count to tol, and
+identical operator/latch sequences in hybrid mode.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import rel, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+
+def cfg_(**kw):
+    from paper_2403_07936_b200.solver import RunConfig
+    base = dict(N_step=1, r_min=8, N_smooth=2)
+    base.update(kw)
+    return RunConfig(**base)
+
+
+def test_v_cycle_spline_golden(cuda, golden):
+    from paper_2403_07936_b200 import solver
+    from paper_2403_07936_b200.grid import Grid
+    from paper_2403_07936_b200.smoother import PoissonProblem
+    out = solver.v_cycle(Grid(golden["vc_p"]), PoissonProblem(Grid(golden["vc_f"])), cfg_(N_smooth_pre=2), "spline")
+    assert rel(out.data, golden["vc_spline_out"]) < 1e-12
+
+
+@pytest.mark.parametrize("n,nsm", [(256, 2), (1024, 2), (1024, 5), (2048, 3), (4096, 2)])
+def test_v_cycle_spline_large_vs_oracle(cuda, orc, n, nsm):
+    from paper_2403_07936_b200 import solver
+    from paper_2403_07936_b200.grid import Grid
+    from paper_2403_07936_b200.smoother import PoissonProblem
+    f = orc.sine_modes_rhs(n, 1)
+    p0 = orc.initial_iterate(n, orc.Config())
+    exp = orc.v_cycle(p0, f, orc.Config(N_step=1, r_min=8, N_smooth=nsm), "spline")
+    got = solver.v_cycle(Grid(p0), PoissonProblem(Grid(f)), cfg_(N_smooth=nsm), "spline").data
+    assert rel(got, exp) < 1e-12
+
+
+def test_v_cycle_nstep4_ladder(cuda, orc):
+    """Paper-fiducial N_step = 4 ladder (192 -> 12, ratio 16)."""
+    from paper_2403_07936_b200 import solver
+    from paper_2403_07936_b200.grid import Grid
+    from paper_2403_07936_b200.smoother import PoissonProblem
+    f = orc.sine_modes_rhs(192, 2)
+    p0 = orc.initial_iterate(192, orc.Config())
+    exp = orc.v_cycle(p0, f, orc.Config(N_step=4, r_min=12, N_smooth=4), "spline")
+    got = solver.v_cycle(Grid(p0), PoissonProblem(Grid(f)), cfg_(N_step=4, r_min=12, N_smooth=4), "spline").data
+    assert rel(got, exp) < 1e-12
+
+
+def test_solve_spline_history_golden(cuda, golden):
+    from paper_2403_07936_b200 import solver
+    from paper_2403_07936_b200.grid import Grid
+    from paper_2403_07936_b200.smoother import PoissonProblem
+    p, log = solver.solve(PoissonProblem(Grid(golden["solve64_f"])), cfg_())
+    ref = golden["solve64_log"]
+    assert log.iterations == len(ref)
+    got = np.array([[r.diff_norm, r.residual_norm] for r in log.records])
+    assert rel_l2(got[:2], ref[:2]) < 1e-12
+    assert (np.abs(got - ref) / ref).max() < 1e-6
+    assert np.abs(p.data - golden["solve64_p"]).max() < 1e-13
+
+
+def test_solve_spline_1024_matches_oracle(cuda, orc):
+    from paper_2403_07936_b200 import solver
+    from paper_2403_07936_b200.grid import Grid
+    from paper_2403_07936_b200.smoother import PoissonProblem
+    f = orc.sine_modes_rhs(1024, 0)
+    p_ref, log_ref = orc.solve(f, orc.Config(N_step=1, r_min=8, N_smooth=2))
+    p, log = solver.solve(PoissonProblem(Grid(f)), cfg_())
+    assert log.iterations == log_ref.iterations
+    a = np.array([[r.diff_norm, r.residual_norm] for r in log.records])
+    b = np.array([[r.diff_norm, r.residual_norm] for r in log_ref.records])
+    assert (np.abs(a - b) / b).max() < 1e-6
+    assert rel(p.data, p_ref) < 1e-9
+
+
+def test_solve_matches_discrete_oracle(cuda, orc):
+    from paper_2403_07936_b200 import solver
+    from paper_2403_07936_b200.grid import Grid
+    from paper_2403_07936_b200.smoother import PoissonProblem
+    f = orc.sine_modes_rhs(256, 3)
+    p, log = solver.solve(PoissonProblem(Grid(f)), cfg_())
+    assert log.converged(1e-10)
+    assert np.sqrt(np.mean((p.data - orc.spectral_solution(f)) ** 2)) < 1e-8
+
+
+def test_solve_hybrid_schedule_golden(cuda, golden, golden_meta):
+    """Latched hybrid: identical operator and latch sequences, same iteration count."""
+    from paper_2403_07936_b200 import solver, srmodel
+    from paper_2403_07936_b200.grid import Grid
+    from paper_2403_07936_b200.smoother import PoissonProblem
+    cfg = cfg_(mode="hybrid", N_GAN=1.0, S_thres=2.27e-4)
+    p, log = solver.solve(PoissonProblem(Grid(golden["hyb64_f"])), cfg, srmodel.random_weights(1, 0))
+    assert [r.operator for r in log.records] == golden_meta["hyb64_ops"]
+    assert [r.switch_latched for r in log.records] == golden_meta["hyb64_latched"]
+    got = np.array([[r.diff_norm, r.residual_norm] for r in log.records])
+    assert rel_l2(got, golden["hyb64_log"]) < 1e-4
+
+
+def test_v_cycle_sr_golden(cuda, golden):
+    from paper_2403_07936_b200 import solver, srmodel
+    from paper_2403_07936_b200.grid import Grid
+    from paper_2403_07936_b200.smoother import PoissonProblem
+    out = solver.v_cycle(Grid(golden["vc_sr_p"]), PoissonProblem(Grid(golden["vc_sr_f"])), cfg_(N_smooth_pre=2),
+                         "sr", srmodel.random_weights(2, 0))
+    assert rel_l2(out.data, golden["vc_sr_out"]) < 1e-4
+
+
+def test_sr_requires_weights(cuda):
+    from paper_2403_07936_b200 import solver
+    from paper_2403_07936_b200.grid import Grid
+    from paper_2403_07936_b200.smoother import PoissonProblem
+    f = np.zeros((32, 32))
+    with pytest.raises(ValueError, match="weights"):
+        solver.v_cycle(Grid(f), PoissonProblem(Grid(f)), cfg_(), "sr")

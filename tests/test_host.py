@@ -1,0 +1,161 @@
+"""CPU: host logic of the package and the C ABI boundary (no compute calls)."""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+import struct
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+
+
+def header_symbols() -> list[str]:
+    text = open(os.path.join(ROOT, "include", "mgsr_b200.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(mgsr_[a-z_0-9]+)\s*\(", text)))
+
+
+def test_library_loads_and_exports_every_header_symbol():
+    from paper_2403_07936_b200 import _lib
+    lib = _lib.load()
+    syms = header_symbols()
+    assert len(syms) >= 17
+    for name in syms:
+        assert hasattr(lib, name), name
+        assert name in _lib.SIGNATURES, f"{name} not bound in _lib.SIGNATURES"
+    assert lib.mgsr_version().startswith(b"mgsr_b200")
+    assert lib.mgsr_workspace_bytes(4096) > 0
+
+
+def test_plan_config_layout_matches_header():
+    from paper_2403_07936_b200 import _lib
+    # int64 n; 4 x int32; 2 x double; int32 precision; uint32 mask
+    assert ctypes.sizeof(_lib.PlanConfig) == 8 + 16 + 16 + 8
+
+
+def test_runconfig_mirrors_reference():
+    from paper_2403_07936_b200.solver import RunConfig
+    c = RunConfig()
+    assert (c.N_iter, c.r_min, c.N_smooth_pre, c.N_smooth, c.N_step, c.N_GAN, c.S_thres, c.tol, c.mode,
+            c.coarse_sweeps) == (300, 12, 10, 20, 4, 1.0, 1e-10, 1e-10, "spline", 10)
+    with pytest.raises(ValueError, match="unknown config keys"):
+        RunConfig.from_json('{"N_iter": 3, "bogus": 1}')
+    with pytest.raises(ValueError, match="must be one of"):
+        RunConfig(mode="gan")
+    with pytest.raises(ValueError, match="even integer"):
+        RunConfig(r_min=7)
+    assert RunConfig.from_json(RunConfig(N_iter=7).to_json()) == RunConfig(N_iter=7)
+
+
+@pytest.mark.parametrize("n,step,rmin,expected", [
+    (4096, 1, 8, [4096, 2048, 1024, 512, 256, 128, 64, 32, 16, 8]),
+    (192, 4, 12, [192, 12]),
+    (3072, 4, 12, [3072, 192, 12]),
+    (64, 1, 8, [64, 32, 16, 8]),
+])
+def test_level_sides(n, step, rmin, expected, orc):
+    from paper_2403_07936_b200.solver import level_sides
+    assert level_sides(n, step, rmin) == expected == orc.level_sides(n, step, rmin)
+
+
+def test_level_sides_errors():
+    from paper_2403_07936_b200.solver import level_sides
+    with pytest.raises(ValueError, match="must exceed"):
+        level_sides(12, 1, 12)
+    with pytest.raises(ValueError, match="no valid ladder"):
+        level_sides(100, 1, 12)
+
+
+def test_schedule_matches_oracle(orc):
+    from paper_2403_07936_b200.solver import schedule_operator
+    for n_gan in (0.25, 0.5, 1.0, 2.0, 3.0, 7.6):
+        for latched in (False, True):
+            for it in range(1, 30):
+                assert schedule_operator(it, n_gan, latched) == orc.schedule_operator(it, n_gan, latched)
+    with pytest.raises(ValueError):
+        schedule_operator(0, 1.0, False)
+
+
+def test_weights_roundtrip_and_errors(tmp_path):
+    from paper_2403_07936_b200 import srmodel
+    w = srmodel.random_weights(2, 5)
+    path = tmp_path / "w.mgsr"
+    srmodel.save_weights(w, path)
+    back = srmodel.load_weights(path)
+    for k, v in w.tensors.items():
+        assert np.array_equal(back.tensors[k], v.astype(np.float32).astype(np.float64))
+    nn = srmodel.make_nearest_neighbor_weights()
+    srmodel.save_weights(nn, tmp_path / "nn.mgsr")
+    assert srmodel.load_weights(tmp_path / "nn.mgsr").tanh_scale == 1e6
+    blob = path.read_bytes()
+    (tmp_path / "bad.mgsr").write_bytes(b"NOPE" + blob[4:])
+    with pytest.raises(srmodel.WeightsMagicError, match="bad magic"):
+        srmodel.load_weights(tmp_path / "bad.mgsr")
+    (tmp_path / "trunc.mgsr").write_bytes(blob[: len(blob) // 2])
+    with pytest.raises(srmodel.WeightsTruncatedError, match="bytes"):
+        srmodel.load_weights(tmp_path / "trunc.mgsr")
+    (tmp_path / "trail.mgsr").write_bytes(blob + b"\0")
+    with pytest.raises(srmodel.WeightsShapeError, match="trailing"):
+        srmodel.load_weights(tmp_path / "trail.mgsr")
+    ver = bytearray(blob)
+    ver[4:8] = struct.pack("<I", 9)
+    (tmp_path / "ver.mgsr").write_bytes(bytes(ver))
+    with pytest.raises(srmodel.WeightsVersionError, match="version"):
+        srmodel.load_weights(tmp_path / "ver.mgsr")
+    for sub in (srmodel.WeightsMagicError, srmodel.WeightsVersionError, srmodel.WeightsShapeError,
+                srmodel.WeightsTruncatedError):
+        assert issubclass(sub, srmodel.WeightsError) and issubclass(sub, ValueError)
+
+
+def test_random_weights_match_oracle(orc):
+    from paper_2403_07936_b200 import srmodel
+    w = srmodel.random_weights(8, 0)
+    o = orc.random_weights(8, 0)
+    for k in o.tensors:
+        assert np.array_equal(w.tensors[k], o.tensors[k])
+
+
+def test_window_plan_matches_oracle(orc):
+    from paper_2403_07936_b200 import srmodel
+    for n in (6, 8, 16, 30):
+        mine = [(a, b, s1.start, s1.stop, s2.start, s2.stop) for a, b, s1, s2 in srmodel.stitch_plan(n)]
+        assert mine == orc.stitch_plan(n)
+    with pytest.raises(ValueError, match=">= 6"):
+        srmodel.window_positions(4)
+    with pytest.raises(ValueError, match="even"):
+        srmodel.window_positions(7)
+
+
+def test_backend_selector_rejects_unknown(monkeypatch):
+    import importlib
+    import subprocess
+    import sys
+    code = "import paper_2403_07936_b200.kernels"
+    env = dict(os.environ, MGSR_BACKEND="numpy", PYTHONPATH=ROOT)
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
+    assert r.returncode != 0 and "MGSR_BACKEND" in r.stderr
+    from paper_2403_07936_b200 import kernels
+    assert kernels.active_backend() == "cuda"
+
+
+def test_no_cpu_fallback_without_gpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_2403_07936_b200 import kernels
+    p = np.zeros((8, 8))
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        kernels.gs_sweeps(p, p.copy(), 1.0, 1)
+
+
+def test_product_package_never_imports_oracle():
+    pkg = os.path.join(ROOT, "paper_2403_07936_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh")):
+                text = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in text and "from oracle" not in text, f
