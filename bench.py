@@ -1,0 +1,452 @@
+#!/usr/bin/env python
+"""Benchmark: V-cycles/s (and GUpdates/s) of the 4096^2 V-cycle with GAN
+prolongation on B200 -- BASELINE.json config 4.
+
+Workload (``config.workload``): periodic 4096^2 grid, N_step=1 ladder
+4096 -> 8 (10 levels), N_smooth=2, coarse_sweeps=10, SR ("GAN") prolongation
+at the 3 finest prolongations (2048->4096, 1024->2048, 512->1024; 1,369,100
+windows of 6x6), Keys spline below; generator = reference architecture, B=8
+residual blocks, seeded He-normal weights (``random_weights(8, 0)``; the
+reference's trained artifacts are absent), bf16 tcgen05 operands with fp32
+accumulation (tf32 head, fp32 tail); fp64 stencils.  RHS: seeded Gaussian
+random field k^-5/3 + 32 blobs scaled to p_rms = 1e-4 (in the SR band).
+A step = one V-cycle + the solve loop's logging pass (diff and residual
+norms), one CUDA-graph launch.  Inputs (134 MB per fp64 grid) exceed the
+126 MB L2, so no explicit flush is needed.
+
+Multi-GPU: the path does not shard (one grid per GPU) ->
+replicas only: each rank runs its own seeded replica, value = sum over ranks
+of cycles / max-over-ranks time ("scaling": "weak").
+
+``--impl reference`` times the reference's own CPU implementation (compiled
+from its sources into oracle/_ref) on a bounded sample per step and projects
+the same metric.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "V-cycles/s and GUpdates/s at 4096² (GAN prolong) on 1 B200; % HBM / tensor roofline"
+UNIT = "V-cycles/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="mine", choices=["mine", "reference"])
+    ap.add_argument("--n", type=int, default=4096)
+    ap.add_argument("--mode", default="gan", choices=["gan", "spline"])
+    ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32"])
+    ap.add_argument("--sr-levels", type=int, default=3)
+    ap.add_argument("--blocks", type=int, default=8)
+    ap.add_argument("--n-smooth", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# algorithmic work model; credits only executed work
+
+def window_macs(blocks: int, kept_px: int) -> int:
+    head = 36 * 64 * 81            # 3 identical input channels folded -> 81 taps executed
+    body = 2 * blocks * 36 * 64 * 576
+    post = 36 * 64 * 576
+    up = 36 * 256 * 576
+    tail = kept_px * 3 * 64 * 81   # tail evaluated only at the stitched (kept) pixels
+    return head + body + post + up + tail
+
+
+def pass_flops(nc: int, blocks: int) -> float:
+    """FLOPs of one ratio-2 SR pass on an nc x nc coarse grid (stitch_plan bands)."""
+    npos = nc // 2 - 2
+    tot = 0
+    for side_i in range(npos):
+        ri = 8 if side_i in (0, npos - 1) else 4
+        if npos == 1:
+            ri = 12
+        for side_j in range(npos):
+            rj = 8 if side_j in (0, npos - 1) else 4
+            if npos == 1:
+                rj = 12
+            tot += window_macs(blocks, ri * rj)
+    return 2.0 * tot
+
+
+def pass_flops_fast(nc: int, blocks: int) -> float:
+    npos = nc // 2 - 2
+    inner = max(npos - 2, 0)
+    n_int, n_edge, n_corner = inner * inner, 4 * inner, 4
+    return 2.0 * (n_int * window_macs(blocks, 16) + n_edge * window_macs(blocks, 32)
+                  + n_corner * window_macs(blocks, 64))
+
+
+def gs_bytes(n: int, fused_rc: bool = True) -> float:
+    """Compulsory bytes of the finest temporally blocked GS launch: read p, f; write p
+    (+ the injected coarse residual)."""
+    return n * n * (24.0 + (2.0 if fused_rc else 0.0))
+
+
+# ---------------------------------------------------------------------------
+# clocks sampling during the timed region
+
+class Clocks:
+    def __init__(self, index: int = 0):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = sorted(float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit())
+        mx = max(float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[4 + i].lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+def load_traffic(mode):
+    """ncu dram bytes per launch of the dominant kernel, if a capture summary is committed."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh).get(mode)
+    except OSError:
+        return None
+
+
+# ---------------------------------------------------------------------------
+# workload
+
+def make_inputs(n: int, seed: int, mode: str):
+    from paper_2403_07936_b200 import datagen
+    f = datagen.grf_blobs_rhs(n, seed=seed, kmax=min(256.0, n / 4))
+    f = datagen.scale_to_p_rms(f, 1e-4)
+    rng = __import__("numpy").random.default_rng(seed)
+    p0 = rng.uniform(-1e-4, 1e-4, size=(n, n))
+    return f - f.mean(), p0 - p0.mean()
+
+
+def run_mine(args, rank: int, world: int, dist):
+    import numpy as np
+    import torch
+
+    from paper_2403_07936_b200 import _lib, ops, srmodel
+    from paper_2403_07936_b200.solver import RunConfig, VCyclePlan
+
+    torch.cuda.set_device(rank % max(torch.cuda.device_count(), 1))
+    dev = torch.device("cuda")
+    n = args.n
+    cfg = RunConfig(N_step=1, r_min=8, N_smooth=args.n_smooth, coarse_sweeps=10)
+    weights = srmodel.random_weights(args.blocks, 0) if args.mode == "gan" else None
+    op = "sr" if args.mode == "gan" else "spline"
+    plan = VCyclePlan(n, cfg, weights, precision=args.precision, sr_levels=args.sr_levels)
+    f_np, p_np = make_inputs(n, 1000 + rank, args.mode)
+    f = torch.from_numpy(f_np).to(dev)
+    p = torch.from_numpy(p_np).to(dev)
+    lib = _lib.load()
+
+    clk = Clocks(torch.cuda.current_device())
+    clk.__enter__()
+    for _ in range(args.warmup):
+        plan.cycle(p, f, op)
+    torch.cuda.synchronize()
+    kernels_per_cycle = int(lib.mgsr_plan_kernel_nodes(plan.handle, 1 if op == "sr" else 0))
+
+    # ---- device-resident timed region (also records in-graph kernel events) ----
+    _lib.check(lib.mgsr_plan_timing_enable(plan.handle, args.steps))
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t_wait = time.time()
+    while not clk.rows and time.time() - t_wait < 5.0:   # sampler running before the timed region
+        time.sleep(0.05)
+    clk.rows.clear()
+    if True:
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0.record(st)
+        for _ in range(args.steps):
+            plan.cycle(p, f, op)
+        e1.record(st)
+        torch.cuda.synchronize()
+        time.sleep(0.15)   # let the 100 ms sampler see the tail of the region
+        clk.__exit__()
+        if dist is not None:
+            dist.barrier()
+    ms_total = e0.elapsed_time(e1)
+    import ctypes
+    kms = (ctypes.c_double * 3)()
+    cnt = ctypes.c_int32()
+    _lib.check(lib.mgsr_plan_timing_read(plan.handle, kms, ctypes.byref(cnt)))
+    gen_ms, gs_ms, cyc_ms = float(kms[0]), float(kms[1]), float(kms[2])
+    stats = plan.stats.cpu().numpy()
+    if not np.all(np.isfinite(stats)):
+        raise RuntimeError(f"non-finite cycle statistics {stats}")
+
+    # ---- end to end through the C ABI with pinned host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        hp = torch.from_numpy(p_np).pin_memory()
+        hf = torch.from_numpy(f_np).pin_memory()
+        hout = torch.empty_like(hp).pin_memory()
+        hstats = torch.empty(2, dtype=torch.float64).pin_memory()
+        dp, df = torch.empty_like(p), torch.empty_like(f)
+        k2 = max(1, min(args.steps, 5))
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        e0.record(st)
+        for _ in range(k2):
+            dp.copy_(hp, non_blocking=True)
+            df.copy_(hf, non_blocking=True)
+            ops.vcycle_(dp, df, plan.handle, 1 if op == "sr" else 0, plan.stats)
+            hout.copy_(dp, non_blocking=True)
+            hstats.copy_(plan.stats, non_blocking=True)
+        e1.record(st)
+        torch.cuda.synchronize()
+        e2e_ms = e0.elapsed_time(e1)
+        e2e = (k2, e2e_ms, 2 * 8 * n * n, 8 * n * n + 16)
+
+    def gather_max(x):
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    ms_total = gather_max(ms_total)
+    if e2e is not None:
+        e2e = (e2e[0], gather_max(e2e[1]), e2e[2], e2e[3])
+    return dict(ms_total=ms_total, gen_ms=gen_ms, gs_ms=gs_ms, cyc_ms=cyc_ms, kernels=kernels_per_cycle,
+                e2e=e2e, clocks=clk.summary(), stats=stats.tolist())
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the reference compiled from its own sources (oracle/_ref)
+
+def cpu_reference_sample(n: int, blocks: int, windows: int, mode: str, sr_levels: int):
+    """Time the reference on a bounded sample and project V-cycles/s at n^2.
+    Returns (projected cycles/s, kind, sample description)."""
+    import numpy as np
+    import oracle
+    ref = oracle.import_ref()
+    kind = "reference"
+    if ref is None:
+        kind = "port"
+    if kind == "reference":
+        from mgsr import smoother, solver, srmodel
+        from mgsr.grid import Grid
+        w = srmodel.random_weights(blocks, 0)
+
+        def fwd(x):
+            return srmodel._forward_batch(w, x)
+
+        def spline_cycle(m):
+            f = _rhs(m)
+            cfg = solver.RunConfig(N_step=1, r_min=8, N_smooth=2)
+            p0 = np.zeros((m, m))
+            t0 = time.perf_counter()
+            solver.v_cycle(Grid(p0), smoother.PoissonProblem(Grid(f)), cfg, "spline")
+            return time.perf_counter() - t0
+    else:
+        from oracle import mgsr_oracle as orc
+        w = orc.random_weights(blocks, 0)
+
+        def fwd(x):
+            return orc.forward_batch(w, x)
+
+        def spline_cycle(m):
+            f = _rhs(m)
+            t0 = time.perf_counter()
+            orc.v_cycle(np.zeros((m, m)), f, orc.Config(N_step=1, r_min=8, N_smooth=2), "spline")
+            return time.perf_counter() - t0
+    m = min(n, 2048)
+    t_spline = spline_cycle(m) * (n * n) / (m * m)
+    t_sr = 0.0
+    nw_total = 0
+    if mode == "gan":
+        x = np.random.default_rng(0).uniform(-1, 1, (windows, 1, 6, 6)).repeat(3, axis=1)
+        t0 = time.perf_counter()
+        fwd(x)
+        t_win = (time.perf_counter() - t0) / windows
+        for lev in range(1, sr_levels + 1):
+            nc = n >> lev
+            nw_total += (nc // 2 - 2) ** 2
+        t_sr = t_win * nw_total
+    cyc = 1.0 / (t_spline + t_sr)
+    sample = (f"reference v_cycle(spline) at {m}^2 scaled by work to {n}^2"
+              + (f" + reference generator (B={blocks}) on {windows} windows, per-window cost x "
+                 f"{nw_total} windows (projected)" if mode == "gan" else ""))
+    return cyc, kind, sample
+
+
+def _rhs(m):
+    import numpy as np
+    x = 2 * np.pi * np.arange(m) / m
+    f = np.outer(np.sin(3 * x), np.sin(5 * x)) + 0.3 * np.outer(np.cos(2 * x), np.sin(x))
+    return f - f.mean()
+
+
+def run_reference_arm(args, rank, world):
+    if rank != 0:
+        return
+    ncpu = os.cpu_count() or 1
+    vals = []
+    kind, sample = "reference", ""
+    windows = 32 if args.mode == "gan" else 0
+    for i in range(args.warmup + args.steps):
+        cyc, kind, sample = cpu_reference_sample(args.n, args.blocks, max(windows, 1), args.mode, args.sr_levels)
+        if i >= args.warmup:
+            vals.append(cyc)
+    v = sum(vals) / len(vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / v, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(args),
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": ncpu, "kind": kind, "sample": sample},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gupdates_per_s": v * args.n * args.n / 1e9,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(args):
+    wl = (f"periodic {args.n}^2 Poisson V-cycle, N_step=1 ladder {args.n}->8, N_smooth={args.n_smooth}, "
+          f"coarse_sweeps=10, " + (f"SR prolongation at the {args.sr_levels} finest levels (B={args.blocks}, "
+                                   f"{args.precision} tcgen05 operands / fp32 accumulate), spline below"
+                                   if args.mode == "gan" else "spline prolongation at all levels"))
+    return {"workload": wl, "grid": args.n, "levels": len(_sides(args.n)), "mode": args.mode,
+            "precision": args.precision if args.mode == "gan" else "fp64",
+            "generator_blocks": args.blocks, "sr_levels": args.sr_levels if args.mode == "gan" else 0,
+            "parallelism": f"replicas x{args.gpus}", "l2": "inputs (134 MB/grid) exceed L2; no flush"}
+
+
+def _sides(n):
+    s = [n]
+    while s[-1] > 8:
+        s.append(s[-1] // 2)
+    return s
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "reference":
+        os.environ.setdefault("OPENBLAS_NUM_THREADS", str(os.cpu_count() or 1))
+        run_reference_arm(args, rank, world)
+        return
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as tdist
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        tdist.init_process_group("nccl")
+        dist = tdist
+    res = run_mine(args, rank, world, dist)
+    if rank == 0:
+        peaks, peak_kind = measured_peaks()
+        n = args.n
+        cyc_s = args.steps / (res["ms_total"] / 1e3) * world
+        if args.mode == "gan":
+            flops = pass_flops_fast(n // 2, args.blocks)
+            ach = flops / (res["gen_ms"] / 1e3) / 1e12 if res["gen_ms"] > 0 else 0.0
+            peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
+            roof = {"bound": "tensor", "kernel": "finest-level SR generator (2048->4096, "
+                                                 f"{(n // 4 - 2) ** 2} windows)",
+                    "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+                    "peak_kind": f"{peak_kind} bf16 sustained (kernel timed inside the cycle)",
+                    "algorithmic_flop_per_launch": flops, "launch_ms": res["gen_ms"],
+                    "traffic": load_traffic("gan")}
+        else:
+            b = gs_bytes(n)
+            ach = b / (res["gs_ms"] / 1e3) / 1e9 if res["gs_ms"] > 0 else 0.0
+            peak = peaks.get("hbm_gbs")
+            roof = {"bound": "hbm", "kernel": f"finest-level temporally blocked GS ({args.n_smooth} sweeps "
+                                              "+ fused residual injection)",
+                    "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                    "peak_kind": f"{peak_kind} HBM copy", "algorithmic_bytes_per_launch": b,
+                    "launch_ms": res["gs_ms"], "traffic": load_traffic("spline")}
+        line = {
+            "metric": METRIC, "value": cyc_s, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": res["ms_total"] / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64+bf16" if args.mode == "gan" else "f64",
+            "data": "synthetic (seeded GRF k^-5/3 + blobs RHS; seeded He-init generator weights)",
+            "config": workload_config(args), "gupdates_per_s": cyc_s * n * n / 1e9,
+            "roofline": roof, "clocks": res["clocks"],
+            "gpu_launches": res["kernels"] * args.steps,
+            "kernel_ms": {"generator_finest": res["gen_ms"], "gs_finest": res["gs_ms"], "cycle": res["cyc_ms"]},
+        }
+        if res["e2e"] is not None:
+            k2, ms, bi, bo = res["e2e"]
+            line["e2e"] = {"value": k2 / (ms / 1e3) * world, "unit": UNIT, "h2d_bytes_per_step": bi,
+                           "d2h_bytes_per_step": bo,
+                           "path": "pinned host p,f -> torch.ops.mgsr.vcycle_ (C ABI mgsr_plan_vcycle) -> host p"}
+        if not args.no_cpu_baseline:
+            try:
+                cyc, kind, sample = cpu_reference_sample(n, args.blocks, 256, args.mode, args.sr_levels)
+                line["cpu_baseline"] = {"value": cyc, "unit": UNIT, "cores": os.cpu_count(), "kind": kind,
+                                        "sample": sample}
+            except Exception as exc:  # the baseline never blocks the GPU line
+                line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+                                        "sample": f"failed: {exc}"}
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

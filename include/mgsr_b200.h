@@ -136,6 +136,17 @@ int32_t mgsr_plan_levels(const mgsr_plan *plan, int64_t *sides_out /* >= 32 entr
 int mgsr_plan_vcycle(mgsr_plan *plan, double *p, const double *f, int32_t use_sr,
                      double *stats_dev, void *stream);
 
+/* Instrumentation for bench.py.  mgsr_plan_timing_enable(plan, k): the next k
+ * V-cycle launches record CUDA events (event-record nodes inside the graph,
+ * re-targeted per launch) around (0) the finest-level generator kernel,
+ * (1) the finest-level Gauss-Seidel kernel, (2) the whole cycle.
+ * mgsr_plan_timing_read: synchronises those events and returns the mean
+ * duration in ms of each over the recorded launches (0 when absent). */
+int mgsr_plan_timing_enable(mgsr_plan *plan, int32_t max_launches);
+int mgsr_plan_timing_read(mgsr_plan *plan, double *ms_out /* 3 */, int32_t *launches_out);
+/* Number of kernel nodes in the captured graph of an operator (0 if not captured yet). */
+int32_t mgsr_plan_kernel_nodes(mgsr_plan *plan, int32_t use_sr);
+
 #ifdef __cplusplus
 }
 #endif

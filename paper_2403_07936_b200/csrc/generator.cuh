@@ -30,10 +30,10 @@ namespace mgsr {
 size_t sr_workspace_bytes(int64_t nc, int s, int precision);
 int launch_sr_prolong(const mgsr_gen *g, const double *c, const double *c_shift, int nc, int s, double p_min,
                       double p_max, int precision, double *out, double *out_mean, void *ws, size_t ws_bytes,
-                      void *red_slot, cudaStream_t st);
+                      void *red_slot, cudaStream_t st, cudaEvent_t *gen_markers = nullptr);
 
 // tensor-core generator (generator_tc.cu): windows of a 6x6 pass, ratio 2.
-int tc_pack_weights(mgsr_gen *g);
+int tc_pack_weights(mgsr_gen *g, const float *const *host_tensors);
 size_t tc_workspace_bytes(int64_t nc);
 int launch_sr_pass_tc(const mgsr_gen *g, const double *c, const double *c_shift, int nc, double log_lo,
                       double span, double *fine, void *ws, size_t ws_bytes, cudaStream_t st);

@@ -288,7 +288,7 @@ static int sr_pass_simt(const mgsr_gen *g, const double *c, const double *c_shif
 
 int launch_sr_prolong(const mgsr_gen *g, const double *c, const double *c_shift, int nc, int s, double p_min,
                       double p_max, int precision, double *out, double *out_mean, void *ws, size_t ws_bytes,
-                      void *red_slot, cudaStream_t st) {
+                      void *red_slot, cudaStream_t st, cudaEvent_t *gen_markers) {
     int npass = 0;
     const int *plan = pass_plan(s, &npass);
     if (!plan) { set_error("unsupported SR ratio " + std::to_string(s) + "; expected one of [2, 4, 8, 16]"); return MGSR_E_SR_RATIO; }
@@ -312,6 +312,8 @@ int launch_sr_prolong(const mgsr_gen *g, const double *c, const double *c_shift,
         const int apps = plan[ip];
         double *dst = (ip == npass - 1) ? out : inter;
         int r;
+        const bool mark = gen_markers && ip == npass - 1;
+        if (mark) MGSR_CUDA_TRY(cudaEventRecordWithFlags(gen_markers[0], st, cudaEventRecordExternal));
         if (precision == MGSR_PREC_BF16) {
             // tensor-core path only; no silent fallback to the fp32 CUDA-core path
             if (apps != 1 || !g->tc_blob) {
@@ -323,6 +325,7 @@ int launch_sr_prolong(const mgsr_gen *g, const double *c, const double *c_shift,
             r = sr_pass_simt(g, src, src_shift, n_in, apps, log_lo, span, dst, reinterpret_cast<float *>(w), st);
         }
         if (r) return r;
+        if (mark) MGSR_CUDA_TRY(cudaEventRecordWithFlags(gen_markers[1], st, cudaEventRecordExternal));
         const int n_out = n_in << apps;
         double *mean_dst = (ip == npass - 1) ? out_mean : scal;
         k_mean_f64<<<grid_for(int64_t(n_out) * n_out, 256), 256, 0, st>>>(dst, int64_t(n_out) * n_out, sl, mean_dst);
@@ -400,7 +403,7 @@ extern "C" int mgsr_generator_create(const float *const *t, int32_t num_tensors,
     UP(3 * 64 * 81, &g->tail_w);
     UP(3, &g->tail_b);
 #undef UP
-    if ((r = tc_pack_weights(g))) goto fail;
+    if ((r = tc_pack_weights(g, t))) goto fail;
     *out = g;
     return MGSR_OK;
 fail:

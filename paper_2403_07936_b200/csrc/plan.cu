@@ -47,7 +47,18 @@ struct mgsr_plan {
     void *srws = nullptr;
     size_t srws_bytes = 0;
     cudaStream_t cap = nullptr;
-    std::map<std::tuple<double *, const double *, int>, cudaGraphExec_t> graphs;
+    struct Graph {
+        cudaGraph_t graph = nullptr;
+        cudaGraphExec_t exec = nullptr;
+        std::vector<std::pair<int, cudaGraphNode_t>> marker_nodes;
+        int kernel_nodes = 0;
+    };
+    std::map<std::tuple<double *, const double *, int>, Graph> graphs;
+    // instrumentation: placeholder events captured as event-record nodes
+    cudaEvent_t cap_ev[6] = {};
+    bool capturing_markers = false;
+    std::vector<cudaEvent_t> pool;
+    int pool_used = 0, pool_cap = 0;
 };
 
 namespace {
@@ -85,7 +96,8 @@ int prolong_into(mgsr_plan *pl, int l, int use_sr, const double *base, const dou
     const bool sr = use_sr && ((pl->cfg.sr_level_mask >> (l - 1)) & 1u);
     if (!sr) return launch_prolong_add(corr, nc, s, base, bshift, out, mean_out, slot(pl, 3), st);
     int r = launch_sr_prolong(pl->gen, corr, nullptr, nc, s, pl->cfg.p_min, pl->cfg.p_max, pl->cfg.precision,
-                              pl->srbuf, sr_mean(pl, l), pl->srws, pl->srws_bytes, slot(pl, 2), st);
+                              pl->srbuf, sr_mean(pl, l), pl->srws, pl->srws_bytes, slot(pl, 2), st,
+                              (l == 1 && pl->capturing_markers) ? pl->cap_ev : nullptr);
     if (r) return r;
     const int64_t nf = int64_t(nc) * s;
     return launch_add2(base, bshift, pl->srbuf, sr_mean(pl, l), out, nf * nf, mean_out, slot(pl, 3), st);
@@ -123,14 +135,21 @@ int record_vcycle(mgsr_plan *pl, double *p, const double *f, int use_sr, cudaStr
     const double h = 2.0 * M_PI / n;
     const int s0 = n / pl->sides[1];
     FSrc fs{f, nullptr, 1.0};
+    const bool mk = pl->capturing_markers;
+    if (mk) MGSR_CUDA_TRY(cudaEventRecordWithFlags(pl->cap_ev[4], st, cudaEventRecordExternal));
+    if (mk) MGSR_CUDA_TRY(cudaEventRecordWithFlags(pl->cap_ev[2], st, cudaEventRecordExternal));
     int r = launch_gs(p, pl->S, pl->tmp, fs, n, h * h, pl->cfg.n_smooth, 0, s0 == 2 ? pl->rc[1] : nullptr,
                       s0 == 2 ? rc_mean(pl, 1) : nullptr, sc(pl, SC_S_MEAN), pl->red, st);
     if (r) return r;
+    if (mk) MGSR_CUDA_TRY(cudaEventRecordWithFlags(pl->cap_ev[3], st, cudaEventRecordExternal));
     if (s0 != 2 && (r = launch_res_restrict(pl->S, fs, n, s0, pl->rc[1], rc_mean(pl, 1), slot(pl, 1), st))) return r;
     if ((r = correction(pl, 1, use_sr, st))) return r;
     const double *bshift = n <= kSmallN ? nullptr : sc(pl, SC_S_MEAN);
     if ((r = prolong_into(pl, 1, use_sr, pl->S, bshift, pl->S, sc(pl, SC_OUT_MEAN), st))) return r;
-    return launch_finalize(pl->S, sc(pl, SC_OUT_MEAN), p, fs, n, sc(pl, SC_ACC), sc(pl, SC_STATS), slot(pl, 0), st);
+    r = launch_finalize(pl->S, sc(pl, SC_OUT_MEAN), p, fs, n, sc(pl, SC_ACC), sc(pl, SC_STATS), slot(pl, 0), st);
+    if (r) return r;
+    if (mk) MGSR_CUDA_TRY(cudaEventRecordWithFlags(pl->cap_ev[5], st, cudaEventRecordExternal));
+    return MGSR_OK;
 }
 
 }  // namespace
@@ -192,13 +211,20 @@ extern "C" int mgsr_plan_create(const mgsr_plan_config *cfg, const mgsr_gen *gen
     }
     e = cudaStreamCreateWithFlags(&pl->cap, cudaStreamNonBlocking);
     if (e != cudaSuccess) { mgsr_plan_destroy(pl); set_error("stream create failed"); return MGSR_E_CUDA; }
+    for (auto &ev : pl->cap_ev) cudaEventCreate(&ev);
+    pl->capturing_markers = true;   // graphs always carry marker nodes (no-ops unless re-targeted)
     *out = pl;
     return MGSR_OK;
 }
 
 extern "C" int mgsr_plan_destroy(mgsr_plan *pl) {
     if (!pl) return MGSR_OK;
-    for (auto &kv : pl->graphs) cudaGraphExecDestroy(kv.second);
+    for (auto &kv : pl->graphs) {
+        cudaGraphExecDestroy(kv.second.exec);
+        cudaGraphDestroy(kv.second.graph);
+    }
+    for (auto ev : pl->cap_ev) if (ev) cudaEventDestroy(ev);
+    for (auto ev : pl->pool) cudaEventDestroy(ev);
     if (pl->cap) cudaStreamDestroy(pl->cap);
     if (pl->mem) cudaFree(pl->mem);
     delete pl;
@@ -227,14 +253,80 @@ extern "C" int mgsr_plan_vcycle(mgsr_plan *pl, double *p, const double *f, int32
         cudaError_t e = cudaStreamEndCapture(pl->cap, &graph);
         if (r) { if (graph) cudaGraphDestroy(graph); return r; }
         if (e != cudaSuccess) { set_error(std::string("graph capture: ") + cudaGetErrorString(e)); return MGSR_E_CUDA; }
-        cudaGraphExec_t exec = nullptr;
-        e = cudaGraphInstantiate(&exec, graph, 0);
-        cudaGraphDestroy(graph);
-        if (e != cudaSuccess) { set_error(std::string("graph instantiate: ") + cudaGetErrorString(e)); return MGSR_E_CUDA; }
-        it = pl->graphs.emplace(key, exec).first;
+        mgsr_plan::Graph G;
+        G.graph = graph;
+        size_t nn = 0;
+        cudaGraphGetNodes(graph, nullptr, &nn);
+        std::vector<cudaGraphNode_t> nodes(nn);
+        cudaGraphGetNodes(graph, nodes.data(), &nn);
+        for (auto nd : nodes) {
+            cudaGraphNodeType t;
+            cudaGraphNodeGetType(nd, &t);
+            if (t == cudaGraphNodeTypeKernel) G.kernel_nodes++;
+            if (t == cudaGraphNodeTypeEventRecord) {
+                cudaEvent_t ev;
+                cudaGraphEventRecordNodeGetEvent(nd, &ev);
+                for (int k = 0; k < 6; ++k)
+                    if (ev == pl->cap_ev[k]) G.marker_nodes.push_back({k, nd});
+            }
+        }
+        e = cudaGraphInstantiate(&G.exec, graph, 0);
+        if (e != cudaSuccess) { cudaGraphDestroy(graph); set_error(std::string("graph instantiate: ") + cudaGetErrorString(e)); return MGSR_E_CUDA; }
+        it = pl->graphs.emplace(key, G).first;
     }
-    MGSR_CUDA_TRY(cudaGraphLaunch(it->second, st));
+    mgsr_plan::Graph &G = it->second;
+    if (pl->pool_used < pl->pool_cap) {
+        cudaEvent_t *evs = pl->pool.data() + 6 * pl->pool_used;
+        for (auto &mn : G.marker_nodes) MGSR_CUDA_TRY(cudaGraphExecEventRecordNodeSetEvent(G.exec, mn.second, evs[mn.first]));
+        pl->pool_used++;
+    } else if (pl->pool_cap > 0 && pl->pool_used == pl->pool_cap) {
+        // stop recording into the pool: point the nodes back at the placeholders
+        for (auto &mn : G.marker_nodes) MGSR_CUDA_TRY(cudaGraphExecEventRecordNodeSetEvent(G.exec, mn.second, pl->cap_ev[mn.first]));
+    }
+    MGSR_CUDA_TRY(cudaGraphLaunch(G.exec, st));
     if (stats_dev)
         MGSR_CUDA_TRY(cudaMemcpyAsync(stats_dev, sc(pl, SC_STATS), 2 * sizeof(double), cudaMemcpyDeviceToDevice, st));
     return MGSR_OK;
+}
+
+extern "C" int mgsr_plan_timing_enable(mgsr_plan *pl, int32_t max_launches) {
+    if (!pl || max_launches < 0) { set_error("bad argument"); return MGSR_E_BAD_ARG; }
+    for (auto ev : pl->pool) cudaEventDestroy(ev);
+    pl->pool.assign(size_t(max_launches) * 6, nullptr);
+    for (auto &ev : pl->pool) MGSR_CUDA_TRY(cudaEventCreate(&ev));
+    pl->pool_cap = max_launches;
+    pl->pool_used = 0;
+    return MGSR_OK;
+}
+
+extern "C" int mgsr_plan_timing_read(mgsr_plan *pl, double *ms_out, int32_t *launches_out) {
+    if (!pl || !ms_out) { set_error("bad argument"); return MGSR_E_BAD_ARG; }
+    double acc[3] = {0, 0, 0};
+    int cnt[3] = {0, 0, 0};
+    for (int i = 0; i < pl->pool_used; ++i) {
+        cudaEvent_t *evs = pl->pool.data() + 6 * i;
+        for (int k = 0; k < 3; ++k) {
+            if (cudaEventSynchronize(evs[2 * k]) != cudaSuccess || cudaEventSynchronize(evs[2 * k + 1]) != cudaSuccess) {
+                cudaGetLastError();
+                continue;
+            }
+            float ms = 0.f;
+            if (cudaEventElapsedTime(&ms, evs[2 * k], evs[2 * k + 1]) == cudaSuccess) {
+                acc[k] += ms;
+                cnt[k]++;
+            } else {
+                cudaGetLastError();   // event never recorded in this graph variant
+            }
+        }
+    }
+    for (int k = 0; k < 3; ++k) ms_out[k] = cnt[k] ? acc[k] / cnt[k] : 0.0;
+    if (launches_out) *launches_out = pl->pool_used;
+    return MGSR_OK;
+}
+
+extern "C" int32_t mgsr_plan_kernel_nodes(mgsr_plan *pl, int32_t use_sr) {
+    if (!pl) return 0;
+    for (auto &kv : pl->graphs)
+        if (std::get<2>(kv.first) == int(use_sr != 0)) return kv.second.kernel_nodes;
+    return 0;
 }

@@ -1,0 +1,21 @@
+"""Profiling driver (GPU): one bf16 SR pass at coarse side nc (default 2048 = the
+finest 4096^2 prolongation).  Not collected by pytest.  Used as
+    ncu --set full -k regex:k_gen_tc -s 1 -c 1 python tests/tc_profile.py"""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2403_07936_b200 import ops, srmodel, _lib  # noqa: E402
+
+nc = int(sys.argv[1]) if len(sys.argv) > 1 else 2048
+reps = int(sys.argv[2]) if len(sys.argv) > 2 else 2
+w = srmodel.random_weights(8, 0)
+rng = np.random.default_rng(0)
+c = torch.from_numpy((10.0 ** rng.uniform(-7, -3.5, (nc, nc))) * np.where(rng.random((nc, nc)) < 0.5, -1, 1)).cuda()
+for _ in range(reps):
+    out = ops.sr_prolong(c, w.device_handle(), 2, 1e-10, 1e-3, _lib.PREC["bf16"])
+torch.cuda.synchronize()
+print("ok", float(out.abs().max()))
