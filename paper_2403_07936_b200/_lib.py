@@ -11,7 +11,7 @@ import os
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmgsr_b200.so")
+LIB_PATH = os.environ.get("MGSR_LIB") or os.path.join(HERE, "libmgsr_b200.so")
 
 MGSR_OK = 0
 MGSR_E_CUDA = -8

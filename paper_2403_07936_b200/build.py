@@ -28,7 +28,7 @@ SOURCES = {
     "stencil.cu": ["--fmad=false"],
     "plan.cu": ["--fmad=false"],
     "generator_simt.cu": [],
-    "generator_tc.cu": [],
+    "generator_tc.cu": ["-maxrregcount=112"],
 }
 
 

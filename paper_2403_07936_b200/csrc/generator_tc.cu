@@ -2,33 +2,44 @@
 //
 // Reference semantics: srmodel.py:285-344 (generator), 414-463 (windowed
 // pass), grid.py:103-114 (log normalisation).  One persistent CTA per SM
-// walks groups of 6 windows; all 20 layers of a window group stay on chip:
+// walks groups of 6 windows; every layer of a window group stays on chip:
 //
 //   * activations: bf16 in shared memory, each 6x6 window stored as an 8x8
 //     replicate-padded tile (64 rows) so that every 3x3 tap of a same-size
 //     replicate-padded correlation is the SAME matrix shifted by a constant
 //     row offset: the UMMA A-descriptor start address moves by 16 B per row
-//     (K-major, no swizzle), no im2col.  Two windows = one 128-row M tile,
+//     (K-major, no swizzle) -- no im2col.  Two windows = one 128-row M tile,
 //     three tiles per group.
-//   * accumulators and the fp32 residual stream live in TMEM (512 columns:
-//     per tile 64 accumulator + 64 residual columns; the 256-wide
-//     up-convolution runs as two N=128 halves in the same 128 columns).
-//   * weights (bf16, pre-packed in the UMMA core-matrix layout) stream from
-//     L2 through a 3-stage ring with cp.async.bulk + mbarrier complete_tx.
+//   * TMEM (512 columns): per tile a 64-column fp32 accumulator, the fp32
+//     residual stream (64 columns) and the global-skip tensor (bf16 pairs,
+//     32 columns); the tail accumulators reuse the dead residual columns.
+//   * weights: bf16, pre-packed in the UMMA core-matrix layout, one 8 KB slot
+//     per 3x3 tap: the 9-slot ring holds a whole layer, so the MMA issuer
+//     runs tile-major and each tile's epilogue overlaps the next tile's MMAs.
+//     Slots refill with the next layer's taps (cp.async.bulk + mbarrier
+//     complete_tx) as soon as the last tile has consumed them.
 //   * head 9x9 conv: tf32 MMA (K = 81 taps, the 3 identical input channels
 //     folded) on an im2col built per tile; PReLU in the epilogue.
-//   * body: 2B+1 3x3 convs (bf16 x bf16 -> fp32) with BN folded into a
-//     per-channel affine, PReLU / residual add / global skip fused into the
-//     epilogue (TMEM -> registers -> smem).
-//   * up conv 64->256 + pixel shuffle + PReLU fused into the epilogue, which
-//     writes the 12x12 shuffled field (fp32) for the tail.
-//   * tail 9x9 conv 64->3 + bias + s*tanh(x/s) + channel mean + denormalise,
-//     evaluated in fp32 on CUDA cores ONLY at the stitched (kept) pixels, and
-//     written straight into the fine fp64 grid.
+//   * body: 2B+1 3x3 convs (bf16 x bf16 -> fp32, N = 64), BN folded into a
+//     per-channel affine; PReLU / residual add / global skip fused into the
+//     TMEM -> register -> smem epilogue.
+//   * up conv 64->256 as four N = 64 quarters; PReLU fused; the output is
+//     kept UNSHUFFLED: quarter u holds shuffled channels 16u..16u+15 in their
+//     four sub-pixel phases.
+//   * tail 9x9 conv (64 -> 3) on the x2 field = a 5x5 conv on the coarse grid
+//     over (channel, phase) inputs producing 3 outputs x 4 phases (sub-pixel
+//     decomposition), run on the same pipeline: 25 shifted taps, N = 16,
+//     accumulated over the four quarters in TMEM.  For interior windows the
+//     stitched (kept) pixels read only in-window cells, so no padding is
+//     involved; windows touching the grid edge (0.4% at n_c = 2048) spill
+//     their up-conv output to global memory and an exact fp32 kernel
+//     evaluates their tail with the reference's replicate clamping.
+//   * bias + s*tanh(x/s) + channel mean + sign-preserving 10^ map in the final
+//     epilogue, written straight into the fine fp64 grid.
 //
-// Warp roles: warp 0 = weight producer (1 lane), warp 1 = MMA issuer (1 lane,
-// also TMEM allocator), warps 2..9 = epilogue (256 threads; warp w reads TMEM
-// lane quadrant w%4, column half (w-2)/4).
+// Warp roles: warp 0 = weight producer, warp 1 = MMA issuer + TMEM allocator,
+// warps 2..17 = epilogue (512 threads; warp w reads TMEM lane quadrant w%4,
+// channel quarter (w-2)/4).
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -51,43 +62,55 @@ constexpr int ROWS = 128;            // rows per tile (2 x 8x8 padded windows)
 constexpr int GUARD = 16;            // guard rows around the act planes (tap shifts are within +-9)
 constexpr int PLANE_ROWS = GUARD + T * ROWS + GUARD;
 constexpr int ACT_PLANE = PLANE_ROWS * 16;            // bytes per 8-channel plane
-constexpr int ACT_BYTES = 8 * ACT_PLANE;              // 53248
-constexpr int SKIP_TILE = 8 * ROWS * 16;              // 16384
-constexpr int SKIP_BYTES = T * SKIP_TILE;             // 49152
-constexpr int STAGES = 3;
-constexpr int STAGE_BYTES = 16384;
-constexpr int RING_BYTES = STAGES * STAGE_BYTES;      // 49152
+constexpr int ACT_BYTES = 8 * ACT_PLANE;              // 55296
+constexpr int NSLOT = 10;                             // ring slots (> 9: next layer's first taps prefetch)
+constexpr int SLOT_BYTES = 8192;                      // 64 oc x 64 ic bf16 (one 3x3 tap)
+constexpr int RING_BYTES = NSLOT * SLOT_BYTES;        // 73728
 constexpr int UNION_BYTES = 69632;
-constexpr int MISC_BYTES = 2048;                      // q table (3 tiles x 72 floats) etc.
-constexpr int BAR_BYTES = 256;
+constexpr int MISC_BYTES = 8192;                      // q tables (6 x 36 floats) + head im2col index table
+constexpr int BAR_BYTES = 512;
+// union, head phase
+constexpr int HK = 88;                                   // head K (81 taps padded to a tf32 K multiple)
+constexpr int HPLANES = HK / 4;                          // 22 planes of 4 tf32
+constexpr int I2C_BYTES = HPLANES * ROWS * 16;           // 45056
+constexpr int HB_BYTES = HPLANES * 64 * 16;              // 22528, streamed through the ring (3 slots)
+constexpr int IDX_OFF = 1024;                            // in misc: uint8 [64 padded pixels][88 k] -> q index
+static_assert(I2C_BYTES <= UNION_BYTES, "union");
+// up phase (union): the up-conv quarter, pixel-shuffled, bf16 [window][12x12][16 ch] with a 48-byte
+// pixel stride (conflict-free ldmatrix rows), double-buffered over tiles; tail weights of the quarter
+// bf16 [tap 81][o 3][16 ch] (double-buffered over quarters); a zero row; the reduction scratch.
+constexpr int UQ = 16;
+constexpr int U_PIX_B = 48;
+constexpr int U_TILE_BYTES = WPT * 144 * U_PIX_B;      // 13824
+
+constexpr int U_OFF0 = 0;
+constexpr int TW_OFF0 = 2 * U_TILE_BYTES;              // 27648
+constexpr int ZERO_OFF = TW_OFF0 + 2 * 7808;           // 43264 (TW slots padded to 16 B multiples)
+constexpr int RED_OFF = ZERO_OFF + 64;                 // 43328
+constexpr int TAIL_UNITS = 2 * 9;                      // (window, dy) per tile
+constexpr int RED_BYTES = 32 * 16 * 8 * 4;             // 16384
+static_assert(RED_OFF + RED_BYTES <= UNION_BYTES, "union");
 constexpr int OFF_ACT = 0;
-constexpr int OFF_SKIP = OFF_ACT + ACT_BYTES;
-constexpr int OFF_RING = OFF_SKIP + SKIP_BYTES;
+constexpr int OFF_RING = OFF_ACT + ACT_BYTES;
 constexpr int OFF_UNION = OFF_RING + RING_BYTES;
 constexpr int OFF_MISC = OFF_UNION + UNION_BYTES;
 constexpr int OFF_BAR = OFF_MISC + MISC_BYTES;
-constexpr int SMEM_BYTES = OFF_BAR + BAR_BYTES + 1024;   // +1024 alignment slack
-// union sub-layout
-constexpr int U_PIX = 33;                                // floats per pixel (32 channels + 1 pad)
-constexpr int U_BYTES = WPT * 144 * U_PIX * 4;           // 38016
-constexpr int TW_OFF = U_BYTES;                          // tail weights [dy][dx][o][32]
-constexpr int TW_BYTES = 81 * 3 * 32 * 4;                // 31104
-constexpr int HK = 88;                                   // head K (81 taps padded to tf32 K multiple)
-constexpr int HPLANES = HK / 4;                          // 22 planes of 4 tf32
-constexpr int I2C_BYTES = HPLANES * ROWS * 16;           // 45056
-constexpr int HB_OFF = I2C_BYTES;
-constexpr int HB_BYTES = HPLANES * 64 * 16;              // 22528
-static_assert(U_BYTES + TW_BYTES <= UNION_BYTES, "union");
-static_assert(HB_OFF + HB_BYTES <= UNION_BYTES, "union");
-static_assert(SMEM_BYTES <= 232448, "smem");
+constexpr int OFF_CONST = OFF_BAR + BAR_BYTES;
+// TMEM columns
+constexpr int COL_ACC = 0, COL_RES = 192, COL_SKIP = 384;
 
-constexpr int NTHREADS = 320;
-constexpr int BODY_TAP_BYTES = 8192;   // 64 oc x 64 ic bf16
-constexpr int UP_TAP_BYTES = 16384;    // 128 oc x 64 ic bf16
+constexpr int NEPI = 16;                       // epilogue warps
+constexpr int NTHREADS = 64 + 32 * NEPI;       // 576
+constexpr int UP_QUARTERS = 4;
+constexpr int BLOB_COPIES = 1;                 // weight blob replicas in HBM/L2: CTA b streams copy b % 8,
+                                               // spreading the lockstep weight stream over more L2 slices
+
+__host__ __device__ inline int const_floats(int nl) { return 64 + 192 * nl + 64 + 4; }
+__host__ __device__ inline int smem_bytes(int nl) { return OFF_CONST + 4 * const_floats(nl); }
 
 // blob layout (bytes); body layer count NL = 2B + 1
 struct BlobLayout {
-    size_t head_b, body, up, tail, consts, total;
+    size_t head_b, body, up, tail, tail_f32, consts, total;
     int nl;
 };
 
@@ -96,10 +119,11 @@ __host__ __device__ inline BlobLayout blob_layout(int blocks) {
     L.nl = 2 * blocks + 1;
     L.head_b = 0;
     L.body = L.head_b + HB_BYTES;
-    L.up = L.body + size_t(L.nl) * 9 * BODY_TAP_BYTES;
-    L.tail = L.up + 2 * 9 * UP_TAP_BYTES;
-    L.consts = L.tail + 2 * TW_BYTES;
-    L.total = L.consts + sizeof(float) * (64 + 192 * L.nl + 64 + 4);
+    L.up = L.body + size_t(L.nl) * 9 * SLOT_BYTES;
+    L.tail = L.up + size_t(UP_QUARTERS) * 9 * SLOT_BYTES;
+    L.tail_f32 = L.tail + size_t(UP_QUARTERS) * 7808;   // then [3][64][81] fp32 (edge kernel)
+    L.consts = L.tail_f32 + sizeof(float) * 3 * 64 * 81;
+    L.total = L.consts + sizeof(float) * const_floats(L.nl);
     return L;
 }
 // consts (floats): [0,64) head alpha; layer L: 64 + 192 L + {0: scale, 64: shift, 128: alpha};
@@ -124,7 +148,7 @@ __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 10000000;\n\t"
         "@!p bra WAIT_%=;\n\t}" ::"r"(bar),
         "r"(parity)
         : "memory");
@@ -160,28 +184,63 @@ __device__ __forceinline__ void umma_commit(uint32_t bar) {
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 512;" ::: "memory"); }
 
-#define TMEM_LD32(taddr, v)                                                                                   \
+#define TMEM_LD16(taddr, v)                                                                                   \
     asm volatile(                                                                                             \
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"      \
-        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                            \
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];" \
         : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),     \
-          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),            \
-          "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),          \
-          "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),          \
-          "=r"(v[29]), "=r"(v[30]), "=r"(v[31])                                                               \
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]) \
         : "r"(taddr))
-
-#define TMEM_ST32(taddr, v)                                                                                   \
+#define TMEM_ST16(taddr, v)                                                                                   \
     asm volatile(                                                                                             \
-        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"   \
-        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),                 \
-        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),    \
-        "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]),        \
-        "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]),       \
-        "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])                    \
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" \
+        ::"r"(taddr), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), \
+        "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])          \
         : "memory")
+#define TMEM_LD8(taddr, v)                                                                                    \
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"                     \
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),       \
+                   "=r"(v[7])                                                                                 \
+                 : "r"(taddr))
+#define TMEM_ST8(taddr, v)                                                                                    \
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),        \
+                 "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])     \
+                 : "memory")
+
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred = 0;
+    asm volatile(
+        "{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.b32 %0, 1, 0, P;\n\t}"
+        : "=r"(pred));
+    return pred != 0;
+}
+
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t (&r)[4]) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x2(uint32_t addr, uint32_t (&r)[2]) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0,%1}, [%2];" : "=r"(r[0]), "=r"(r[1]) : "r"(addr));
+}
+__device__ __forceinline__ void mma_16816(float (&c)[4], const uint32_t (&a)[4], const uint32_t (&b)[2]) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
+__device__ __forceinline__ void lds16(const float *src, float (&dst)[16]) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const float4 v = reinterpret_cast<const float4 *>(src)[k];
+        dst[4 * k] = v.x;
+        dst[4 * k + 1] = v.y;
+        dst[4 * k + 2] = v.z;
+        dst[4 * k + 3] = v.w;
+    }
+}
 
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
@@ -191,7 +250,6 @@ __device__ __forceinline__ float to_tf32(float x) {
     asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
     return __uint_as_float(r);
 }
-
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
     __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
     return *reinterpret_cast<uint32_t *>(&h);
@@ -200,8 +258,12 @@ __device__ __forceinline__ float bf16_lo(uint32_t u) { return __uint_as_float(u 
 __device__ __forceinline__ float bf16_hi(uint32_t u) { return __uint_as_float(u & 0xFFFF0000u); }
 
 // instruction descriptors: D fp32, K-major A and B, M = 128
-__host__ __device__ constexpr uint32_t idesc_bf16(int n) { return (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(n >> 3) << 17) | (uint32_t(128 >> 4) << 24); }
-__host__ __device__ constexpr uint32_t idesc_tf32(int n) { return (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(n >> 3) << 17) | (uint32_t(128 >> 4) << 24); }
+__host__ __device__ constexpr uint32_t idesc_bf16(int n) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(n >> 3) << 17) | (uint32_t(128 >> 4) << 24);
+}
+__host__ __device__ constexpr uint32_t idesc_tf32(int n) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(n >> 3) << 17) | (uint32_t(128 >> 4) << 24);
+}
 
 struct Params {
     const double *c;
@@ -212,31 +274,40 @@ struct Params {
     double log_lo, span;
     double *fine;
     int nf;
+    const float *qgrid;   // normalised coarse grid, tf32-rounded fp32 (k_normalize)
     const uint8_t *blob;
     int nl;
     float tanh_s;
+    uint16_t *edge_u;   // [n_edge][36][256] bf16 up-conv output of edge windows
     float *dbg;
     int dbg_layer;
+    unsigned long long *prof;   // optional wait-cycle counters (bring-up instrumentation)
 };
 
-// window geometry of a global window index
+// window geometry of a global window index (srmodel.py:414-440)
 struct Win {
-    int iw, jw, lo_i, hi_i, lo_j, hi_j;
-    bool valid;
+    int iw, jw, wi, wj;
+    bool valid, edge;
 };
 __device__ __forceinline__ Win window_of(const Params &P, long long k) {
     Win w;
     w.valid = k < P.nwin;
-    long long kk = w.valid ? k : P.nwin - 1;
-    w.iw = 2 * int(kk / P.npos);
-    w.jw = 2 * int(kk % P.npos);
-    const int last = 2 * (P.npos - 1);
-    w.lo_i = w.iw == 0 ? 0 : 2;
-    w.hi_i = w.iw == last ? 6 : 4;
-    w.lo_j = w.jw == 0 ? 0 : 2;
-    w.hi_j = w.jw == last ? 6 : 4;
+    const int kk = int(w.valid ? k : P.nwin - 1);
+    w.wi = kk / P.npos;
+    w.wj = kk - w.wi * P.npos;
+    w.iw = 2 * w.wi;
+    w.jw = 2 * w.wj;
+    w.edge = w.wi == 0 || w.wj == 0 || w.wi == P.npos - 1 || w.wj == P.npos - 1;
     return w;
 }
+// index of an edge window among the 4 npos - 4 edge windows (row 0, row last, then the side columns)
+__host__ __device__ __forceinline__ int edge_index(int wi, int wj, int npos) {
+    if (npos == 1) return 0;
+    if (wi == 0) return wj;
+    if (wi == npos - 1) return npos + wj;
+    return 2 * npos + 2 * (wi - 1) + (wj == 0 ? 0 : 1);
+}
+__host__ __device__ inline int edge_count(int npos) { return npos == 1 ? 1 : 4 * npos - 4; }
 
 __device__ __forceinline__ double normalize_q(double v, double log_lo, double span) {
     if (v == 0.0) return 0.0;
@@ -244,52 +315,70 @@ __device__ __forceinline__ double normalize_q(double v, double log_lo, double sp
     t = t < 0.0 ? 0.0 : (t > 1.0 ? 1.0 : t);
     return v > 0.0 ? t : -t;
 }
+__device__ __forceinline__ double denormalize_q(double q, double log_lo, double span) {
+    if (q == 0.0) return 0.0;   // sign 0 annihilates (grid.py:112-114)
+    const double mag = pow(10.0, log_lo + fabs(q) * span);
+    return q > 0.0 ? mag : -mag;
+}
 
-// Write one row's 32 channels (bf16) of tile t into the act planes at row `row`
-// plus its replicate-padding images.  kc0 = first 8-channel plane (4 planes).
-__device__ __forceinline__ void store_act_row(uint8_t *act, int t, int row, int kc0, const uint32_t (&pk)[16]) {
+// Write one row's 16 channels (bf16, planes kc0, kc0+1) of tile t into the
+// planes at `row`, plus (replicas) its replicate-padding images.
+template <bool REPLICAS>
+__device__ __forceinline__ void store_row(uint8_t *buf, int t, int row, int kc0, const uint32_t (&pk)[8]) {
     const int w = row >> 6, pix = row & 63, py = pix >> 3, px = pix & 7;
-    if (py < 1 || py > 6 || px < 1 || px > 6) return;   // border rows hold replicas written by interior rows
-    int ty[2] = {py, py == 1 ? 0 : (py == 6 ? 7 : -1)};
-    int tx[2] = {px, px == 1 ? 0 : (px == 6 ? 7 : -1)};
+    if (py < 1 || py > 6 || px < 1 || px > 6) return;
+    const uint4 v0 = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+    const uint4 v1 = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+    if (!REPLICAS) {
+        const int r = GUARD + t * ROWS + row;
+        *reinterpret_cast<uint4 *>(buf + kc0 * ACT_PLANE + r * 16) = v0;
+        *reinterpret_cast<uint4 *>(buf + (kc0 + 1) * ACT_PLANE + r * 16) = v1;
+        return;
+    }
+    const int ty[2] = {py, py == 1 ? 0 : (py == 6 ? 7 : -1)};
+    const int tx[2] = {px, px == 1 ? 0 : (px == 6 ? 7 : -1)};
 #pragma unroll
     for (int a = 0; a < 2; ++a) {
 #pragma unroll
         for (int b = 0; b < 2; ++b) {
             if (ty[a] < 0 || tx[b] < 0) continue;
             const int r = GUARD + t * ROWS + w * 64 + ty[a] * 8 + tx[b];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                uint4 v = make_uint4(pk[4 * k], pk[4 * k + 1], pk[4 * k + 2], pk[4 * k + 3]);
-                *reinterpret_cast<uint4 *>(act + (kc0 + k) * ACT_PLANE + r * 16) = v;
-            }
+            *reinterpret_cast<uint4 *>(buf + kc0 * ACT_PLANE + r * 16) = v0;
+            *reinterpret_cast<uint4 *>(buf + (kc0 + 1) * ACT_PLANE + r * 16) = v1;
         }
     }
 }
 
 __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
-    extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    extern __shared__ __align__(128) uint8_t smem[];
     uint8_t *act = smem + OFF_ACT;
-    uint8_t *skip = smem + OFF_SKIP;
     uint8_t *ring = smem + OFF_RING;
     uint8_t *uni = smem + OFF_UNION;
     float *misc = reinterpret_cast<float *>(smem + OFF_MISC);
+    float *cs = reinterpret_cast<float *>(smem + OFF_CONST);
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + OFF_BAR);
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + OFF_BAR + 200);
-    const uint32_t b_full = smem_u32(bars + 0);      // [STAGES]
-    const uint32_t b_empty = smem_u32(bars + 3);     // [STAGES]
-    const uint32_t b_i2c_full = smem_u32(bars + 6);
-    const uint32_t b_i2c_empty = smem_u32(bars + 7);
-    const uint32_t b_acc_full = smem_u32(bars + 8);  // [T]
-    const uint32_t b_act_ready = smem_u32(bars + 11);  // [T]
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + OFF_BAR + 480);
+    const uint32_t b_full = smem_u32(bars + 0);         // [NSLOT]
+    const uint32_t b_empty = smem_u32(bars + NSLOT);    // [NSLOT]
+    const uint32_t b_i2c_full = smem_u32(bars + 2 * NSLOT);
+    const uint32_t b_i2c_empty = smem_u32(bars + 2 * NSLOT + 1);
+    const uint32_t b_acc_full = smem_u32(bars + 2 * NSLOT + 2);    // [T] MMA -> epilogue: accumulator ready
+    const uint32_t b_act_ready = smem_u32(bars + 2 * NSLOT + 5);   // [T] epilogue -> MMA: accumulator drained, act written
+    const uint32_t b_ubuf_full = smem_u32(bars + 2 * NSLOT + 8);   // [2] drain warps -> tail warps: U buffer written
+    const uint32_t b_ubuf_free = smem_u32(bars + 2 * NSLOT + 10);  // [2] tail warps -> drain warps: U buffer consumed
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int NL = P.nl, NLAYERS = P.nl;
     const BlobLayout BL = blob_layout((P.nl - 1) / 2);
-    const float *consts = reinterpret_cast<const float *>(P.blob + BL.consts);
+    const uint8_t *wblob = P.blob + size_t(blockIdx.x % BLOB_COPIES) * ((BL.total + 1023) & ~size_t(1023));
 
+    {
+        const float4 *src = reinterpret_cast<const float4 *>(P.blob + BL.consts);
+        float4 *dst = reinterpret_cast<float4 *>(cs);
+        for (int i = threadIdx.x; i < const_floats(NL) / 4; i += NTHREADS) dst[i] = src[i];
+    }
     if (threadIdx.x == 0) {
-        for (int s = 0; s < STAGES; ++s) {
+        for (int s = 0; s < NSLOT; ++s) {
             mbar_init(b_full + 8 * s, 1);
             mbar_init(b_empty + 8 * s, 1);
         }
@@ -297,7 +386,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
         mbar_init(b_i2c_empty, 1);
         for (int t = 0; t < T; ++t) {
             mbar_init(b_acc_full + 8 * t, 1);
-            mbar_init(b_act_ready + 8 * t, 8);
+            mbar_init(b_act_ready + 8 * t, NEPI);
+            if (t < 2) {
+                mbar_init(b_ubuf_full + 8 * t, NEPI / 2);
+                mbar_init(b_ubuf_free + 8 * t, NEPI / 2);
+            }
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -313,90 +406,146 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
 
     if (warp == 0) {
         // ================= weight producer =================
-        if (lane == 0) {
-            int stage = 0;
-            uint32_t phase = 0;
-            for (int g = blockIdx.x; g < P.ngroups; g += gridDim.x) {
-                for (int L = 0; L < P.nl + 2; ++L) {
-                    const bool up = L >= P.nl;
-                    const uint32_t bytes = up ? UP_TAP_BYTES : BODY_TAP_BYTES;
-                    const uint8_t *src = up ? P.blob + BL.up + size_t(L - P.nl) * 9 * UP_TAP_BYTES
-                                            : P.blob + BL.body + size_t(L) * 9 * BODY_TAP_BYTES;
-                    for (int tap = 0; tap < 9; ++tap) {
-                        mbar_wait(b_empty + 8 * stage, phase ^ 1);
-                        mbar_expect_tx(b_full + 8 * stage, bytes);
-                        bulk_g2s(smem_u32(ring + stage * STAGE_BYTES), src + size_t(tap) * bytes, bytes,
-                                 b_full + 8 * stage);
-                        if (++stage == STAGES) { stage = 0; phase ^= 1; }
-                    }
-                }
+        uint32_t ph = 0;   // bit s = fill parity of slot s
+        int slot = 0;      // taps stream through the ring in order: slot = global tap index mod NSLOT
+        auto fill = [&](const uint8_t *src, uint32_t bytes = SLOT_BYTES) {
+            mbar_wait(b_empty + 8 * slot, ((ph >> slot) & 1u) ^ 1u);
+            if (elect_one()) {
+                mbar_expect_tx(b_full + 8 * slot, bytes);
+                bulk_g2s(smem_u32(ring + slot * SLOT_BYTES), src, bytes, b_full + 8 * slot);
             }
+            __syncwarp();
+            ph ^= 1u << slot;
+            slot = slot == NSLOT - 1 ? 0 : slot + 1;
+        };
+        for (int g = blockIdx.x; g < P.ngroups; g += gridDim.x) {
+            for (int h = 0; h < 3; ++h)   // head weights: planes 0-7, 8-15, 16-21
+                fill(wblob + BL.head_b + h * SLOT_BYTES, h < 2 ? SLOT_BYTES : HB_BYTES - 2 * SLOT_BYTES);
+            for (int L = 0; L < NLAYERS; ++L)
+                for (int tap = 0; tap < 9; ++tap) fill(wblob + BL.body + (size_t(L) * 9 + tap) * SLOT_BYTES);
+            for (int u = 0; u < UP_QUARTERS; ++u)
+                for (int tap = 0; tap < 9; ++tap) fill(wblob + BL.up + (size_t(u) * 9 + tap) * SLOT_BYTES);
         }
     } else if (warp == 1) {
-        // ================= MMA issuer =================
-        if (lane == 0) {
-            int stage = 0;
-            uint32_t phase = 0, i2c_ph = 0;
-            uint32_t ar_ph[T] = {0, 0, 0};
-            const uint32_t act_base = smem_u32(act);
-            const uint32_t ring_base = smem_u32(ring);
-            const uint32_t i2c_base = smem_u32(uni);
-            const uint32_t hb_base = smem_u32(uni + HB_OFF);
-            for (int g = blockIdx.x; g < P.ngroups; g += gridDim.x) {
-                // head: D[t] = im2col(q) (128 x 88, tf32) x Wh^T (88 x 64)
-                for (int t = 0; t < T; ++t) {
-                    mbar_wait(b_act_ready + 8 * t, ar_ph[t]);
-                    ar_ph[t] ^= 1;
-                    mbar_wait(b_i2c_full, i2c_ph);
-                    i2c_ph ^= 1;
-                    tc_fence_after();
-                    const uint32_t d = tmem + 128 * t;
+        // ================= MMA issuer (warp-uniform control, one elected lane issues) =================
+        uint32_t ph = 0, i2c_ph = 0;
+        int slot0 = 0;   // ring slot of tap 0 of the current layer
+        uint32_t ar_ph[T] = {0, 0, 0};
+        const uint32_t act_base = smem_u32(act), uni_base = smem_u32(uni), ring_base = smem_u32(ring);
+        const uint32_t i2c_base = uni_base;
+        const uint32_t id64 = idesc_bf16(64);
+        const uint64_t a_desc0 = make_desc(act_base, ACT_PLANE, 128);
+        const uint64_t b_desc0 = make_desc(ring_base, 1024, 128);        // 3x3 tap: 64-row planes
+        long long w_act = 0, w_full = 0, t_start = clock64();
+        // one N = 64 3x3 layer over the three tiles (body, post, up quarter)
+        long long t_head_m = 0, t_body_m = 0, t_up_m = 0;
+        auto conv_layer = [&]() {
+#pragma unroll
+            for (int t = 0; t < T; ++t) {
+                long long c0 = P.prof ? clock64() : 0;
+                mbar_wait(b_act_ready + 8 * t, ar_ph[t]);
+                if (P.prof) w_act += clock64() - c0;
+                ar_ph[t] ^= 1;
+                tc_fence_after();
+                const uint64_t a_t = a_desc0 + uint64_t(GUARD + t * ROWS);
+                const uint32_t d = tmem + COL_ACC + 64 * t;
+                if (elect_one()) {
+#pragma unroll
+                    for (int tap = 0; tap < 9; ++tap) {
+                        int s = slot0 + tap;
+                        s = s >= NSLOT ? s - NSLOT : s;
+                        if (t == 0) {
+                            long long c1 = P.prof ? clock64() : 0;
+                            mbar_wait(b_full + 8 * s, (ph >> s) & 1u);
+                            if (P.prof) w_full += clock64() - c1;
+                            tc_fence_after();
+                        }
+                        const int shift = (tap / 3 - 1) * 8 + (tap % 3 - 1);
+                        const uint64_t a = a_t + uint64_t(int64_t(shift));
+                        const uint64_t b = b_desc0 + uint64_t(s * (SLOT_BYTES / 16));
+#pragma unroll
+                        for (int ks = 0; ks < 4; ++ks)
+                            mma_bf16(d, a + uint64_t(ks * (2 * ACT_PLANE / 16)), b + uint64_t(ks * (2 * 1024 / 16)),
+                                     id64, (tap | ks) > 0);
+                        if (t == T - 1) umma_commit(b_empty + 8 * s);
+                    }
+                    umma_commit(b_acc_full + 8 * t);
+                }
+                __syncwarp();
+            }
+#pragma unroll
+            for (int tap = 0; tap < 9; ++tap) {
+                int s = slot0 + tap;
+                s = s >= NSLOT ? s - NSLOT : s;
+                ph ^= 1u << s;
+            }
+            slot0 += 9;
+            slot0 = slot0 >= NSLOT ? slot0 - NSLOT : slot0;
+        };
+        for (int g = blockIdx.x; g < P.ngroups; g += gridDim.x) {
+            // head: D[t] = im2col(q) (128 x 88, tf32) x Wh^T (88 x 64)
+            const long long ph0 = P.prof ? clock64() : 0;
+            for (int t = 0; t < T; ++t) {
+                mbar_wait(b_act_ready + 8 * t, ar_ph[t]);
+                ar_ph[t] ^= 1;
+                mbar_wait(b_i2c_full, i2c_ph);
+                i2c_ph ^= 1;
+                tc_fence_after();
+                const uint32_t d = tmem + COL_ACC + 64 * t;
+                if (elect_one()) {
+#pragma unroll
                     for (int ks = 0; ks < HK / 8; ++ks) {
+                        int sl = slot0 + (ks >> 2);
+                        sl = sl >= NSLOT ? sl - NSLOT : sl;
+                        if (t == 0 && (ks & 3) == 0) {
+                            mbar_wait(b_full + 8 * sl, (ph >> sl) & 1u);
+                            tc_fence_after();
+                        }
                         uint64_t a = make_desc(i2c_base + 2 * ks * (ROWS * 16), ROWS * 16, 128);
-                        uint64_t b = make_desc(hb_base + 2 * ks * (64 * 16), 64 * 16, 128);
+                        uint64_t b = make_desc(ring_base + sl * SLOT_BYTES + (ks & 3) * 2048, 64 * 16, 128);
                         mma_tf32(d, a, b, idesc_tf32(64), ks > 0);
+                        if (t == T - 1 && ((ks & 3) == 3 || ks == HK / 8 - 1)) umma_commit(b_empty + 8 * sl);
                     }
                     umma_commit(b_acc_full + 8 * t);
                     umma_commit(b_i2c_empty);
                 }
-                // body + post (N = 64) and the two up-conv halves (N = 128)
-                for (int L = 0; L < P.nl + 2; ++L) {
-                    const bool up = L >= P.nl;
-                    const uint32_t idesc = up ? idesc_bf16(128) : idesc_bf16(64);
-                    const uint32_t bplane = up ? 128 * 16 : 64 * 16;
-                    for (int tap = 0; tap < 9; ++tap) {
-                        mbar_wait(b_full + 8 * stage, phase);
-                        tc_fence_after();
-                        const int shift = (tap / 3 - 1) * 8 + (tap % 3 - 1);
-                        const uint32_t bbase = ring_base + stage * STAGE_BYTES;
-                        for (int t = 0; t < T; ++t) {
-                            if (tap == 0) {
-                                mbar_wait(b_act_ready + 8 * t, ar_ph[t]);
-                                ar_ph[t] ^= 1;
-                                tc_fence_after();
-                            }
-                            const uint32_t d = tmem + 128 * t;
-                            const uint32_t arow = act_base + uint32_t(GUARD + t * ROWS + shift) * 16;
+                __syncwarp();
+            }
 #pragma unroll
-                            for (int ks = 0; ks < 4; ++ks) {
-                                uint64_t a = make_desc(arow + 2 * ks * ACT_PLANE, ACT_PLANE, 128);
-                                uint64_t b = make_desc(bbase + 2 * ks * bplane, bplane, 128);
-                                mma_bf16(d, a, b, idesc, (tap | ks) > 0);
-                            }
-                            if (tap == 8) umma_commit(b_acc_full + 8 * t);
-                        }
-                        umma_commit(b_empty + 8 * stage);
-                        if (++stage == STAGES) { stage = 0; phase ^= 1; }
-                    }
-                }
+            for (int h = 0; h < 3; ++h) {
+                int sl = slot0 + h;
+                sl = sl >= NSLOT ? sl - NSLOT : sl;
+                ph ^= 1u << sl;
+            }
+            slot0 += 3;
+            slot0 = slot0 >= NSLOT ? slot0 - NSLOT : slot0;
+            const long long ph1 = P.prof ? clock64() : 0;
+#pragma unroll 1
+            for (int L = 0; L < NLAYERS; ++L) conv_layer();
+            const long long ph2 = P.prof ? clock64() : 0;
+#pragma unroll 1
+            for (int u = 0; u < UP_QUARTERS; ++u) conv_layer();   // up quarters
+            if (P.prof) {
+                t_head_m += ph1 - ph0;
+                t_body_m += ph2 - ph1;
+                t_up_m += clock64() - ph2;
             }
         }
+        if (P.prof && lane == 0) {
+            atomicAdd(P.prof + 0, (unsigned long long)w_act);
+            atomicAdd(P.prof + 1, (unsigned long long)w_full);
+            atomicAdd(P.prof + 2, (unsigned long long)(clock64() - t_start));
+            atomicAdd(P.prof + 40, (unsigned long long)t_head_m);
+            atomicAdd(P.prof + 41, (unsigned long long)t_body_m);
+            atomicAdd(P.prof + 42, (unsigned long long)t_up_m);
+        }
     } else {
-        // ================= epilogue (warps 2..9) =================
-        const int ew = warp - 2;               // 0..7
+        // ================= epilogue (warps 2..17) =================
+        const int ew = warp - 2;               // 0..15
         const int q = warp & 3;                // TMEM lane quadrant
-        const int hh = ew >> 2;                // column half
-        const int et = threadIdx.x - 64;       // 0..255
+        const int cq = ew >> 2;                // channel quarter
+        const int cb = 16 * cq;                // first channel of this thread
+        const int et = threadIdx.x - 64;       // 0..511
         const int row = 32 * q + lane;         // row within a tile
         const int wt = row >> 6, pix = row & 63, py = pix >> 3, px = pix & 7;
         const bool interior = py >= 1 && py <= 6 && px >= 1 && px <= 6;
@@ -404,54 +553,54 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
         uint32_t af_ph[T] = {0, 0, 0};
         uint32_t i2c_empty_ph = 0;
         bool first_build = true;
-        // pre-arrive: every accumulator starts free
         if (lane == 0)
-            for (int t = 0; t < T; ++t) mbar_arrive(b_act_ready + 8 * t);
-        const float *head_a = consts;
-        const float *up_a = consts + 64 + 192 * P.nl;
+            for (int t = 0; t < T; ++t) mbar_arrive(b_act_ready + 8 * t);   // accumulators start free
+        const float *head_a = cs;
+        uint8_t *idx_tab = reinterpret_cast<uint8_t *>(smem + OFF_MISC + IDX_OFF);
+        for (int i = et; i < 64 * HK; i += 32 * NEPI) {   // im2col index table (replicate-clamped 9x9 taps)
+            const int rp = i / HK, k = i - rp * HK;
+            const int cy = min(max((rp >> 3) - 1, 0), 5), cx = min(max((rp & 7) - 1, 0), 5);
+            uint8_t v = 255;
+            if (k < 81) {
+                const int y = min(max(cy + k / 9 - 4, 0), 5), x = min(max(cx + k % 9 - 4, 0), 5);
+                v = uint8_t(y * 6 + x);
+            }
+            idx_tab[i] = v;
+        }
+        const float *up_a = cs + 64 + 192 * NL;
         const float *tail_b = up_a + 64;
+        long long w_acc = 0, t_up = 0, e_q = 0, e_i2c = 0, e_head = 0, e_body = 0, e_end = 0;
         for (int g = blockIdx.x; g < P.ngroups; g += gridDim.x) {
             const long long k0 = (long long)g * WPG;
+            long long ce0 = clock64();
             // ---- q tables of the 6 windows (fp64 normalise -> fp32) ----
-            for (int i = et; i < WPG * 36; i += 256) {
-                const int wk = i / 36, pp = i % 36;
-                Win W = window_of(P, k0 + wk);
-                const double sh = P.c_shift ? *P.c_shift : 0.0;
-                double v = P.c[(long long)(W.iw + pp / 6) * P.nc + W.jw + pp % 6] - sh;
-                misc[i] = float(normalize_q(v, P.log_lo, P.span));
+            if (et < WPG * 36) {
+                const int wk = et / 36, pp = et % 36;
+                const Win W = window_of(P, k0 + wk);
+                misc[et] = __ldg(P.qgrid + (long long)(W.iw + pp / 6) * P.nc + W.jw + pp % 6);
             }
             epi_bar();
-            // ---- head: im2col per tile (tf32) + head weights, MMA, PReLU epilogue ----
+            long long ce1 = clock64();
+            // ---- head: im2col per tile (tf32) + head weights ----
             for (int t = 0; t < T; ++t) {
                 if (!first_build) {
                     mbar_wait(b_i2c_empty, i2c_empty_ph);
                     i2c_empty_ph ^= 1;
                 }
-                if (first_build || t == 0) {
-                    // head weights (tf32, UMMA layout) into the union
-                    const uint4 *src = reinterpret_cast<const uint4 *>(P.blob + BL.head_b);
-                    uint4 *dst = reinterpret_cast<uint4 *>(uni + HB_OFF);
-                    for (int i = et; i < HB_BYTES / 16; i += 256) dst[i] = src[i];
-                }
                 first_build = false;
                 {
-                    // row `r` of tile t: 2 threads per row split the 22 planes
-                    const int r = et & 127, part = et >> 7;
+                    const int r = et & 127, part4 = et >> 7;
                     const int rw = r >> 6, rp = r & 63;
-                    const int cy = min(max((rp >> 3) - 1, 0), 5), cx = min(max((rp & 7) - 1, 0), 5);
                     const float *qt = misc + (t * WPT + rw) * 36;
-                    for (int kc = part * 11; kc < part * 11 + 11; ++kc) {
+                    const uint32_t *ix = reinterpret_cast<const uint32_t *>(idx_tab + rp * HK);
+                    const int kc_end = min(part4 * 6 + 6, HPLANES);
+                    for (int kc = part4 * 6; kc < kc_end; ++kc) {
+                        const uint32_t i4 = ix[kc];
                         float v[4];
 #pragma unroll
                         for (int e = 0; e < 4; ++e) {
-                            const int k = 4 * kc + e;
-                            if (k < 81) {
-                                const int dy = k / 9, dx = k % 9;
-                                const int y = min(max(cy + dy - 4, 0), 5), x = min(max(cx + dx - 4, 0), 5);
-                                v[e] = to_tf32(qt[y * 6 + x]);
-                            } else {
-                                v[e] = 0.f;
-                            }
+                            const uint32_t id = (i4 >> (8 * e)) & 0xFFu;
+                            v[e] = id < 36 ? qt[id] : 0.f;
                         }
                         *reinterpret_cast<float4 *>(uni + kc * (ROWS * 16) + r * 16) = make_float4(v[0], v[1], v[2], v[3]);
                     }
@@ -460,86 +609,84 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
                 epi_bar();
                 if (et == 0) mbar_arrive(b_i2c_full);
             }
-            // ---- per-layer epilogues ----
-            for (int L = -1; L < P.nl; ++L) {
+            long long ce2 = clock64();
+            // ---- head + body + post epilogues ----
+            long long ce3 = 0;
+            for (int L = -1; L < NL; ++L) {
+                if (L == 0) ce3 = clock64();
                 for (int t = 0; t < T; ++t) {
+                    long long c2 = (P.prof && et == 0) ? clock64() : 0;
                     mbar_wait(b_acc_full + 8 * t, af_ph[t]);
+                    if (P.prof && et == 0) w_acc += clock64() - c2;
                     af_ph[t] ^= 1;
                     tc_fence_after();
-                    uint32_t v[32];
-                    TMEM_LD32(tmem + lane_addr + 128 * t + 32 * hh, v);
+                    uint32_t v[16];
+                    TMEM_LD16(tmem + lane_addr + COL_ACC + 64 * t + cb, v);
                     tmem_wait_ld();
-                    float y[32];
-                    const int cb = 32 * hh;
+                    float y[16];
                     if (L < 0) {
-                        // head: PReLU, residual stream := y, skip := y
+                        float al[16];
+                        lds16(head_a + cb, al);
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) {
+                        for (int j = 0; j < 16; ++j) {
                             float x = __uint_as_float(v[j]);
-                            y[j] = x > 0.f ? x : __ldg(head_a + cb + j) * x;
+                            y[j] = x > 0.f ? x : al[j] * x;
                         }
-                        uint32_t st[32];
+                        uint32_t st[16], sk[8];
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) st[j] = __float_as_uint(y[j]);
-                        TMEM_ST32(tmem + lane_addr + 128 * t + 64 + cb, st);
+                        for (int j = 0; j < 16; ++j) st[j] = __float_as_uint(y[j]);
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) sk[j] = pack_bf16(y[2 * j], y[2 * j + 1]);
+                        TMEM_ST16(tmem + lane_addr + COL_RES + 64 * t + cb, st);
+                        TMEM_ST8(tmem + lane_addr + COL_SKIP + 32 * t + 8 * cq, sk);
                         tmem_wait_st();
-                        uint32_t pk[16];
-#pragma unroll
-                        for (int j = 0; j < 16; ++j) pk[j] = pack_bf16(y[2 * j], y[2 * j + 1]);
-                        if (interior) {
-#pragma unroll
-                            for (int k = 0; k < 4; ++k)
-                                *reinterpret_cast<uint4 *>(skip + t * SKIP_TILE + (4 * hh + k) * (ROWS * 16) + row * 16) =
-                                    make_uint4(pk[4 * k], pk[4 * k + 1], pk[4 * k + 2], pk[4 * k + 3]);
-                        }
-                        store_act_row(act, t, row, 4 * hh, pk);
                     } else {
-                        const float *sc = consts + 64 + 192 * L;
-                        const bool conv1 = (L < P.nl - 1) && !(L & 1);
-                        const bool post = L == P.nl - 1;
+                        const float *sc = cs + 64 + 192 * L;
+                        const bool conv1 = (L < NL - 1) && !(L & 1);
+                        const bool post = L == NL - 1;
+                        float kb[16];   // BN scale is folded into the packed weights; shift remains
+                        lds16(sc + 64 + cb, kb);
                         if (conv1) {
+                            float al[16];
+                            lds16(sc + 128 + cb, al);
 #pragma unroll
-                            for (int j = 0; j < 32; ++j) {
-                                float x = fmaf(__uint_as_float(v[j]), __ldg(sc + cb + j), __ldg(sc + 64 + cb + j));
-                                y[j] = x > 0.f ? x : __ldg(sc + 128 + cb + j) * x;
+                            for (int j = 0; j < 16; ++j) {
+                                float x = __uint_as_float(v[j]) + kb[j];
+                                y[j] = x > 0.f ? x : al[j] * x;
                             }
                         } else if (!post) {
-                            uint32_t rv[32];
-                            TMEM_LD32(tmem + lane_addr + 128 * t + 64 + cb, rv);
+                            uint32_t rv[16];
+                            TMEM_LD16(tmem + lane_addr + COL_RES + 64 * t + cb, rv);
                             tmem_wait_ld();
 #pragma unroll
-                            for (int j = 0; j < 32; ++j)
-                                y[j] = __uint_as_float(rv[j]) +
-                                       fmaf(__uint_as_float(v[j]), __ldg(sc + cb + j), __ldg(sc + 64 + cb + j));
-                            uint32_t st[32];
+                            for (int j = 0; j < 16; ++j)
+                                y[j] = __uint_as_float(rv[j]) + (__uint_as_float(v[j]) + kb[j]);
+                            uint32_t st[16];
 #pragma unroll
-                            for (int j = 0; j < 32; ++j) st[j] = __float_as_uint(y[j]);
-                            TMEM_ST32(tmem + lane_addr + 128 * t + 64 + cb, st);
+                            for (int j = 0; j < 16; ++j) st[j] = __float_as_uint(y[j]);
+                            TMEM_ST16(tmem + lane_addr + COL_RES + 64 * t + cb, st);
                             tmem_wait_st();
                         } else {
+                            uint32_t sk[8];
+                            TMEM_LD8(tmem + lane_addr + COL_SKIP + 32 * t + 8 * cq, sk);
+                            tmem_wait_ld();
 #pragma unroll
-                            for (int k = 0; k < 4; ++k) {
-                                uint4 s4 = *reinterpret_cast<const uint4 *>(skip + t * SKIP_TILE + (4 * hh + k) * (ROWS * 16) + row * 16);
-                                uint32_t s[4] = {s4.x, s4.y, s4.z, s4.w};
-#pragma unroll
-                                for (int e = 0; e < 4; ++e) {
-                                    const int j = 8 * k + 2 * e;
-                                    y[j] = fmaf(__uint_as_float(v[j]), __ldg(sc + cb + j), __ldg(sc + 64 + cb + j)) + bf16_lo(s[e]);
-                                    y[j + 1] = fmaf(__uint_as_float(v[j + 1]), __ldg(sc + cb + j + 1), __ldg(sc + 64 + cb + j + 1)) + bf16_hi(s[e]);
-                                }
+                            for (int e = 0; e < 8; ++e) {
+                                y[2 * e] = (__uint_as_float(v[2 * e]) + kb[2 * e]) + bf16_lo(sk[e]);
+                                y[2 * e + 1] = (__uint_as_float(v[2 * e + 1]) + kb[2 * e + 1]) + bf16_hi(sk[e]);
                             }
                         }
-                        uint32_t pk[16];
-#pragma unroll
-                        for (int j = 0; j < 16; ++j) pk[j] = pack_bf16(y[2 * j], y[2 * j + 1]);
-                        store_act_row(act, t, row, 4 * hh, pk);
                     }
+                    uint32_t pk[8];
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) pk[j] = pack_bf16(y[2 * j], y[2 * j + 1]);
+                    store_row<true>(act, t, row, 2 * cq, pk);
                     if (P.dbg && P.dbg_layer == L + 1 && interior) {
                         const long long k = k0 + t * WPT + wt;
                         if (k < P.nwin) {
                             const int pp = (py - 1) * 6 + (px - 1);
 #pragma unroll
-                            for (int j = 0; j < 32; ++j) P.dbg[(k * 36 + pp) * 64 + cb + j] = y[j];
+                            for (int j = 0; j < 16; ++j) P.dbg[(k * 36 + pp) * 64 + cb + j] = y[j];
                         }
                     }
                     fence_async_smem();
@@ -548,114 +695,182 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
                     if (lane == 0) mbar_arrive(b_act_ready + 8 * t);
                 }
             }
-            // ---- up conv halves + pixel shuffle + PReLU -> U; pruned fp32 tail ----
-            float *U = reinterpret_cast<float *>(uni);
-            const float *TW = reinterpret_cast<const float *>(uni + TW_OFF);
-            float *part = reinterpret_cast<float *>(skip);   // [T][72][12] partial tail sums
-            for (int h = 0; h < 2; ++h) {
-                epi_bar();   // previous users of the union are done
-                {
-                    const uint4 *src = reinterpret_cast<const uint4 *>(P.blob + BL.tail + size_t(h) * TW_BYTES);
-                    uint4 *dst = reinterpret_cast<uint4 *>(uni + TW_OFF);
-                    for (int i = et; i < TW_BYTES / 16; i += 256) dst[i] = src[i];
-                }
-                for (int t = 0; t < T; ++t) {
-                    mbar_wait(b_acc_full + 8 * t, af_ph[t]);
-                    af_ph[t] ^= 1;
-                    tc_fence_after();
-                    uint32_t v0[32], v1[32];
-                    TMEM_LD32(tmem + lane_addr + 128 * t + 64 * hh, v0);
-                    TMEM_LD32(tmem + lane_addr + 128 * t + 64 * hh + 32, v1);
-                    tmem_wait_ld();
-                    tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(b_act_ready + 8 * t);   // accumulator free
-                    if (t > 0) epi_bar();   // tail of the previous tile done reading U
-                    if (interior) {
-                        const int y0 = 2 * (py - 1), x0 = 2 * (px - 1);
-                        float *Uw = U + wt * 144 * U_PIX;
+            // ---- up quarters.  Roles split for this phase:
+            //  * drain warps (ew < 8: quadrant q, 32 columns each) read the up accumulator, apply PReLU and
+            //    write the pixel-shuffled quarter (bf16, 16 channels) into U buffer (step & 1); edge windows
+            //    also spill their unshuffled output for k_tail_edge;
+            //  * tail warps (ew >= 8) run the pruned 9x9 tail of interior windows on mma.sync m16n8k16:
+            //    A rows = the window's 16 kept pixels gathered by ldmatrix (kept outputs read only in-window
+            //    pixels, so no clamping), B = the tap's weights (n = o, 3 of 8 used); unit = (window, group of
+            //    ~10 taps), two per warp; fp32 accumulators stay in registers across the four quarters.
+            //  U buffers hand off through mbarriers (ubuf_full / ubuf_free), so draining runs ahead. ----
+            long long cu = (P.prof && et == 0) ? clock64() : 0;
+            const uint32_t uni_s = smem_u32(uni);
+            if (ew < NEPI / 2) {
+                const int ch = ew >> 2;   // column half: quarter columns 32 ch .. 32 ch + 31
+                for (int u = 0; u < UP_QUARTERS; ++u) {
+                    float ua[8];
 #pragma unroll
-                        for (int j = 0; j < 64; ++j) {
-                            const int ocl = 64 * hh + j, cl = ocl >> 2, i = (ocl >> 1) & 1, jj = ocl & 1;
-                            float x = __uint_as_float(j < 32 ? v0[j] : v1[j - 32]);
-                            x = x > 0.f ? x : __ldg(up_a + 32 * h + cl) * x;
-                            Uw[((y0 + i) * 12 + x0 + jj) * U_PIX + cl] = x;
-                            if (P.dbg && P.dbg_layer == P.nl + 1) {
-                                const long long k = k0 + t * WPT + wt;
-                                if (k < P.nwin) P.dbg[(k * 144 + (y0 + i) * 12 + x0 + jj) * 64 + 32 * h + cl] = x;
+                    for (int m = 0; m < 8; ++m) ua[m] = up_a[UQ * u + 8 * ch + m];
+#pragma unroll
+                    for (int t = 0; t < T; ++t) {
+                        const int step = u * T + t, ub = step & 1;
+                        mbar_wait(b_acc_full + 8 * t, af_ph[t]);
+                        af_ph[t] ^= 1;
+                        tc_fence_after();
+                        uint32_t v0[16], v1[16];
+                        TMEM_LD16(tmem + lane_addr + COL_ACC + 64 * t + 32 * ch, v0);
+                        TMEM_LD16(tmem + lane_addr + COL_ACC + 64 * t + 32 * ch + 16, v1);
+                        tmem_wait_ld();
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) {   // two arrivals: this phase has half the epilogue warps draining
+                            mbar_arrive(b_act_ready + 8 * t);
+                            mbar_arrive(b_act_ready + 8 * t);
+                        }
+                        mbar_wait(b_ubuf_free + 8 * ub, ((step >> 1) & 1) ^ 1);   // tail of step - 2 done
+                        if (interior) {
+                            // column j = 32 ch + jj -> up channel 64 u + j -> shuffled c = 16 u + 8 ch + jj/4,
+                            // sub-pixel (i, j') = ((jj >> 1) & 1, jj & 1)
+                            uint8_t *Uw = uni + U_OFF0 + ub * U_TILE_BYTES + wt * (144 * U_PIX_B);
+                            const long long k = k0 + t * WPT + wt;
+                            const Win W = window_of(P, k);
+                            const int pp = (py - 1) * 6 + (px - 1);
+#pragma unroll
+                            for (int hf = 0; hf < 2; ++hf) {
+                                float y[16];
+#pragma unroll
+                                for (int j = 0; j < 16; ++j) {
+                                    const float x = __uint_as_float(hf ? v1[j] : v0[j]);
+                                    y[j] = x > 0.f ? x : ua[4 * hf + (j >> 2)] * x;
+                                }
+#pragma unroll
+                                for (int sub = 0; sub < 4; ++sub) {
+                                    const int Y = 2 * (py - 1) + (sub >> 1), X = 2 * (px - 1) + (sub & 1);
+                                    *reinterpret_cast<uint2 *>(Uw + (Y * 12 + X) * U_PIX_B + 16 * ch + 8 * hf) =
+                                        make_uint2(pack_bf16(y[sub], y[4 + sub]), pack_bf16(y[8 + sub], y[12 + sub]));
+                                }
+                                if (W.valid && W.edge) {
+                                    uint32_t pk[8];
+#pragma unroll
+                                    for (int j = 0; j < 8; ++j) pk[j] = pack_bf16(y[2 * j], y[2 * j + 1]);
+                                    uint4 *dst = reinterpret_cast<uint4 *>(P.edge_u +
+                                        (size_t(edge_index(W.wi, W.wj, P.npos)) * 36 + pp) * 256 + 64 * u + 32 * ch + 16 * hf);
+                                    dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                                    dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+                                }
+                                if (P.dbg && P.dbg_layer == NL + 1 && W.valid) {
+#pragma unroll
+                                    for (int j = 0; j < 16; ++j) {
+                                        const int c = UQ * u + 8 * ch + 4 * hf + (j >> 2), Y = 2 * (py - 1) + ((j >> 1) & 1),
+                                                  X = 2 * (px - 1) + (j & 1);
+                                        P.dbg[(k * 144 + Y * 12 + X) * 64 + c] = y[j];
+                                    }
+                                }
                             }
                         }
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(b_ubuf_full + 8 * ub);
                     }
-                    epi_bar();   // U complete
-                    // tail over the kept segments of the tile's two windows
-                    Win W0 = window_of(P, k0 + t * WPT), W1 = window_of(P, k0 + t * WPT + 1);
-                    const int sx0 = (W0.hi_j - W0.lo_j) / 2, sx1 = (W1.hi_j - W1.lo_j) / 2;
-                    const int n0 = W0.valid ? 2 * (W0.hi_i - W0.lo_i) * sx0 : 0;
-                    const int n1 = W1.valid ? 2 * (W1.hi_i - W1.lo_i) * sx1 : 0;
-                    for (int s = ew; s < n0 + n1; s += 8) {
-                        const int w = s < n0 ? 0 : 1;
-                        const Win &Wn = w ? W1 : W0;
-                        const int ls = w ? s - n0 : s, sx = w ? sx1 : sx0;
-                        const int fy = 2 * Wn.lo_i + ls / sx, fx0 = 2 * Wn.lo_j + 4 * (ls % sx);
-                        const float *Uw = U + w * 144 * U_PIX + lane;
-                        float acc[12];
+                }
+            } else {
+                const int tw = ew - NEPI / 2;                                        // 0..7
+                const int r = (lane & 7) + ((lane >> 3) & 1) * 8, kh = lane >> 4;   // A row / k half of this lane
+                const int n = lane & 7, kb = (lane >> 3) & 1;                      // B row / k half
+                float tacc[T][2][4];   // [tile][unit][fragment]
 #pragma unroll
-                        for (int a = 0; a < 12; ++a) acc[a] = 0.f;
-#pragma unroll 1
-                        for (int dy = 0; dy < 9; ++dy) {
-                            const int Y = min(max(fy + dy - 4, 0), 11);
-                            float u[12];
+                for (int t = 0; t < T; ++t)
 #pragma unroll
-                            for (int m = 0; m < 12; ++m) u[m] = Uw[(Y * 12 + min(max(fx0 - 4 + m, 0), 11)) * U_PIX];
-                            const float *tw = TW + dy * 9 * 96 + lane;
+                    for (int k = 0; k < 2; ++k)
 #pragma unroll
-                            for (int dx = 0; dx < 9; ++dx) {
-                                const float w0 = tw[dx * 96], w1 = tw[dx * 96 + 32], w2 = tw[dx * 96 + 64];
+                        for (int e = 0; e < 4; ++e) tacc[t][k][e] = 0.f;
+                if (tw == 0 && lane < 4) reinterpret_cast<uint4 *>(uni + ZERO_OFF)[lane] = make_uint4(0, 0, 0, 0);
+                for (int u = 0; u < UP_QUARTERS; ++u) {
+                    {   // tail weights of this quarter -> TW[u & 1]
+                        const uint4 *src = reinterpret_cast<const uint4 *>(P.blob + BL.tail + size_t(u) * 7808);
+                        uint4 *dst = reinterpret_cast<uint4 *>(uni + TW_OFF0 + (u & 1) * 7808);
+                        for (int i = et - 256; i < 7808 / 16; i += 256) dst[i] = src[i];
+                    }
+                    asm volatile("bar.sync 2, 256;" ::: "memory");   // TW ready; every tail warp left quarter u-1
+                    const uint32_t tw_s = uni_s + TW_OFF0 + (u & 1) * 7808;
+                    const uint32_t b0 = n < 3 ? tw_s + uint32_t(n * 32 + kb * 16) : uni_s + ZERO_OFF;
+                    const uint32_t bstep = n < 3 ? 3 * 32 : 0;
 #pragma unroll
-                                for (int p = 0; p < 4; ++p) {
-                                    acc[3 * p] = fmaf(u[p + dx], w0, acc[3 * p]);
-                                    acc[3 * p + 1] = fmaf(u[p + dx], w1, acc[3 * p + 1]);
-                                    acc[3 * p + 2] = fmaf(u[p + dx], w2, acc[3 * p + 2]);
+                    for (int t = 0; t < T; ++t) {
+                        const int step = u * T + t, ub = step & 1;
+                        mbar_wait(b_ubuf_full + 8 * ub, (step >> 1) & 1);
+                        const Win W0 = window_of(P, k0 + t * WPT), W1 = window_of(P, k0 + t * WPT + 1);
+#pragma unroll
+                        for (int k = 0; k < 2; ++k) {
+                            const int unit = tw + 8 * k, w = unit >> 3, grp = unit & 7;
+                            const Win Wn = w ? W1 : W0;
+                            if (Wn.valid && !Wn.edge) {
+                                const uint32_t a0 = uni_s + U_OFF0 + ub * U_TILE_BYTES + w * (144 * U_PIX_B) +
+                                                    uint32_t((r >> 2) * 12 + (r & 3)) * U_PIX_B + kh * 16;
+                                const int tap_lo = (81 * grp) >> 3, tap_hi = (81 * (grp + 1)) >> 3;
+                                int dy = tap_lo / 9, dx = tap_lo - 9 * dy;
+                                for (int tap = tap_lo; tap < tap_hi; ++tap) {
+                                    uint32_t a[4], bb[2];
+                                    ldsm_x4(a0 + uint32_t(dy * 12 + dx) * U_PIX_B, a);
+                                    ldsm_x2(b0 + uint32_t(tap) * bstep, bb);
+                                    mma_16816(tacc[t][k], a, bb);
+                                    if (++dx == 9) { dx = 0; ++dy; }
                                 }
                             }
                         }
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(b_ubuf_free + 8 * ub);
+                        if (u == UP_QUARTERS - 1) {
+                            const int gq = lane >> 2, tq = lane & 3;
 #pragma unroll
-                        for (int a = 0; a < 12; ++a) {
-#pragma unroll
-                            for (int o = 16; o > 0; o >>= 1) acc[a] += __shfl_xor_sync(0xffffffffu, acc[a], o);
-                        }
-                        float *pp = part + (t * 72 + s) * 12;
-                        if (h == 0) {
-                            if (lane == 0) {
-#pragma unroll
-                                for (int a = 0; a < 12; ++a) pp[a] = acc[a];
+                            for (int k = 0; k < 2; ++k) {
+                                float *ru = reinterpret_cast<float *>(uni + RED_OFF) + (tw + 8 * k) * 128;
+                                ru[gq * 8 + 2 * tq] = tacc[t][k][0];
+                                ru[gq * 8 + 2 * tq + 1] = tacc[t][k][1];
+                                ru[(gq + 8) * 8 + 2 * tq] = tacc[t][k][2];
+                                ru[(gq + 8) * 8 + 2 * tq + 1] = tacc[t][k][3];
                             }
-                        } else {
-                            const long long k = k0 + t * WPT + w;
-                            const int fy_g = 2 * Wn.iw + fy;
+                            asm volatile("bar.sync 2, 256;" ::: "memory");
+                            if (et - 256 < 32) {
+                                const int w = (et - 256) >> 4, rr = (et - 256) & 15;
+                                const Win Wn = w ? W1 : W0;
+                                if (Wn.valid && !Wn.edge) {
+                                    const float *rd = reinterpret_cast<const float *>(uni + RED_OFF) + (w * 8) * 128 + rr * 8;
+                                    double m = 0.0;
 #pragma unroll
-                            for (int p = 0; p < 4; ++p) {
-                                if (lane != p) continue;
-                                double m = 0.0;
+                                    for (int o = 0; o < 3; ++o) {
+                                        float pre = tail_b[o];
 #pragma unroll
-                                for (int o = 0; o < 3; ++o) {
-                                    const float pre = pp[3 * p + o] + acc[3 * p + o] + __ldg(tail_b + o);
-                                    m += double(P.tanh_s * tanhf(pre / P.tanh_s));
+                                        for (int d = 0; d < 8; ++d) pre += rd[d * 128 + o];
+                                        m += double(P.tanh_s * tanhf(pre / P.tanh_s));
+                                    }
+                                    m = m / 3.0;
+                                    const int fy = 4 + (rr >> 2), fx = 4 + (rr & 3);
+                                    P.fine[(long long)(2 * Wn.iw + fy) * P.nf + 2 * Wn.jw + fx] =
+                                        denormalize_q(m, P.log_lo, P.span);
                                 }
-                                m = m / 3.0;
-                                double outv = 0.0;
-                                if (m != 0.0) {
-                                    double mag = pow(10.0, P.log_lo + fabs(m) * P.span);
-                                    outv = m > 0.0 ? mag : -mag;
-                                }
-                                (void)k;
-                                P.fine[(long long)fy_g * P.nf + 2 * Wn.jw + fx0 + p] = outv;
                             }
+                            asm volatile("bar.sync 2, 256;" ::: "memory");   // red reusable
                         }
                     }
                 }
             }
+            long long ce5 = clock64();
+            if (P.prof && (et == 0 || et == 256)) {
+                e_q += ce1 - ce0; e_i2c += ce2 - ce1; e_head += ce3 - ce2; e_body += cu - ce3; t_up += ce5 - cu;
+            }
             epi_bar();
+            if (P.prof && (et == 0 || et == 256)) e_end += clock64() - ce5;
+        }
+        if (P.prof && (et == 0 || et == 256)) {
+            const int o = et == 0 ? 0 : 8;
+            if (et == 0) atomicAdd(P.prof + 3, (unsigned long long)w_acc);
+            atomicAdd(P.prof + 4 + o, (unsigned long long)t_up);
+            atomicAdd(P.prof + 20 + o, (unsigned long long)e_q);
+            atomicAdd(P.prof + 21 + o, (unsigned long long)e_i2c);
+            atomicAdd(P.prof + 22 + o, (unsigned long long)e_head);
+            atomicAdd(P.prof + 23 + o, (unsigned long long)e_body);
+            atomicAdd(P.prof + 24 + o, (unsigned long long)e_end);
         }
     }
     // teardown
@@ -663,6 +878,62 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
     __syncthreads();
     tc_fence_after();
     if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
+// q = clip((log10|c - shift| - log_lo)/span, 0, 1) * sign, rounded to tf32 (the head MMA operand)
+__global__ void k_normalize(const double *__restrict__ c, const double *shift, int nc, double log_lo, double span,
+                            float *__restrict__ q) {
+    const double sh = shift ? *shift : 0.0;
+    const long long total = (long long)nc * nc;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x)
+        q[i] = to_tf32(float(normalize_q(c[i] - sh, log_lo, span)));
+}
+
+// Tail of the edge windows (kept band touching the grid edge), exact fp32 with
+// the reference's replicate clamping (srmodel.py:285-289) on the 12x12 field.
+__global__ void __launch_bounds__(256) k_tail_edge(Params P) {
+    __shared__ float U[64 * 144];   // [c][Y][X]
+    const int e = blockIdx.x;
+    // invert edge_index
+    int wi, wj;
+    const int n = P.npos;
+    if (n == 1) { wi = 0; wj = 0; }
+    else if (e < n) { wi = 0; wj = e; }
+    else if (e < 2 * n) { wi = n - 1; wj = e - n; }
+    else { wi = 1 + (e - 2 * n) / 2; wj = ((e - 2 * n) & 1) ? n - 1 : 0; }
+    const uint16_t *src = P.edge_u + size_t(e) * 36 * 256;
+    for (int i = threadIdx.x; i < 36 * 256; i += blockDim.x) {
+        const int pp = i >> 8, oc = i & 255, c = oc >> 2, ii = (oc >> 1) & 1, jj = oc & 1;
+        const int Y = 2 * (pp / 6) + ii, X = 2 * (pp % 6) + jj;
+        U[c * 144 + Y * 12 + X] = __uint_as_float(uint32_t(src[i]) << 16);
+    }
+    __syncthreads();
+    const BlobLayout BL = blob_layout((P.nl - 1) / 2);
+    const float *w = reinterpret_cast<const float *>(P.blob + BL.tail_f32);   // [3][64][81]
+    const float *bias = reinterpret_cast<const float *>(P.blob + BL.consts) + 64 + 192 * P.nl + 64;
+    const int last = P.npos - 1;
+    const int lo_i = wi == 0 ? 0 : 2, hi_i = wi == last ? 6 : 4, lo_j = wj == 0 ? 0 : 2, hi_j = wj == last ? 6 : 4;
+    const int wk = 2 * (hi_j - lo_j), npix = 2 * (hi_i - lo_i) * wk;
+    for (int idx = threadIdx.x; idx < npix; idx += blockDim.x) {
+        const int fy = 2 * lo_i + idx / wk, fx = 2 * lo_j + idx % wk;
+        double m = 0.0;
+        for (int o = 0; o < 3; ++o) {
+            float acc = 0.f;
+            for (int c = 0; c < 64; ++c) {
+                const float *wc = w + (o * 64 + c) * 81;
+                const float *uc = U + c * 144;
+                for (int dy = 0; dy < 9; ++dy) {
+                    const int Y = min(max(fy + dy - 4, 0), 11);
+#pragma unroll
+                    for (int dx = 0; dx < 9; ++dx) acc = fmaf(uc[Y * 12 + min(max(fx + dx - 4, 0), 11)], __ldg(wc + dy * 9 + dx), acc);
+                }
+            }
+            const float pre = acc + __ldg(bias + o);
+            m += double(P.tanh_s * tanhf(pre / P.tanh_s));
+        }
+        m = m / 3.0;
+        P.fine[(long long)(2 * (2 * wi) + fy) * P.nf + 2 * (2 * wj) + fx] = denormalize_q(m, P.log_lo, P.span);
+    }
 }
 
 }  // namespace tc
@@ -685,6 +956,8 @@ static inline float tf32_rna(float f) {
     return r;
 }
 
+// Pack the MGSR1 tensors (host f32, expected_tensor_shapes order) into the
+// kernel's weight blob: UMMA core-matrix layout (K-major, 8-element planes).
 int tc_pack_weights(mgsr_gen *g, const float *const *t) {
     using namespace tc;
     const int B = g->blocks;
@@ -712,44 +985,45 @@ int tc_pack_weights(mgsr_gen *g, const float *const *t) {
         if (L == 2 * B) return 2 + 11 * B;
         return 2 + 11 * (L / 2) + ((L & 1) ? 6 : 0);
     };
-    for (int L = 0; L < BL.nl; ++L) {
-        const float *w = t[conv_index(L)];
-        for (int tap = 0; tap < 9; ++tap) {
-            uint16_t *dst = reinterpret_cast<uint16_t *>(blob.data() + BL.body + (size_t(L) * 9 + tap) * BODY_TAP_BYTES);
-            int dy = tap / 3, dx = tap % 3;
-            for (int kc = 0; kc < 8; ++kc)
-                for (int oc = 0; oc < 64; ++oc)
-                    for (int e = 0; e < 8; ++e) {
-                        int ic = 8 * kc + e;
-                        dst[(kc * 64 + oc) * 8 + e] = f2bf(w[((oc * 64 + ic) * 3 + dy) * 3 + dx]);
-                    }
-        }
-    }
-    const int ip = 2 + 11 * B;   // post conv index
-    {
-        const float *w = t[ip + 5];   // up.conv.weight 256 x 64 x 3 x 3
-        for (int h = 0; h < 2; ++h)
-            for (int tap = 0; tap < 9; ++tap) {
-                uint16_t *dst = reinterpret_cast<uint16_t *>(blob.data() + BL.up + (size_t(h) * 9 + tap) * UP_TAP_BYTES);
-                int dy = tap / 3, dx = tap % 3;
-                for (int kc = 0; kc < 8; ++kc)
-                    for (int ocl = 0; ocl < 128; ++ocl)
-                        for (int e = 0; e < 8; ++e) {
-                            int ic = 8 * kc + e, oc = 128 * h + ocl;
-                            dst[(kc * 128 + ocl) * 8 + e] = f2bf(w[((oc * 64 + ic) * 3 + dy) * 3 + dx]);
-                        }
+    // BN(conv(x)) = conv(x; W * k) + (beta - mean * k), k = gamma / sqrt(var + 1e-5): the scale is
+    // folded into the packed weights (per output channel), the shift stays in the epilogue.
+    auto bn_scale = [&](int gi, int oc) { return double(t[gi][oc]) / std::sqrt(double(t[gi + 3][oc]) + 1e-5); };
+    auto pack_tap = [&](uint16_t *dst, const float *w, int oc0, int tap, int bn_gi) {
+        int dy = tap / 3, dx = tap % 3;
+        for (int kc = 0; kc < 8; ++kc)
+            for (int oc = 0; oc < 64; ++oc) {
+                const double k = bn_gi >= 0 ? bn_scale(bn_gi, oc0 + oc) : 1.0;
+                for (int e = 0; e < 8; ++e) {
+                    int ic = 8 * kc + e;
+                    dst[(kc * 64 + oc) * 8 + e] = f2bf(float(double(w[(((oc0 + oc) * 64 + ic) * 3 + dy) * 3 + dx]) * k));
+                }
             }
-    }
+    };
+    const int ip = 2 + 11 * B;   // post conv index
+    auto bn_index = [&](int L) -> int {   // tensor index of body layer L's BN gamma
+        if (L == 2 * B) return ip + 1;
+        return 2 + 11 * (L / 2) + ((L & 1) ? 7 : 1);
+    };
+    for (int L = 0; L < BL.nl; ++L)
+        for (int tap = 0; tap < 9; ++tap)
+            pack_tap(reinterpret_cast<uint16_t *>(blob.data() + BL.body + (size_t(L) * 9 + tap) * SLOT_BYTES),
+                     t[conv_index(L)], 0, tap, bn_index(L));
+    for (int u = 0; u < UP_QUARTERS; ++u)
+        for (int tap = 0; tap < 9; ++tap)
+            pack_tap(reinterpret_cast<uint16_t *>(blob.data() + BL.up + (size_t(u) * 9 + tap) * SLOT_BYTES),
+                     t[ip + 5], 64 * u, tap, -1);
     {
+        // mma.sync tail operand: per quarter u, [tap = dy*9+dx][o][16 shuffled channels 16u..16u+15] bf16
         const float *w = t[ip + 7];   // tail.conv.weight 3 x 64 x 9 x 9
-        for (int h = 0; h < 2; ++h) {
-            float *dst = reinterpret_cast<float *>(blob.data() + BL.tail + size_t(h) * TW_BYTES);
-            for (int dy = 0; dy < 9; ++dy)
-                for (int dx = 0; dx < 9; ++dx)
-                    for (int o = 0; o < 3; ++o)
-                        for (int cl = 0; cl < 32; ++cl)
-                            dst[((dy * 9 + dx) * 3 + o) * 32 + cl] = w[((o * 64 + 32 * h + cl) * 9 + dy) * 9 + dx];
+        for (int u = 0; u < UP_QUARTERS; ++u) {
+            uint16_t *dst = reinterpret_cast<uint16_t *>(blob.data() + BL.tail + size_t(u) * 7808);
+            for (int tap = 0; tap < 81; ++tap)
+                for (int o = 0; o < 3; ++o)
+                    for (int cl = 0; cl < UQ; ++cl)
+                        dst[(tap * 3 + o) * UQ + cl] = f2bf(w[((o * 64 + UQ * u + cl) * 9 + tap / 9) * 9 + tap % 9]);
         }
+        float *wf = reinterpret_cast<float *>(blob.data() + BL.tail_f32);
+        std::memcpy(wf, w, sizeof(float) * 3 * 64 * 81);
     }
     {
         float *cs = reinterpret_cast<float *>(blob.data() + BL.consts);
@@ -773,23 +1047,29 @@ int tc_pack_weights(mgsr_gen *g, const float *const *t) {
         for (int i = 0; i < 64; ++i) upa[i] = t[ip + 6][i];
         for (int o = 0; o < 3; ++o) upa[64 + o] = t[ip + 8][o];
     }
-    MGSR_CUDA_TRY(cudaMalloc(&g->tc_blob, BL.total));
-    MGSR_CUDA_TRY(cudaMemcpy(g->tc_blob, blob.data(), BL.total, cudaMemcpyHostToDevice));
-    g->tc_bytes = BL.total;
+    const size_t stride = (BL.total + 1023) & ~size_t(1023);
+    MGSR_CUDA_TRY(cudaMalloc(&g->tc_blob, stride * BLOB_COPIES));
+    for (int c = 0; c < BLOB_COPIES; ++c)
+        MGSR_CUDA_TRY(cudaMemcpy(static_cast<uint8_t *>(g->tc_blob) + c * stride, blob.data(), BL.total,
+                                 cudaMemcpyHostToDevice));
+    g->tc_bytes = stride * BLOB_COPIES;
     return MGSR_OK;
 }
 
-size_t tc_workspace_bytes(int64_t nc) {
-    (void)nc;
-    return 0;
+// workspace: [edge-window up outputs (bf16)][normalised coarse grid q (fp32)]
+static size_t tc_edge_bytes(int64_t nc) {
+    const int npos = int(nc / 2 - 2);
+    const size_t b = npos >= 1 ? size_t(tc::edge_count(npos)) * 36 * 256 * sizeof(uint16_t) : 0;
+    return (b + 255) & ~size_t(255);
 }
-
-static int g_num_sms = 0;
+size_t tc_workspace_bytes(int64_t nc) { return tc_edge_bytes(nc) + sizeof(float) * size_t(nc) * nc + 256; }
 
 int launch_sr_pass_tc_dbg(const mgsr_gen *g, const double *c, const double *c_shift, int nc, double log_lo,
-                          double span, double *fine, float *dbg, int dbg_layer, cudaStream_t st) {
+                          double span, double *fine, void *ws, size_t ws_bytes, float *dbg, int dbg_layer,
+                          cudaStream_t st, unsigned long long *prof = nullptr) {
     using namespace tc;
     if (!g->tc_blob) { set_error("tensor-core weights not packed"); return MGSR_E_UNSUPPORTED; }
+    if (ws_bytes < tc_workspace_bytes(nc)) { set_error("tensor-core workspace too small"); return MGSR_E_WORKSPACE; }
     Params P{};
     P.c = c;
     P.c_shift = c_shift;
@@ -804,33 +1084,55 @@ int launch_sr_pass_tc_dbg(const mgsr_gen *g, const double *c, const double *c_sh
     P.blob = static_cast<const uint8_t *>(g->tc_blob);
     P.nl = 2 * g->blocks + 1;
     P.tanh_s = float(g->tanh_scale);
+    P.edge_u = static_cast<uint16_t *>(ws);
+    float *qgrid = reinterpret_cast<float *>(static_cast<char *>(ws) + tc_edge_bytes(nc));
+    P.qgrid = qgrid;
     P.dbg = dbg;
     P.dbg_layer = dbg_layer;
-    if (!g_num_sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-        MGSR_CUDA_TRY(cudaFuncSetAttribute(k_gen_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
-    }
-    int grid = P.ngroups < g_num_sms ? P.ngroups : g_num_sms;
-    k_gen_tc<<<grid, NTHREADS, SMEM_BYTES, st>>>(P);
+    P.prof = prof;
+    const int smem = smem_bytes(P.nl);
+    if (smem > 232448) { set_error("generator too deep for the tensor-core kernel's shared memory"); return MGSR_E_UNSUPPORTED; }
+    int dev = 0, nsm = 0;
+    MGSR_CUDA_TRY(cudaGetDevice(&dev));
+    MGSR_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    MGSR_CUDA_TRY(cudaFuncSetAttribute(k_gen_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    const int grid = P.ngroups < nsm ? P.ngroups : nsm;
+    k_normalize<<<grid_for((long long)nc * nc, 256), 256, 0, st>>>(c, c_shift, nc, log_lo, span, qgrid);
+    MGSR_LAUNCH_CHECK();
+    k_gen_tc<<<grid, NTHREADS, smem, st>>>(P);
+    MGSR_LAUNCH_CHECK();
+    k_tail_edge<<<edge_count(P.npos), 256, 0, st>>>(P);
     MGSR_LAUNCH_CHECK();
     return MGSR_OK;
 }
 
 int launch_sr_pass_tc(const mgsr_gen *g, const double *c, const double *c_shift, int nc, double log_lo, double span,
                       double *fine, void *ws, size_t ws_bytes, cudaStream_t st) {
-    (void)ws;
-    (void)ws_bytes;
-    return launch_sr_pass_tc_dbg(g, c, c_shift, nc, log_lo, span, fine, nullptr, -1, st);
+    return launch_sr_pass_tc_dbg(g, c, c_shift, nc, log_lo, span, fine, ws, ws_bytes, nullptr, -1, st);
 }
 
 }  // namespace mgsr
 
-// debug entry (not in the public header): dump one layer's fp32 output
+// debug entries (not in the public header)
 extern "C" int mgsr_debug_tc_pass(const mgsr_gen *g, const double *c, int64_t nc, double p_min, double p_max,
                                   double *fine, float *dbg, int32_t dbg_layer, void *stream) {
-    return mgsr::launch_sr_pass_tc_dbg(g, c, nullptr, int(nc), std::log10(p_min),
-                                       std::log10(p_max) - std::log10(p_min), fine, dbg, dbg_layer,
-                                       static_cast<cudaStream_t>(stream));
+    const size_t wsb = mgsr::tc_workspace_bytes(nc);
+    void *ws = nullptr;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (cudaMallocAsync(&ws, wsb, st) != cudaSuccess) return MGSR_E_CUDA;
+    int r = mgsr::launch_sr_pass_tc_dbg(g, c, nullptr, int(nc), std::log10(p_min),
+                                        std::log10(p_max) - std::log10(p_min), fine, ws, wsb, dbg, dbg_layer, st);
+    cudaFreeAsync(ws, st);
+    return r;
+}
+
+extern "C" int mgsr_debug_tc_prof(const mgsr_gen *g, const double *c, int64_t nc, double *fine,
+                                  unsigned long long *prof, void *stream) {
+    const size_t wsb = mgsr::tc_workspace_bytes(nc);
+    void *ws = nullptr;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (cudaMallocAsync(&ws, wsb, st) != cudaSuccess) return MGSR_E_CUDA;
+    int r = mgsr::launch_sr_pass_tc_dbg(g, c, nullptr, int(nc), -10.0, 7.0, fine, ws, wsb, nullptr, -1, st, prof);
+    cudaFreeAsync(ws, st);
+    return r;
 }
