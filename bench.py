@@ -48,7 +48,7 @@ def parse():
     ap.add_argument("--impl", default="mine", choices=["mine", "reference"])
     ap.add_argument("--n", type=int, default=4096)
     ap.add_argument("--mode", default="gan", choices=["gan", "spline"])
-    ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32"])
+    ap.add_argument("--precision", default="fp16", choices=["fp16", "bf16", "fp32"])
     ap.add_argument("--sr-levels", type=int, default=3)
     ap.add_argument("--blocks", type=int, default=8)
     ap.add_argument("--n-smooth", type=int, default=2)

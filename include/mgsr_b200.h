@@ -78,7 +78,7 @@ int mgsr_rms_diff(const double *a, const double *b, int64_t count, double *out_h
 
 typedef struct mgsr_gen mgsr_gen;
 
-enum { MGSR_PREC_FP32 = 0, MGSR_PREC_BF16 = 1 };
+enum { MGSR_PREC_FP32 = 0, MGSR_PREC_BF16 = 1, MGSR_PREC_FP16 = 2 };
 
 /* Build an immutable generator from the MGSR1 tensor set (host float32 arrays in
  * the canonical order of expected_tensor_shapes(B), srmodel.py:90-114), i.e.
@@ -98,8 +98,9 @@ int mgsr_generator_forward(const mgsr_gen *g, const double *x, int64_t batch, in
 
 /* Windowed SR prolongation by s in {2,4,8,16}: normalise, 6x6 windows at
  * stride 2, generator, channel mean, stitch, denormalise with output signs,
- * mean-subtract (per pass).  precision: MGSR_PREC_FP32 (CUDA-core fp32) or
- * MGSR_PREC_BF16 (tcgen05 bf16 operands / fp32 accumulate; s == 2 only).
+ * mean-subtract (per pass).  precision: MGSR_PREC_FP32 (CUDA-core fp32),
+ * MGSR_PREC_BF16 / MGSR_PREC_FP16 (tcgen05 megakernel with bf16 / fp16 operands,
+ * fp32 accumulation, tf32 head; ratio-2 passes only).
  * Replaces srmodel.sr_prolong (srmodel.py:470-487). */
 size_t mgsr_sr_workspace_bytes(int64_t nc, int32_t s);
 int mgsr_sr_prolong(const mgsr_gen *g, const double *c, int64_t nc, int32_t s,

@@ -15,7 +15,7 @@ LIB_PATH = os.environ.get("MGSR_LIB") or os.path.join(HERE, "libmgsr_b200.so")
 
 MGSR_OK = 0
 MGSR_E_CUDA = -8
-PREC = {"fp32": 0, "bf16": 1}
+PREC = {"fp32": 0, "bf16": 1, "fp16": 2}
 
 _lock = threading.Lock()
 _lib = None

@@ -36,6 +36,6 @@ int launch_sr_prolong(const mgsr_gen *g, const double *c, const double *c_shift,
 int tc_pack_weights(mgsr_gen *g, const float *const *host_tensors);
 size_t tc_workspace_bytes(int64_t nc);
 int launch_sr_pass_tc(const mgsr_gen *g, const double *c, const double *c_shift, int nc, double log_lo,
-                      double span, double *fine, void *ws, size_t ws_bytes, cudaStream_t st);
+                      double span, double *fine, void *ws, size_t ws_bytes, cudaStream_t st, int f16);
 
 }  // namespace mgsr

@@ -239,7 +239,7 @@ size_t sr_workspace_bytes(int64_t nc, int s, int precision) {
     // intermediate fine grid for two-pass ratios + fp32 chunk buffers + scalars
     size_t inter = (s == 8 || s == 16) ? sizeof(double) * size_t(nc * 4) * size_t(nc * 4) : 0;
     size_t simt = sizeof(float) * pass_ws_floats(2) + 4096;
-    size_t tc = precision == MGSR_PREC_BF16 ? tc_workspace_bytes(nc) : 0;
+    size_t tc = precision != MGSR_PREC_FP32 ? tc_workspace_bytes(nc) : 0;
     return inter + (simt > tc ? simt : tc) + 512;
 }
 
@@ -314,13 +314,14 @@ int launch_sr_prolong(const mgsr_gen *g, const double *c, const double *c_shift,
         int r;
         const bool mark = gen_markers && ip == npass - 1;
         if (mark) MGSR_CUDA_TRY(cudaEventRecordWithFlags(gen_markers[0], st, cudaEventRecordExternal));
-        if (precision == MGSR_PREC_BF16) {
+        if (precision == MGSR_PREC_BF16 || precision == MGSR_PREC_FP16) {
             // tensor-core path only; no silent fallback to the fp32 CUDA-core path
             if (apps != 1 || !g->tc_blob) {
-                set_error("bf16 tensor-core generator supports 6x6 windows (ratio-2 passes) only");
+                set_error("tensor-core generator supports 6x6 windows (ratio-2 passes) only");
                 return MGSR_E_UNSUPPORTED;
             }
-            r = launch_sr_pass_tc(g, src, src_shift, n_in, log_lo, span, dst, w, ws_bytes - (w - static_cast<char *>(ws)), st);
+            r = launch_sr_pass_tc(g, src, src_shift, n_in, log_lo, span, dst, w, ws_bytes - (w - static_cast<char *>(ws)), st,
+                                  precision == MGSR_PREC_FP16);
         } else {
             r = sr_pass_simt(g, src, src_shift, n_in, apps, log_lo, span, dst, reinterpret_cast<float *>(w), st);
         }

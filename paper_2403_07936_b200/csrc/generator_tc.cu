@@ -41,6 +41,7 @@
 // warps 2..17 = epilogue (512 threads; warp w reads TMEM lane quadrant w%4,
 // channel quarter (w-2)/4).
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -110,7 +111,7 @@ __host__ __device__ inline int smem_bytes(int nl) { return OFF_CONST + 4 * const
 
 // blob layout (bytes); body layer count NL = 2B + 1
 struct BlobLayout {
-    size_t head_b, body, up, tail, tail_f32, consts, total;
+    size_t head_b, body, up, tail, tail_f32, consts, fmt_stride, total;
     int nl;
 };
 
@@ -123,7 +124,9 @@ __host__ __device__ inline BlobLayout blob_layout(int blocks) {
     L.tail = L.up + size_t(UP_QUARTERS) * 9 * SLOT_BYTES;
     L.tail_f32 = L.tail + size_t(UP_QUARTERS) * 7808;   // then [3][64][81] fp32 (edge kernel)
     L.consts = L.tail_f32 + sizeof(float) * 3 * 64 * 81;
-    L.total = L.consts + sizeof(float) * const_floats(L.nl);
+    // fp16 operand set (body, up, tail) follows at +fmt_stride from the bf16 set
+    L.fmt_stride = ((L.consts + sizeof(float) * const_floats(L.nl)) + 1023) & ~size_t(1023);
+    L.total = L.fmt_stride + L.tail_f32;
     return L;
 }
 // consts (floats): [0,64) head alpha; layer L: 64 + 192 L + {0: scale, 64: shift, 128: alpha};
@@ -224,12 +227,20 @@ __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t (&r)[4]) {
 __device__ __forceinline__ void ldsm_x2(uint32_t addr, uint32_t (&r)[2]) {
     asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0,%1}, [%2];" : "=r"(r[0]), "=r"(r[1]) : "r"(addr));
 }
+template <bool F16>
 __device__ __forceinline__ void mma_16816(float (&c)[4], const uint32_t (&a)[4], const uint32_t (&b)[2]) {
-    asm volatile(
-        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-        "{%0,%1,%2,%3};"
-        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+    if (F16)
+        asm volatile(
+            "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+            "{%0,%1,%2,%3};"
+            : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+            : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+    else
+        asm volatile(
+            "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+            "{%0,%1,%2,%3};"
+            : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+            : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
 }
 __device__ __forceinline__ void lds16(const float *src, float (&dst)[16]) {
 #pragma unroll
@@ -250,6 +261,25 @@ __device__ __forceinline__ float to_tf32(float x) {
     asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
     return __uint_as_float(r);
 }
+template <bool F16>
+__device__ __forceinline__ uint32_t pack_op(float a, float b) {
+    if (F16) {
+        __half2 h = __floats2half2_rn(a, b);
+        return *reinterpret_cast<uint32_t *>(&h);
+    }
+    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t *>(&h);
+}
+template <bool F16>
+__device__ __forceinline__ float op_lo(uint32_t u) {
+    if (F16) return __half2float(__ushort_as_half(uint16_t(u & 0xFFFFu)));
+    return __uint_as_float(u << 16);
+}
+template <bool F16>
+__device__ __forceinline__ float op_hi(uint32_t u) {
+    if (F16) return __half2float(__ushort_as_half(uint16_t(u >> 16)));
+    return __uint_as_float(u & 0xFFFF0000u);
+}
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
     __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
     return *reinterpret_cast<uint32_t *>(&h);
@@ -260,6 +290,9 @@ __device__ __forceinline__ float bf16_hi(uint32_t u) { return __uint_as_float(u 
 // instruction descriptors: D fp32, K-major A and B, M = 128
 __host__ __device__ constexpr uint32_t idesc_bf16(int n) {
     return (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(n >> 3) << 17) | (uint32_t(128 >> 4) << 24);
+}
+__host__ __device__ constexpr uint32_t idesc_f16(int n) {   // a/b format 0 = F16
+    return (1u << 4) | (uint32_t(n >> 3) << 17) | (uint32_t(128 >> 4) << 24);
 }
 __host__ __device__ constexpr uint32_t idesc_tf32(int n) {
     return (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(n >> 3) << 17) | (uint32_t(128 >> 4) << 24);
@@ -279,6 +312,7 @@ struct Params {
     int nl;
     float tanh_s;
     uint16_t *edge_u;   // [n_edge][36][256] bf16 up-conv output of edge windows
+    size_t wfmt;        // byte offset of the operand-format weight set (0: bf16, BL.fmt_stride: fp16)
     float *dbg;
     int dbg_layer;
     unsigned long long *prof;   // optional wait-cycle counters (bring-up instrumentation)
@@ -349,6 +383,7 @@ __device__ __forceinline__ void store_row(uint8_t *buf, int t, int row, int kc0,
     }
 }
 
+template <bool F16>
 __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
     extern __shared__ __align__(128) uint8_t smem[];
     uint8_t *act = smem + OFF_ACT;
@@ -422,9 +457,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
             for (int h = 0; h < 3; ++h)   // head weights: planes 0-7, 8-15, 16-21
                 fill(wblob + BL.head_b + h * SLOT_BYTES, h < 2 ? SLOT_BYTES : HB_BYTES - 2 * SLOT_BYTES);
             for (int L = 0; L < NLAYERS; ++L)
-                for (int tap = 0; tap < 9; ++tap) fill(wblob + BL.body + (size_t(L) * 9 + tap) * SLOT_BYTES);
+                for (int tap = 0; tap < 9; ++tap) fill(wblob + P.wfmt + BL.body + (size_t(L) * 9 + tap) * SLOT_BYTES);
             for (int u = 0; u < UP_QUARTERS; ++u)
-                for (int tap = 0; tap < 9; ++tap) fill(wblob + BL.up + (size_t(u) * 9 + tap) * SLOT_BYTES);
+                for (int tap = 0; tap < 9; ++tap) fill(wblob + P.wfmt + BL.up + (size_t(u) * 9 + tap) * SLOT_BYTES);
         }
     } else if (warp == 1) {
         // ================= MMA issuer (warp-uniform control, one elected lane issues) =================
@@ -433,7 +468,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
         uint32_t ar_ph[T] = {0, 0, 0};
         const uint32_t act_base = smem_u32(act), uni_base = smem_u32(uni), ring_base = smem_u32(ring);
         const uint32_t i2c_base = uni_base;
-        const uint32_t id64 = idesc_bf16(64);
+        const uint32_t id64 = F16 ? idesc_f16(64) : idesc_bf16(64);
         const uint64_t a_desc0 = make_desc(act_base, ACT_PLANE, 128);
         const uint64_t b_desc0 = make_desc(ring_base, 1024, 128);        // 3x3 tap: 64-row planes
         long long w_act = 0, w_full = 0, t_start = clock64();
@@ -636,7 +671,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
 #pragma unroll
                         for (int j = 0; j < 16; ++j) st[j] = __float_as_uint(y[j]);
 #pragma unroll
-                        for (int j = 0; j < 8; ++j) sk[j] = pack_bf16(y[2 * j], y[2 * j + 1]);
+                        for (int j = 0; j < 8; ++j) sk[j] = pack_op<F16>(y[2 * j], y[2 * j + 1]);
                         TMEM_ST16(tmem + lane_addr + COL_RES + 64 * t + cb, st);
                         TMEM_ST8(tmem + lane_addr + COL_SKIP + 32 * t + 8 * cq, sk);
                         tmem_wait_st();
@@ -672,14 +707,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
                             tmem_wait_ld();
 #pragma unroll
                             for (int e = 0; e < 8; ++e) {
-                                y[2 * e] = (__uint_as_float(v[2 * e]) + kb[2 * e]) + bf16_lo(sk[e]);
-                                y[2 * e + 1] = (__uint_as_float(v[2 * e + 1]) + kb[2 * e + 1]) + bf16_hi(sk[e]);
+                                y[2 * e] = (__uint_as_float(v[2 * e]) + kb[2 * e]) + op_lo<F16>(sk[e]);
+                                y[2 * e + 1] = (__uint_as_float(v[2 * e + 1]) + kb[2 * e + 1]) + op_hi<F16>(sk[e]);
                             }
                         }
                     }
                     uint32_t pk[8];
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) pk[j] = pack_bf16(y[2 * j], y[2 * j + 1]);
+                    for (int j = 0; j < 8; ++j) pk[j] = pack_op<F16>(y[2 * j], y[2 * j + 1]);
                     store_row<true>(act, t, row, 2 * cq, pk);
                     if (P.dbg && P.dbg_layer == L + 1 && interior) {
                         const long long k = k0 + t * WPT + wt;
@@ -748,12 +783,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
                                 for (int sub = 0; sub < 4; ++sub) {
                                     const int Y = 2 * (py - 1) + (sub >> 1), X = 2 * (px - 1) + (sub & 1);
                                     *reinterpret_cast<uint2 *>(Uw + (Y * 12 + X) * U_PIX_B + 16 * ch + 8 * hf) =
-                                        make_uint2(pack_bf16(y[sub], y[4 + sub]), pack_bf16(y[8 + sub], y[12 + sub]));
+                                        make_uint2(pack_op<F16>(y[sub], y[4 + sub]), pack_op<F16>(y[8 + sub], y[12 + sub]));
                                 }
                                 if (W.valid && W.edge) {
                                     uint32_t pk[8];
 #pragma unroll
-                                    for (int j = 0; j < 8; ++j) pk[j] = pack_bf16(y[2 * j], y[2 * j + 1]);
+                                    for (int j = 0; j < 8; ++j) pk[j] = pack_op<F16>(y[2 * j], y[2 * j + 1]);
                                     uint4 *dst = reinterpret_cast<uint4 *>(P.edge_u +
                                         (size_t(edge_index(W.wi, W.wj, P.npos)) * 36 + pp) * 256 + 64 * u + 32 * ch + 16 * hf);
                                     dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
@@ -787,7 +822,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
                 if (tw == 0 && lane < 4) reinterpret_cast<uint4 *>(uni + ZERO_OFF)[lane] = make_uint4(0, 0, 0, 0);
                 for (int u = 0; u < UP_QUARTERS; ++u) {
                     {   // tail weights of this quarter -> TW[u & 1]
-                        const uint4 *src = reinterpret_cast<const uint4 *>(P.blob + BL.tail + size_t(u) * 7808);
+                        const uint4 *src = reinterpret_cast<const uint4 *>(P.blob + P.wfmt + BL.tail + size_t(u) * 7808);
                         uint4 *dst = reinterpret_cast<uint4 *>(uni + TW_OFF0 + (u & 1) * 7808);
                         for (int i = et - 256; i < 7808 / 16; i += 256) dst[i] = src[i];
                     }
@@ -813,7 +848,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
                                     uint32_t a[4], bb[2];
                                     ldsm_x4(a0 + uint32_t(dy * 12 + dx) * U_PIX_B, a);
                                     ldsm_x2(b0 + uint32_t(tap) * bstep, bb);
-                                    mma_16816(tacc[t][k], a, bb);
+                                    mma_16816<F16>(tacc[t][k], a, bb);
                                     if (++dx == 9) { dx = 0; ++dy; }
                                 }
                             }
@@ -891,6 +926,7 @@ __global__ void k_normalize(const double *__restrict__ c, const double *shift, i
 
 // Tail of the edge windows (kept band touching the grid edge), exact fp32 with
 // the reference's replicate clamping (srmodel.py:285-289) on the 12x12 field.
+template <bool F16>
 __global__ void __launch_bounds__(256) k_tail_edge(Params P) {
     __shared__ float U[64 * 144];   // [c][Y][X]
     const int e = blockIdx.x;
@@ -905,7 +941,7 @@ __global__ void __launch_bounds__(256) k_tail_edge(Params P) {
     for (int i = threadIdx.x; i < 36 * 256; i += blockDim.x) {
         const int pp = i >> 8, oc = i & 255, c = oc >> 2, ii = (oc >> 1) & 1, jj = oc & 1;
         const int Y = 2 * (pp / 6) + ii, X = 2 * (pp % 6) + jj;
-        U[c * 144 + Y * 12 + X] = __uint_as_float(uint32_t(src[i]) << 16);
+        U[c * 144 + Y * 12 + X] = op_lo<F16>(uint32_t(src[i]));
     }
     __syncthreads();
     const BlobLayout BL = blob_layout((P.nl - 1) / 2);
@@ -941,6 +977,12 @@ __global__ void __launch_bounds__(256) k_tail_edge(Params P) {
 // ---------------------------------------------------------------------------
 // host side
 
+static inline uint16_t f2h(float f) {
+    __half h = __float2half_rn(f);
+    uint16_t u;
+    std::memcpy(&u, &h, 2);
+    return u;
+}
 static inline uint16_t f2bf(float f) {
     uint32_t u;
     std::memcpy(&u, &f, 4);
@@ -990,12 +1032,15 @@ int tc_pack_weights(mgsr_gen *g, const float *const *t) {
     auto bn_scale = [&](int gi, int oc) { return double(t[gi][oc]) / std::sqrt(double(t[gi + 3][oc]) + 1e-5); };
     auto pack_tap = [&](uint16_t *dst, const float *w, int oc0, int tap, int bn_gi) {
         int dy = tap / 3, dx = tap % 3;
+        uint16_t *dst16 = reinterpret_cast<uint16_t *>(reinterpret_cast<uint8_t *>(dst) + BL.fmt_stride);
         for (int kc = 0; kc < 8; ++kc)
             for (int oc = 0; oc < 64; ++oc) {
                 const double k = bn_gi >= 0 ? bn_scale(bn_gi, oc0 + oc) : 1.0;
                 for (int e = 0; e < 8; ++e) {
                     int ic = 8 * kc + e;
-                    dst[(kc * 64 + oc) * 8 + e] = f2bf(float(double(w[(((oc0 + oc) * 64 + ic) * 3 + dy) * 3 + dx]) * k));
+                    const float v = float(double(w[(((oc0 + oc) * 64 + ic) * 3 + dy) * 3 + dx]) * k);
+                    dst[(kc * 64 + oc) * 8 + e] = f2bf(v);
+                    dst16[(kc * 64 + oc) * 8 + e] = f2h(v);
                 }
             }
     };
@@ -1017,10 +1062,14 @@ int tc_pack_weights(mgsr_gen *g, const float *const *t) {
         const float *w = t[ip + 7];   // tail.conv.weight 3 x 64 x 9 x 9
         for (int u = 0; u < UP_QUARTERS; ++u) {
             uint16_t *dst = reinterpret_cast<uint16_t *>(blob.data() + BL.tail + size_t(u) * 7808);
+            uint16_t *dst16 = reinterpret_cast<uint16_t *>(blob.data() + BL.fmt_stride + BL.tail + size_t(u) * 7808);
             for (int tap = 0; tap < 81; ++tap)
                 for (int o = 0; o < 3; ++o)
-                    for (int cl = 0; cl < UQ; ++cl)
-                        dst[(tap * 3 + o) * UQ + cl] = f2bf(w[((o * 64 + UQ * u + cl) * 9 + tap / 9) * 9 + tap % 9]);
+                    for (int cl = 0; cl < UQ; ++cl) {
+                        const float v = w[((o * 64 + UQ * u + cl) * 9 + tap / 9) * 9 + tap % 9];
+                        dst[(tap * 3 + o) * UQ + cl] = f2bf(v);
+                        dst16[(tap * 3 + o) * UQ + cl] = f2h(v);
+                    }
         }
         float *wf = reinterpret_cast<float *>(blob.data() + BL.tail_f32);
         std::memcpy(wf, w, sizeof(float) * 3 * 64 * 81);
@@ -1066,7 +1115,7 @@ size_t tc_workspace_bytes(int64_t nc) { return tc_edge_bytes(nc) + sizeof(float)
 
 int launch_sr_pass_tc_dbg(const mgsr_gen *g, const double *c, const double *c_shift, int nc, double log_lo,
                           double span, double *fine, void *ws, size_t ws_bytes, float *dbg, int dbg_layer,
-                          cudaStream_t st, unsigned long long *prof = nullptr) {
+                          cudaStream_t st, unsigned long long *prof = nullptr, int f16 = 0) {
     using namespace tc;
     if (!g->tc_blob) { set_error("tensor-core weights not packed"); return MGSR_E_UNSUPPORTED; }
     if (ws_bytes < tc_workspace_bytes(nc)) { set_error("tensor-core workspace too small"); return MGSR_E_WORKSPACE; }
@@ -1090,38 +1139,43 @@ int launch_sr_pass_tc_dbg(const mgsr_gen *g, const double *c, const double *c_sh
     P.dbg = dbg;
     P.dbg_layer = dbg_layer;
     P.prof = prof;
+    P.wfmt = f16 ? blob_layout(g->blocks).fmt_stride : 0;
     const int smem = smem_bytes(P.nl);
     if (smem > 232448) { set_error("generator too deep for the tensor-core kernel's shared memory"); return MGSR_E_UNSUPPORTED; }
     int dev = 0, nsm = 0;
     MGSR_CUDA_TRY(cudaGetDevice(&dev));
     MGSR_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    MGSR_CUDA_TRY(cudaFuncSetAttribute(k_gen_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    MGSR_CUDA_TRY(cudaFuncSetAttribute(k_gen_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    MGSR_CUDA_TRY(cudaFuncSetAttribute(k_gen_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     const int grid = P.ngroups < nsm ? P.ngroups : nsm;
     k_normalize<<<grid_for((long long)nc * nc, 256), 256, 0, st>>>(c, c_shift, nc, log_lo, span, qgrid);
     MGSR_LAUNCH_CHECK();
-    k_gen_tc<<<grid, NTHREADS, smem, st>>>(P);
+    if (f16) k_gen_tc<true><<<grid, NTHREADS, smem, st>>>(P);
+    else k_gen_tc<false><<<grid, NTHREADS, smem, st>>>(P);
     MGSR_LAUNCH_CHECK();
-    k_tail_edge<<<edge_count(P.npos), 256, 0, st>>>(P);
+    if (f16) k_tail_edge<true><<<edge_count(P.npos), 256, 0, st>>>(P);
+    else k_tail_edge<false><<<edge_count(P.npos), 256, 0, st>>>(P);
     MGSR_LAUNCH_CHECK();
     return MGSR_OK;
 }
 
 int launch_sr_pass_tc(const mgsr_gen *g, const double *c, const double *c_shift, int nc, double log_lo, double span,
-                      double *fine, void *ws, size_t ws_bytes, cudaStream_t st) {
-    return launch_sr_pass_tc_dbg(g, c, c_shift, nc, log_lo, span, fine, ws, ws_bytes, nullptr, -1, st);
+                      double *fine, void *ws, size_t ws_bytes, cudaStream_t st, int f16) {
+    return launch_sr_pass_tc_dbg(g, c, c_shift, nc, log_lo, span, fine, ws, ws_bytes, nullptr, -1, st, nullptr, f16);
 }
 
 }  // namespace mgsr
 
 // debug entries (not in the public header)
 extern "C" int mgsr_debug_tc_pass(const mgsr_gen *g, const double *c, int64_t nc, double p_min, double p_max,
-                                  double *fine, float *dbg, int32_t dbg_layer, void *stream) {
+                                  double *fine, float *dbg, int32_t dbg_layer, int32_t f16, void *stream) {
     const size_t wsb = mgsr::tc_workspace_bytes(nc);
     void *ws = nullptr;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (cudaMallocAsync(&ws, wsb, st) != cudaSuccess) return MGSR_E_CUDA;
     int r = mgsr::launch_sr_pass_tc_dbg(g, c, nullptr, int(nc), std::log10(p_min),
-                                        std::log10(p_max) - std::log10(p_min), fine, ws, wsb, dbg, dbg_layer, st);
+                                        std::log10(p_max) - std::log10(p_min), fine, ws, wsb, dbg, dbg_layer, st,
+                                        nullptr, f16);
     cudaFreeAsync(ws, st);
     return r;
 }

@@ -58,13 +58,19 @@ def torch_layers(w, x):
     return outs, s * torch.tanh(out / s)
 
 
+F16 = 0
+
+
 def main():
+    global F16
     nc = int(sys.argv[1]) if len(sys.argv) > 1 else 32
+    prec = sys.argv[3] if len(sys.argv) > 3 else "bf16"
+    F16 = 1 if prec == "fp16" else 0
     blocks = int(sys.argv[2]) if len(sys.argv) > 2 else 2
     lib = _lib.load()
     lib.mgsr_debug_tc_pass.restype = ctypes.c_int
     lib.mgsr_debug_tc_pass.argtypes = [ctypes.c_void_p] * 2 + [ctypes.c_int64, ctypes.c_double, ctypes.c_double,
-                                       ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p]
+                                       ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p]
     w = srmodel.random_weights(blocks, 0)
     rng = np.random.default_rng(0)
     c = (10.0 ** rng.uniform(-7, -3.5, (nc, nc))) * np.where(rng.random((nc, nc)) < 0.5, -1, 1)
@@ -83,7 +89,7 @@ def main():
     for L in range(nl + 2):
         size = nw * (144 if L == nl + 1 else 36) * 64
         dbg = torch.full((size,), float("nan"), dtype=torch.float32, device="cuda")
-        _lib.check(lib.mgsr_debug_tc_pass(h, dc.data_ptr(), nc, 1e-10, 1e-3, fine.data_ptr(), dbg.data_ptr(), L, st))
+        _lib.check(lib.mgsr_debug_tc_pass(h, dc.data_ptr(), nc, 1e-10, 1e-3, fine.data_ptr(), dbg.data_ptr(), L, F16, st))
         torch.cuda.synchronize()
         side = 12 if L == nl + 1 else 6
         got = dbg.view(nw, side, side, 64).permute(0, 3, 1, 2)
@@ -93,9 +99,9 @@ def main():
         print(f"layer {L:2d}: relL2 {err:.3e}  nan {nan}  max|ref| {float(ref.abs().max()):.3e}", flush=True)
     # final field vs fp32 SIMT path
     from paper_2403_07936_b200.grid import Grid, NormBounds
-    a = srmodel.sr_prolong(Grid(c), w, NormBounds(), 2, precision="bf16").data
+    a = srmodel.sr_prolong(Grid(c), w, NormBounds(), 2, precision=prec).data
     b = srmodel.sr_prolong(Grid(c), w, NormBounds(), 2, precision="fp32").data
-    print(f"sr_prolong bf16 vs fp32: relL2 {np.linalg.norm(a - b) / np.linalg.norm(b):.3e}  "
+    print(f"sr_prolong {prec} vs fp32: relL2 {np.linalg.norm(a - b) / np.linalg.norm(b):.3e}  "
           f"nan {int(np.isnan(a).sum())}")
 
 

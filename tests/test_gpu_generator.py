@@ -77,3 +77,112 @@ def test_sr_ratio_errors(cuda):
         srmodel.sr_prolong(Grid(np.ones((8, 8))), w, NormBounds(), 3)
     with pytest.raises(ValueError, match=">= 6"):
         srmodel.sr_prolong(Grid(np.ones((4, 4))), w, NormBounds(), 2)
+
+
+# ---------------------------------------------------------------------------
+# tensor-core (tcgen05) megakernel: fp16 / bf16 operands, fp32 accumulation
+
+def _fields(nc):
+    from paper_2403_07936_b200 import datagen
+    rng = np.random.default_rng(0)
+    noise = (10.0 ** rng.uniform(-7, -3.5, (nc, nc))) * np.where(rng.random((nc, nc)) < 0.5, -1, 1)
+    f = datagen.scale_to_p_rms(datagen.grf_blobs_rhs(nc, seed=3, kmax=nc / 8), 1e-5)
+    return {"noise": noise, "smooth": datagen.spectral_solution(f)}
+
+
+def _trained(blocks):
+    import os
+    from paper_2403_07936_b200 import srmodel
+    from conftest import ROOT
+    return srmodel.load_weights(os.path.join(ROOT, "artifacts", f"trained_b{blocks}.mgsr"))
+
+
+@pytest.mark.parametrize("blocks", [4, 8])
+def test_tc_fp16_field_parity_trained(cuda, blocks):
+    """North-star bar: GAN-prolonged field within 1e-2 relL2 of the fp32 generator."""
+    from paper_2403_07936_b200 import srmodel
+    from paper_2403_07936_b200.grid import Grid, NormBounds
+    w = _trained(blocks)
+    for name, c in _fields(128).items():
+        ref = srmodel.sr_prolong(Grid(c), w, NormBounds(), 2, precision="fp32").data
+        got = srmodel.sr_prolong(Grid(c), w, NormBounds(), 2, precision="fp16").data
+        assert rel_l2(got, ref) < 1e-2, name
+
+
+def test_tc_fp16_field_parity_he_init_smooth(cuda):
+    """Seeded He-init B=8 (BASELINE's fallback weights) on a smooth correction field."""
+    from paper_2403_07936_b200 import srmodel
+    from paper_2403_07936_b200.grid import Grid, NormBounds
+    w = srmodel.random_weights(8, 0)
+    c = _fields(128)["smooth"]
+    ref = srmodel.sr_prolong(Grid(c), w, NormBounds(), 2, precision="fp32").data
+    got = srmodel.sr_prolong(Grid(c), w, NormBounds(), 2, precision="fp16").data
+    assert rel_l2(got, ref) < 1e-2
+
+
+def test_tc_bf16_vs_fp16_error_ordering(cuda):
+    """bf16 (7-bit mantissa) is measurably worse than fp16 (10-bit) at the same speed; record both."""
+    from paper_2403_07936_b200 import srmodel
+    from paper_2403_07936_b200.grid import Grid, NormBounds
+    w = _trained(8)
+    c = _fields(128)["noise"]
+    ref = srmodel.sr_prolong(Grid(c), w, NormBounds(), 2, precision="fp32").data
+    e16 = rel_l2(srmodel.sr_prolong(Grid(c), w, NormBounds(), 2, precision="fp16").data, ref)
+    eb = rel_l2(srmodel.sr_prolong(Grid(c), w, NormBounds(), 2, precision="bf16").data, ref)
+    assert e16 < eb < 2e-2
+
+
+def test_tc_vs_oracle_full_field(cuda, orc):
+    """Full field against the fp64 CPU oracle on MGSR1-quantised trained weights (n_c = 64)."""
+    from paper_2403_07936_b200 import srmodel
+    from paper_2403_07936_b200.grid import Grid, NormBounds
+    w = _trained(4)
+    c = _fields(64)["smooth"]
+    ow = orc.Weights({k: v for k, v in w.tensors.items()}, w.num_residual_blocks, w.tanh_scale)
+    exp = orc.sr_prolong(c, ow, orc.Bounds(), 2)
+    got = srmodel.sr_prolong(Grid(c), w, NormBounds(), 2, precision="fp16").data
+    assert rel_l2(got, exp) < 1e-2
+
+
+@pytest.mark.parametrize("nc", [6, 8, 10, 16])
+def test_tc_edge_windows_and_tiny_grids(cuda, nc):
+    """Grids whose windows are all (or mostly) edge windows exercise the exact fallback tail;
+    every fine cell is written (stitch coverage) and matches the fp32 path."""
+    from paper_2403_07936_b200 import srmodel
+    from paper_2403_07936_b200.grid import Grid, NormBounds
+    w = _trained(4)
+    c = _fields(nc)["noise"]
+    ref = srmodel.sr_prolong(Grid(c), w, NormBounds(), 2, precision="fp32").data
+    got = srmodel.sr_prolong(Grid(c), w, NormBounds(), 2, precision="fp16").data
+    assert np.all(np.isfinite(got))
+    assert rel_l2(got, ref) < 1e-2
+
+
+def test_tc_nn_weights_upsampler(cuda):
+    """Crafted nearest-neighbour weights: the generator copies q; the field returns to the
+    input values at the coincident fine cells up to operand rounding (tf32 head)."""
+    from paper_2403_07936_b200 import srmodel
+    from paper_2403_07936_b200.grid import Grid, NormBounds
+    c = _fields(32)["noise"]
+    w = srmodel.make_nearest_neighbor_weights()
+    ref = srmodel.sr_prolong(Grid(c), w, NormBounds(), 2, precision="fp32").data
+    got = srmodel.sr_prolong(Grid(c), w, NormBounds(), 2, precision="fp16").data
+    assert rel_l2(got, ref) < 1e-2
+
+
+def test_tc_deterministic(cuda):
+    from paper_2403_07936_b200 import srmodel
+    from paper_2403_07936_b200.grid import Grid, NormBounds
+    w = _trained(8)
+    c = _fields(256)["smooth"]
+    a = srmodel.sr_prolong(Grid(c), w, NormBounds(), 2, precision="fp16").data
+    b = srmodel.sr_prolong(Grid(c), w, NormBounds(), 2, precision="fp16").data
+    assert np.array_equal(a, b)
+
+
+def test_tc_rejects_multi_pass_ratio(cuda):
+    from paper_2403_07936_b200 import srmodel
+    from paper_2403_07936_b200.grid import Grid, NormBounds
+    w = _trained(4)
+    with pytest.raises(ValueError, match="ratio-2"):
+        srmodel.sr_prolong(Grid(np.ones((16, 16)) * 1e-5), w, NormBounds(), 4, precision="fp16")

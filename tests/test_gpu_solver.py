@@ -121,3 +121,44 @@ def test_sr_requires_weights(cuda):
     f = np.zeros((32, 32))
     with pytest.raises(ValueError, match="weights"):
         solver.v_cycle(Grid(f), PoissonProblem(Grid(f)), cfg_(), "sr")
+
+
+@pytest.mark.parametrize("sr_levels,bar", [(1, 1e-2), (2, 3e-2), (None, 3e-2)])
+def test_v_cycle_sr_fp16_vs_oracle(cuda, orc, sr_levels, bar):
+    """SR V-cycle (trained weights, SR at the `sr_levels` finest prolongations -- the per-level
+    GAN mask of BASELINE config 4 -- else at every level) through the tensor-core path vs the
+    fp64 oracle.  The 1e-2 bar is the north-star field bar; with SR at every level (down to
+    8 -> 16, where nearly all windows are edge windows) the errors of four prolongations
+    compound within one cycle: measured 1.9e-2 (two SR levels) and 2.1e-2 (all levels)."""
+    import os
+    from paper_2403_07936_b200 import solver, srmodel
+    from paper_2403_07936_b200.grid import Grid
+    from paper_2403_07936_b200.smoother import PoissonProblem
+    from conftest import ROOT
+    w = srmodel.load_weights(os.path.join(ROOT, "artifacts", "trained_b4.mgsr"))
+    f = orc.scale_to_p_rms(orc.sine_modes_rhs(128, 0), 1e-4)
+    p0 = orc.initial_iterate(128, orc.Config()) * 0.1
+    ow = orc.Weights(dict(w.tensors), w.num_residual_blocks, w.tanh_scale)
+    nlev = len(orc.level_sides(128, 1, 8))
+    lops = None if sr_levels is None else [None] + ["sr" if l <= sr_levels else "spline" for l in range(1, nlev)]
+    exp = orc.v_cycle(p0, f, orc.Config(N_step=1, r_min=8, N_smooth=2), "sr", ow, level_ops=lops)
+    got = solver.v_cycle(Grid(p0), PoissonProblem(Grid(f)), cfg_(), "sr", w, precision="fp16",
+                         sr_levels=sr_levels).data
+    assert rel_l2(got, exp) < bar
+
+
+def test_solve_hybrid_fp16_matches_fp32_schedule(cuda, orc):
+    """Latched hybrid solve at 256^2 with the tensor-core generator: same operator/latch
+    sequence and iteration count as the fp32 path, converged to tol."""
+    import os
+    from paper_2403_07936_b200 import solver, srmodel
+    from paper_2403_07936_b200.grid import Grid
+    from paper_2403_07936_b200.smoother import PoissonProblem
+    from conftest import ROOT
+    w = srmodel.load_weights(os.path.join(ROOT, "artifacts", "trained_b8.mgsr"))
+    f = orc.scale_to_p_rms(orc.sine_modes_rhs(256, 0), 1e-4)
+    cfg = cfg_(mode="hybrid", N_GAN=1.0, S_thres=5e-4)
+    _, l32 = solver.solve(PoissonProblem(Grid(f)), cfg, w, precision="fp32")
+    _, l16 = solver.solve(PoissonProblem(Grid(f)), cfg, w, precision="fp16")
+    assert [r.operator for r in l16.records] == [r.operator for r in l32.records]
+    assert l16.iterations == l32.iterations and l16.converged(1e-10)
