@@ -422,7 +422,7 @@ def main():
         line = {
             "metric": METRIC, "value": cyc_s, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": res["ms_total"] / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64+bf16" if args.mode == "gan" else "f64",
+            "scaling": "weak", "vs_baseline": None, "dtype": f"f64+{args.precision}" if args.mode == "gan" else "f64",
             "data": "synthetic (seeded GRF k^-5/3 + blobs RHS; seeded He-init generator weights)",
             "config": workload_config(args), "gupdates_per_s": cyc_s * n * n / 1e9,
             "roofline": roof, "clocks": res["clocks"],

@@ -59,9 +59,14 @@ __device__ __forceinline__ double warp_sum(double v) {
 // fixed-order partial; the last block to arrive (ticket counter) sums the
 // partials in index order and writes result[k] = total_k * scale.  Bitwise
 // reproducible for a fixed launch geometry.  blockDim.x must be a multiple of 32.
+// grid_reduce_to: component k goes to *outs[k] * scales[k] (null outs[k] skipped;
+// all null -> no-op).  One fence + one ticket per block for all NV sums.
 template <int NV>
-__device__ void grid_reduce(double (&v)[NV], RedSlot slot, double *result, double scale) {
-    if (result == nullptr) return;   // uniform across the grid
+__device__ void grid_reduce_to(double (&v)[NV], RedSlot slot, double *const (&outs)[NV], const double (&scales)[NV]) {
+    bool any = false;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) any |= outs[k] != nullptr;
+    if (!any) return;   // uniform across the grid
     __shared__ double sred[NV][32];
     __shared__ bool s_last;
     const int tid = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
@@ -109,10 +114,22 @@ __device__ void grid_reduce(double (&v)[NV], RedSlot slot, double *result, doubl
         for (int k = 0; k < NV; ++k) {
             double w = lane < nwarps ? sred[k][lane] : 0.0;
             w = warp_sum(w);
-            if (lane == 0) result[k] = w * scale;
+            if (lane == 0 && outs[k]) *outs[k] = w * scales[k];
         }
     }
     if (tid == 0) *slot.counter = 0u;
+}
+
+template <int NV>
+__device__ __forceinline__ void grid_reduce(double (&v)[NV], RedSlot slot, double *result, double scale) {
+    double *outs[NV];
+    double scales[NV];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+        outs[k] = result ? result + k : nullptr;
+        scales[k] = scale;
+    }
+    grid_reduce_to<NV>(v, slot, outs, scales);
 }
 
 // Source of a right-hand side: f_eff = (f - *shift) * scale when shift != null,

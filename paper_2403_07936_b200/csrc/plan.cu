@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <map>
 #include <string>
 #include <tuple>
@@ -242,6 +243,17 @@ extern "C" int mgsr_plan_vcycle(mgsr_plan *pl, double *p, const double *f, int32
     if (!pl || !p || !f) { set_error("bad argument"); return MGSR_E_BAD_ARG; }
     if (use_sr && !pl->gen) { set_error("SR prolongation requires generator weights"); return MGSR_E_BAD_ARG; }
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (std::getenv("MGSR_NO_GRAPH")) {
+        // eager issue of the same kernel sequence (profilers that cannot replay graph nodes)
+        const bool mk = pl->capturing_markers;
+        pl->capturing_markers = false;   // external event records exist only inside captures
+        int r = record_vcycle(pl, p, f, use_sr != 0, st);
+        pl->capturing_markers = mk;
+        if (r) return r;
+        if (stats_dev)
+            MGSR_CUDA_TRY(cudaMemcpyAsync(stats_dev, sc(pl, SC_STATS), 2 * sizeof(double), cudaMemcpyDeviceToDevice, st));
+        return MGSR_OK;
+    }
     auto key = std::make_tuple(p, f, int(use_sr != 0));
     auto it = pl->graphs.find(key);
     if (it == pl->graphs.end()) {
