@@ -177,6 +177,26 @@ def make_inputs(n: int, seed: int, mode: str):
     return f - f.mean(), p0 - p0.mean()
 
 
+def reduce_max(x: float, dist, device) -> float:
+    """Max over ranks (the timing rule: a multi-GPU number is the slowest rank's)."""
+    if dist is None:
+        return x
+    import torch
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def replica_value(steps: int, ms_max: float, world: int) -> float:
+    """Whole-job V-cycles/s of `world` independent replicas (weak scaling, replicas only)."""
+    return steps / (ms_max / 1e3) * world
+
+
+def replica_seed(rank: int) -> int:
+    """Each replica solves its own seeded right-hand side."""
+    return 1000 + rank
+
+
 def run_mine(args, rank: int, world: int, dist):
     import numpy as np
     import torch
@@ -191,7 +211,7 @@ def run_mine(args, rank: int, world: int, dist):
     weights = srmodel.random_weights(args.blocks, 0) if args.mode == "gan" else None
     op = "sr" if args.mode == "gan" else "spline"
     plan = VCyclePlan(n, cfg, weights, precision=args.precision, sr_levels=args.sr_levels)
-    f_np, p_np = make_inputs(n, 1000 + rank, args.mode)
+    f_np, p_np = make_inputs(n, replica_seed(rank), args.mode)
     f = torch.from_numpy(f_np).to(dev)
     p = torch.from_numpy(p_np).to(dev)
     lib = _lib.load()
@@ -258,16 +278,9 @@ def run_mine(args, rank: int, world: int, dist):
         e2e_ms = e0.elapsed_time(e1)
         e2e = (k2, e2e_ms, 2 * 8 * n * n, 8 * n * n + 16)
 
-    def gather_max(x):
-        if dist is None:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
-
-    ms_total = gather_max(ms_total)
+    ms_total = reduce_max(ms_total, dist, dev)
     if e2e is not None:
-        e2e = (e2e[0], gather_max(e2e[1]), e2e[2], e2e[3])
+        e2e = (e2e[0], reduce_max(e2e[1], dist, dev), e2e[2], e2e[3])
     return dict(ms_total=ms_total, gen_ms=gen_ms, gs_ms=gs_ms, cyc_ms=cyc_ms, kernels=kernels_per_cycle,
                 e2e=e2e, clocks=clk.summary(), stats=stats.tolist())
 
@@ -399,7 +412,7 @@ def main():
     if rank == 0:
         peaks, peak_kind = measured_peaks()
         n = args.n
-        cyc_s = args.steps / (res["ms_total"] / 1e3) * world
+        cyc_s = replica_value(args.steps, res["ms_total"], world)
         if args.mode == "gan":
             flops = pass_flops_fast(n // 2, args.blocks)
             ach = flops / (res["gen_ms"] / 1e3) / 1e12 if res["gen_ms"] > 0 else 0.0
@@ -431,7 +444,7 @@ def main():
         }
         if res["e2e"] is not None:
             k2, ms, bi, bo = res["e2e"]
-            line["e2e"] = {"value": k2 / (ms / 1e3) * world, "unit": UNIT, "h2d_bytes_per_step": bi,
+            line["e2e"] = {"value": replica_value(k2, ms, world), "unit": UNIT, "h2d_bytes_per_step": bi,
                            "d2h_bytes_per_step": bo,
                            "path": "pinned host p,f -> torch.ops.mgsr.vcycle_ (C ABI mgsr_plan_vcycle) -> host p"}
         if not args.no_cpu_baseline:

@@ -159,3 +159,30 @@ def test_product_package_never_imports_oracle():
             if f.endswith((".py", ".cu", ".cuh")):
                 text = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in text and "from oracle" not in text, f
+
+
+def test_replicas_gloo_world2(tmp_path):
+    """bench.py --gpus 2 host logic on CPU: two gloo ranks (127.0.0.1), max-over-ranks
+    time, whole-job value = replicas x steps / max time, distinct seeded inputs per rank."""
+    import json
+    import socket
+    import subprocess
+    import sys
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    procs = []
+    for r in range(2):
+        env = dict(os.environ, RANK=str(r), WORLD_SIZE="2", LOCAL_RANK=str(r), MASTER_ADDR="127.0.0.1",
+                   MASTER_PORT=str(port), PYTHONPATH=ROOT)
+        procs.append(subprocess.Popen([sys.executable, os.path.join(ROOT, "tests", "_replica_worker.py"),
+                                       str(tmp_path)], env=env))
+    for pr in procs:
+        assert pr.wait(timeout=240) == 0
+    res = [json.load(open(tmp_path / f"rank{r}.json")) for r in range(2)]
+    for r in res:
+        assert r["ms"] == 150.0                        # the slower rank's time, on every rank
+        assert abs(r["value"] - 2 * 10 / 0.150) < 1e-9
+        assert abs(r["f_mean"]) < 1e-12                # mean-free RHS
+    d = res[0]["digests"]
+    assert d == res[1]["digests"] and d[0] != d[1]     # each replica solves its own RHS
