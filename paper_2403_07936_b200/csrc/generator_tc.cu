@@ -81,15 +81,16 @@ static_assert(I2C_BYTES <= UNION_BYTES, "union");
 // pixel stride (conflict-free ldmatrix rows), double-buffered over tiles; tail weights of the quarter
 // bf16 [tap 81][o 3][16 ch] (double-buffered over quarters); a zero row; the reduction scratch.
 constexpr int UQ = 16;
+constexpr int UP_QUARTERS_C = 4;
 constexpr int U_PIX_B = 48;
 constexpr int U_TILE_BYTES = WPT * 144 * U_PIX_B;      // 13824
 
 constexpr int U_OFF0 = 0;
 constexpr int TW_OFF0 = 2 * U_TILE_BYTES;              // 27648
-constexpr int ZERO_OFF = TW_OFF0 + 2 * 7808;           // 43264 (TW slots padded to 16 B multiples)
-constexpr int RED_OFF = ZERO_OFF + 64;                 // 43328
-constexpr int TAIL_UNITS = 2 * 9;                      // (window, dy) per tile
-constexpr int RED_BYTES = 32 * 16 * 8 * 4;             // 16384
+constexpr int TW_SLOTS = UP_QUARTERS_C;                // one tail-weight slot per up quarter
+constexpr int ZERO_OFF = TW_OFF0 + TW_SLOTS * 7808;    // 58880
+constexpr int RED_OFF = ZERO_OFF + 64;                 // 58944
+constexpr int RED_BYTES = 16 * 16 * 8 * 4;             // 8192: [unit 16][row 16][8] fp32
 static_assert(RED_OFF + RED_BYTES <= UNION_BYTES, "union");
 constexpr int OFF_ACT = 0;
 constexpr int OFF_RING = OFF_ACT + ACT_BYTES;
@@ -315,7 +316,22 @@ struct Params {
     size_t wfmt;        // byte offset of the operand-format weight set (0: bf16, BL.fmt_stride: fp16)
     float *dbg;
     int dbg_layer;
-    unsigned long long *prof;   // optional wait-cycle counters (bring-up instrumentation)
+    unsigned long long *prof;   // optional event trace (bring-up instrumentation, tests/tc_trace.py)
+};
+
+// Event trace of one steady-state group of CTA 0: role r (0 producer, 1 MMA, 2 epilogue warp 2,
+// 3 epilogue warp 10) appends (id, clock64) pairs at prof[r * 4096 + 2 i]; id = type * 1000 + a * 10 + b.
+constexpr int TRACE_GROUP = 3;
+struct Tracer {
+    unsigned long long *buf;
+    int n;
+    __device__ __forceinline__ void operator()(int type, int a, int b) {
+        if (buf && n < 2040) {
+            buf[2 * n] = (unsigned long long)(type * 1000 + a * 10 + b);
+            buf[2 * n + 1] = (unsigned long long)clock64();
+            ++n;
+        }
+    }
 };
 
 // window geometry of a global window index (srmodel.py:414-440)
@@ -401,6 +417,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
     const uint32_t b_act_ready = smem_u32(bars + 2 * NSLOT + 5);   // [T] epilogue -> MMA: accumulator drained, act written
     const uint32_t b_ubuf_full = smem_u32(bars + 2 * NSLOT + 8);   // [2] drain warps -> tail warps: U buffer written
     const uint32_t b_ubuf_free = smem_u32(bars + 2 * NSLOT + 10);  // [2] tail warps -> drain warps: U buffer consumed
+    const uint32_t b_tw_full = smem_u32(bars + 2 * NSLOT + 25);    // [4] producer -> tail warps: quarter weights landed
+    const uint32_t b_tw_empty = smem_u32(bars + 2 * NSLOT + 29);   // [4] tail warps -> producer: fragments taken
+    const uint32_t b_drained = smem_u32(bars + 2 * NSLOT + 16);    // [2][T] drain warps -> MMA: up accumulator buffer free
+    const uint32_t b_acc_full2 = smem_u32(bars + 2 * NSLOT + 22);  // [T] MMA -> drain: up accumulator buffer 1 ready
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int NL = P.nl, NLAYERS = P.nl;
@@ -426,6 +446,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
                 mbar_init(b_ubuf_full + 8 * t, NEPI / 2);
                 mbar_init(b_ubuf_free + 8 * t, NEPI / 2);
             }
+            mbar_init(b_drained + 8 * t, NEPI / 2);
+            mbar_init(b_acc_full2 + 8 * t, 1);
+            mbar_init(b_drained + 8 * (T + t), NEPI / 2);
+        }
+        for (int u = 0; u < UP_QUARTERS_C; ++u) {
+            mbar_init(b_tw_full + 8 * u, 1);
+            mbar_init(b_tw_empty + 8 * u, NEPI / 2);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -443,8 +470,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
         // ================= weight producer =================
         uint32_t ph = 0;   // bit s = fill parity of slot s
         int slot = 0;      // taps stream through the ring in order: slot = global tap index mod NSLOT
+        uint32_t tw_ph[UP_QUARTERS_C] = {0, 0, 0, 0};
+        Tracer tr{nullptr, 0};
+        int seq = 0;
         auto fill = [&](const uint8_t *src, uint32_t bytes = SLOT_BYTES) {
             mbar_wait(b_empty + 8 * slot, ((ph >> slot) & 1u) ^ 1u);
+            if (lane == 0) tr(1, seq / 10, seq % 10);
+            ++seq;
             if (elect_one()) {
                 mbar_expect_tx(b_full + 8 * slot, bytes);
                 bulk_g2s(smem_u32(ring + slot * SLOT_BYTES), src, bytes, b_full + 8 * slot);
@@ -454,45 +486,66 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
             slot = slot == NSLOT - 1 ? 0 : slot + 1;
         };
         for (int g = blockIdx.x; g < P.ngroups; g += gridDim.x) {
+            tr.buf = (P.prof && blockIdx.x == 0 && g == TRACE_GROUP * int(gridDim.x)) ? P.prof : nullptr;
+            seq = 0;
             for (int h = 0; h < 3; ++h)   // head weights: planes 0-7, 8-15, 16-21
                 fill(wblob + BL.head_b + h * SLOT_BYTES, h < 2 ? SLOT_BYTES : HB_BYTES - 2 * SLOT_BYTES);
             for (int L = 0; L < NLAYERS; ++L)
                 for (int tap = 0; tap < 9; ++tap) fill(wblob + P.wfmt + BL.body + (size_t(L) * 9 + tap) * SLOT_BYTES);
-            for (int u = 0; u < UP_QUARTERS; ++u)
+            for (int u = 0; u < UP_QUARTERS; ++u) {
+                {   // the quarter's tail weights -> TW[u] (union; free once last group's quarter u took them)
+                    const int ts = u;
+                    mbar_wait(b_tw_empty + 8 * ts, tw_ph[ts] ^ 1u);
+                    tw_ph[ts] ^= 1u;
+                    if (elect_one()) {
+                        mbar_expect_tx(b_tw_full + 8 * ts, 7808);
+                        bulk_g2s(smem_u32(uni + TW_OFF0 + ts * 7808), wblob + P.wfmt + BL.tail + size_t(u) * 7808, 7808,
+                                 b_tw_full + 8 * ts);
+                    }
+                    __syncwarp();
+                }
                 for (int tap = 0; tap < 9; ++tap) fill(wblob + P.wfmt + BL.up + (size_t(u) * 9 + tap) * SLOT_BYTES);
+            }
         }
     } else if (warp == 1) {
         // ================= MMA issuer (warp-uniform control, one elected lane issues) =================
         uint32_t ph = 0, i2c_ph = 0;
         int slot0 = 0;   // ring slot of tap 0 of the current layer
         uint32_t ar_ph[T] = {0, 0, 0};
+        uint32_t dr_ph = 0;   // bit t: parity of the next completion of b_drained[0][t]
         const uint32_t act_base = smem_u32(act), uni_base = smem_u32(uni), ring_base = smem_u32(ring);
         const uint32_t i2c_base = uni_base;
         const uint32_t id64 = F16 ? idesc_f16(64) : idesc_bf16(64);
         const uint64_t a_desc0 = make_desc(act_base, ACT_PLANE, 128);
         const uint64_t b_desc0 = make_desc(ring_base, 1024, 128);        // 3x3 tap: 64-row planes
-        long long w_act = 0, w_full = 0, t_start = clock64();
+        Tracer tr{nullptr, 0};
         // one N = 64 3x3 layer over the three tiles (body, post, up quarter)
-        long long t_head_m = 0, t_body_m = 0, t_up_m = 0;
-        auto conv_layer = [&]() {
+        // wait: 0 = act_ready (activations of this tile written), 1 = none, 2/3 = up accumulator
+        // buffer 0/1 of this tile drained
+        auto conv_layer = [&](int lid, int wait, uint32_t dcol) {
 #pragma unroll
             for (int t = 0; t < T; ++t) {
-                long long c0 = P.prof ? clock64() : 0;
-                mbar_wait(b_act_ready + 8 * t, ar_ph[t]);
-                if (P.prof) w_act += clock64() - c0;
-                ar_ph[t] ^= 1;
+                if (wait == 0) {
+                    mbar_wait(b_act_ready + 8 * t, ar_ph[t]);
+                    ar_ph[t] ^= 1;
+                } else if (wait == 2) {   // buffer 0: waited at every completion (u = 2 here, head next group)
+                    mbar_wait(b_drained + 8 * t, (dr_ph >> t) & 1u);
+                    dr_ph ^= 1u << t;
+                } else if (wait == 3) {   // buffer 1 completes twice per group (u = 1, 3 drained); only the
+                    mbar_wait(b_drained + 8 * (T + t), 0u);   // first is waited: always an even completion
+                }
+                if (lane == 0) tr(2, lid, t);
                 tc_fence_after();
                 const uint64_t a_t = a_desc0 + uint64_t(GUARD + t * ROWS);
-                const uint32_t d = tmem + COL_ACC + 64 * t;
+                const uint32_t d = tmem + dcol + 64 * t;
                 if (elect_one()) {
 #pragma unroll
                     for (int tap = 0; tap < 9; ++tap) {
                         int s = slot0 + tap;
                         s = s >= NSLOT ? s - NSLOT : s;
                         if (t == 0) {
-                            long long c1 = P.prof ? clock64() : 0;
                             mbar_wait(b_full + 8 * s, (ph >> s) & 1u);
-                            if (P.prof) w_full += clock64() - c1;
+                            if (tap == 0) tr(4, lid, 0);
                             tc_fence_after();
                         }
                         const int shift = (tap / 3 - 1) * 8 + (tap % 3 - 1);
@@ -504,9 +557,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
                                      id64, (tap | ks) > 0);
                         if (t == T - 1) umma_commit(b_empty + 8 * s);
                     }
-                    umma_commit(b_acc_full + 8 * t);
+                    // separate completion barriers per up buffer: a tile's two buffers may complete
+                    // back to back, which a single barrier could not tell apart
+                    umma_commit((dcol == COL_RES ? b_acc_full2 : b_acc_full) + 8 * t);
                 }
                 __syncwarp();
+                if (lane == 0) tr(3, lid, t);
             }
 #pragma unroll
             for (int tap = 0; tap < 9; ++tap) {
@@ -518,12 +574,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
             slot0 = slot0 >= NSLOT ? slot0 - NSLOT : slot0;
         };
         for (int g = blockIdx.x; g < P.ngroups; g += gridDim.x) {
+            tr.buf = (P.prof && blockIdx.x == 0 && g == TRACE_GROUP * int(gridDim.x)) ? P.prof + 4096 : nullptr;
             // head: D[t] = im2col(q) (128 x 88, tf32) x Wh^T (88 x 64)
-            const long long ph0 = P.prof ? clock64() : 0;
             for (int t = 0; t < T; ++t) {
-                mbar_wait(b_act_ready + 8 * t, ar_ph[t]);
-                ar_ph[t] ^= 1;
+                // the head accumulates into up buffer 0 of this tile (cols COL_ACC + 64 t)
+                mbar_wait(b_drained + 8 * t, (dr_ph >> t) & 1u);
+                dr_ph ^= 1u << t;
+                if (lane == 0) tr(2, 0, t);
                 mbar_wait(b_i2c_full, i2c_ph);
+                if (lane == 0) tr(5, 0, t);
                 i2c_ph ^= 1;
                 tc_fence_after();
                 const uint32_t d = tmem + COL_ACC + 64 * t;
@@ -545,6 +604,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
                     umma_commit(b_i2c_empty);
                 }
                 __syncwarp();
+                if (lane == 0) tr(3, 0, t);
             }
 #pragma unroll
             for (int h = 0; h < 3; ++h) {
@@ -554,25 +614,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
             }
             slot0 += 3;
             slot0 = slot0 >= NSLOT ? slot0 - NSLOT : slot0;
-            const long long ph1 = P.prof ? clock64() : 0;
 #pragma unroll 1
-            for (int L = 0; L < NLAYERS; ++L) conv_layer();
-            const long long ph2 = P.prof ? clock64() : 0;
-#pragma unroll 1
-            for (int u = 0; u < UP_QUARTERS; ++u) conv_layer();   // up quarters
-            if (P.prof) {
-                t_head_m += ph1 - ph0;
-                t_body_m += ph2 - ph1;
-                t_up_m += clock64() - ph2;
-            }
-        }
-        if (P.prof && lane == 0) {
-            atomicAdd(P.prof + 0, (unsigned long long)w_act);
-            atomicAdd(P.prof + 1, (unsigned long long)w_full);
-            atomicAdd(P.prof + 2, (unsigned long long)(clock64() - t_start));
-            atomicAdd(P.prof + 40, (unsigned long long)t_head_m);
-            atomicAdd(P.prof + 41, (unsigned long long)t_body_m);
-            atomicAdd(P.prof + 42, (unsigned long long)t_up_m);
+            for (int L = 0; L < NLAYERS; ++L) conv_layer(L + 1, 0, COL_ACC);
+            // up quarters, accumulators double-buffered over cols [0, 192) and [192, 384) (the residual
+            // stream and skip are dead after the post layer): quarter u + 1 runs while u drains
+            conv_layer(40, 0, COL_ACC);
+            conv_layer(41, 1, COL_RES);
+            conv_layer(42, 2, COL_ACC);
+            conv_layer(43, 3, COL_RES);
         }
     } else {
         // ================= epilogue (warps 2..17) =================
@@ -588,8 +637,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
         uint32_t af_ph[T] = {0, 0, 0};
         uint32_t i2c_empty_ph = 0;
         bool first_build = true;
-        if (lane == 0)
-            for (int t = 0; t < T; ++t) mbar_arrive(b_act_ready + 8 * t);   // accumulators start free
+        if (lane == 0 && ew < NEPI / 2)
+            for (int t = 0; t < T; ++t) mbar_arrive(b_drained + 8 * t);   // up buffer 0 (= head accumulator) starts free
         const float *head_a = cs;
         uint8_t *idx_tab = reinterpret_cast<uint8_t *>(smem + OFF_MISC + IDX_OFF);
         for (int i = et; i < 64 * HK; i += 32 * NEPI) {   // im2col index table (replicate-clamped 9x9 taps)
@@ -604,10 +653,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
         }
         const float *up_a = cs + 64 + 192 * NL;
         const float *tail_b = up_a + 64;
-        long long w_acc = 0, t_up = 0, e_q = 0, e_i2c = 0, e_head = 0, e_body = 0, e_end = 0;
+        Tracer tr{nullptr, 0};
+        uint32_t tw_full_ph = 0;   // tail warps: bit s = parity of the next completion of b_tw_full[s]
+        uint32_t af2_ph = 0;       // drain warps: bit t = parity of the next completion of b_acc_full2[t]
         for (int g = blockIdx.x; g < P.ngroups; g += gridDim.x) {
             const long long k0 = (long long)g * WPG;
-            long long ce0 = clock64();
+            tr.buf = (P.prof && blockIdx.x == 0 && g == TRACE_GROUP * int(gridDim.x) && lane == 0 &&
+                      (warp == 2 || warp == 10)) ? P.prof + (warp == 2 ? 2 : 3) * 4096 : nullptr;
+            tr(11, 0, 0);
             // ---- q tables of the 6 windows (fp64 normalise -> fp32) ----
             if (et < WPG * 36) {
                 const int wk = et / 36, pp = et % 36;
@@ -615,7 +668,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
                 misc[et] = __ldg(P.qgrid + (long long)(W.iw + pp / 6) * P.nc + W.jw + pp % 6);
             }
             epi_bar();
-            long long ce1 = clock64();
+            tr(11, 1, 0);
             // ---- head: im2col per tile (tf32) + head weights ----
             for (int t = 0; t < T; ++t) {
                 if (!first_build) {
@@ -643,16 +696,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
                 fence_async_smem();
                 epi_bar();
                 if (et == 0) mbar_arrive(b_i2c_full);
+                tr(12, 0, t);
             }
-            long long ce2 = clock64();
             // ---- head + body + post epilogues ----
-            long long ce3 = 0;
             for (int L = -1; L < NL; ++L) {
-                if (L == 0) ce3 = clock64();
                 for (int t = 0; t < T; ++t) {
-                    long long c2 = (P.prof && et == 0) ? clock64() : 0;
                     mbar_wait(b_acc_full + 8 * t, af_ph[t]);
-                    if (P.prof && et == 0) w_acc += clock64() - c2;
+                    tr(6, L + 1, t);
                     af_ph[t] ^= 1;
                     tc_fence_after();
                     uint32_t v[16];
@@ -728,6 +778,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(b_act_ready + 8 * t);
+                    tr(7, L + 1, t);
                 }
             }
             // ---- up quarters.  Roles split for this phase:
@@ -739,7 +790,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
             //    pixels, so no clamping), B = the tap's weights (n = o, 3 of 8 used); unit = (window, group of
             //    ~10 taps), two per warp; fp32 accumulators stay in registers across the four quarters.
             //  U buffers hand off through mbarriers (ubuf_full / ubuf_free), so draining runs ahead. ----
-            long long cu = (P.prof && et == 0) ? clock64() : 0;
             const uint32_t uni_s = smem_u32(uni);
             if (ew < NEPI / 2) {
                 const int ch = ew >> 2;   // column half: quarter columns 32 ch .. 32 ch + 31
@@ -750,20 +800,25 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
 #pragma unroll
                     for (int t = 0; t < T; ++t) {
                         const int step = u * T + t, ub = step & 1;
-                        mbar_wait(b_acc_full + 8 * t, af_ph[t]);
-                        af_ph[t] ^= 1;
+                        if (u & 1) {
+                            mbar_wait(b_acc_full2 + 8 * t, (af2_ph >> t) & 1u);
+                            af2_ph ^= 1u << t;
+                        } else {
+                            mbar_wait(b_acc_full + 8 * t, af_ph[t]);
+                            af_ph[t] ^= 1;
+                        }
+                        tr(8, u, t);
                         tc_fence_after();
                         uint32_t v0[16], v1[16];
-                        TMEM_LD16(tmem + lane_addr + COL_ACC + 64 * t + 32 * ch, v0);
-                        TMEM_LD16(tmem + lane_addr + COL_ACC + 64 * t + 32 * ch + 16, v1);
+                        const uint32_t ucol = (u & 1 ? COL_RES : COL_ACC) + 64 * t + 32 * ch;
+                        TMEM_LD16(tmem + lane_addr + ucol, v0);
+                        TMEM_LD16(tmem + lane_addr + ucol + 16, v1);
                         tmem_wait_ld();
                         tc_fence_before();
                         __syncwarp();
-                        if (lane == 0) {   // two arrivals: this phase has half the epilogue warps draining
-                            mbar_arrive(b_act_ready + 8 * t);
-                            mbar_arrive(b_act_ready + 8 * t);
-                        }
+                        if (lane == 0) mbar_arrive(b_drained + 8 * ((u & 1) * T + t));
                         mbar_wait(b_ubuf_free + 8 * ub, ((step >> 1) & 1) ^ 1);   // tail of step - 2 done
+                        tr(9, u, t);
                         if (interior) {
                             // column j = 32 ch + jj -> up channel 64 u + j -> shuffled c = 16 u + 8 ch + jj/4,
                             // sub-pixel (i, j') = ((jj >> 1) & 1, jj & 1)
@@ -806,13 +861,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
                         }
                         __syncwarp();
                         if (lane == 0) mbar_arrive(b_ubuf_full + 8 * ub);
+                        tr(10, u, t);
                     }
                 }
             } else {
                 const int tw = ew - NEPI / 2;                                        // 0..7
                 const int r = (lane & 7) + ((lane >> 3) & 1) * 8, kh = lane >> 4;   // A row / k half of this lane
                 const int n = lane & 7, kb = (lane >> 3) & 1;                      // B row / k half
-                float tacc[T][2][4];   // [tile][unit][fragment]
+                // this warp's tap group (the same for both windows of a tile): taps [tap_lo, tap_lo + ntap)
+                const int tap_lo = (81 * tw) >> 3, ntap = ((81 * (tw + 1)) >> 3) - tap_lo;   // 10 or 11
+                float tacc[T][2][4];   // [tile][window][fragment]
 #pragma unroll
                 for (int t = 0; t < T; ++t)
 #pragma unroll
@@ -820,41 +878,42 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
 #pragma unroll
                         for (int e = 0; e < 4; ++e) tacc[t][k][e] = 0.f;
                 if (tw == 0 && lane < 4) reinterpret_cast<uint4 *>(uni + ZERO_OFF)[lane] = make_uint4(0, 0, 0, 0);
+                asm volatile("bar.sync 2, 256;" ::: "memory");   // zero row visible
+                const uint32_t arow = uint32_t((r >> 2) * 12 + (r & 3)) * U_PIX_B + kh * 16;
                 for (int u = 0; u < UP_QUARTERS; ++u) {
-                    {   // tail weights of this quarter -> TW[u & 1]
-                        const uint4 *src = reinterpret_cast<const uint4 *>(P.blob + P.wfmt + BL.tail + size_t(u) * 7808);
-                        uint4 *dst = reinterpret_cast<uint4 *>(uni + TW_OFF0 + (u & 1) * 7808);
-                        for (int i = et - 256; i < 7808 / 16; i += 256) dst[i] = src[i];
-                    }
-                    asm volatile("bar.sync 2, 256;" ::: "memory");   // TW ready; every tail warp left quarter u-1
-                    const uint32_t tw_s = uni_s + TW_OFF0 + (u & 1) * 7808;
-                    const uint32_t b0 = n < 3 ? tw_s + uint32_t(n * 32 + kb * 16) : uni_s + ZERO_OFF;
+                    // the quarter's tail weights (TW[u], filled by the producer)
+                    const int ts = u;
+                    mbar_wait(b_tw_full + 8 * ts, (tw_full_ph >> ts) & 1u);
+                    tw_full_ph ^= 1u << ts;
+                    const uint32_t tw_s = uni_s + TW_OFF0 + ts * 7808;
                     const uint32_t bstep = n < 3 ? 3 * 32 : 0;
+                    const uint32_t b0 = (n < 3 ? tw_s + uint32_t(n * 32 + kb * 16) : uni_s + ZERO_OFF) + tap_lo * bstep;
 #pragma unroll
                     for (int t = 0; t < T; ++t) {
                         const int step = u * T + t, ub = step & 1;
                         mbar_wait(b_ubuf_full + 8 * ub, (step >> 1) & 1);
+                        tr(13, u, t);
                         const Win W0 = window_of(P, k0 + t * WPT), W1 = window_of(P, k0 + t * WPT + 1);
-#pragma unroll
-                        for (int k = 0; k < 2; ++k) {
-                            const int unit = tw + 8 * k, w = unit >> 3, grp = unit & 7;
-                            const Win Wn = w ? W1 : W0;
-                            if (Wn.valid && !Wn.edge) {
-                                const uint32_t a0 = uni_s + U_OFF0 + ub * U_TILE_BYTES + w * (144 * U_PIX_B) +
-                                                    uint32_t((r >> 2) * 12 + (r & 3)) * U_PIX_B + kh * 16;
-                                const int tap_lo = (81 * grp) >> 3, tap_hi = (81 * (grp + 1)) >> 3;
-                                int dy = tap_lo / 9, dx = tap_lo - 9 * dy;
-                                for (int tap = tap_lo; tap < tap_hi; ++tap) {
-                                    uint32_t a[4], bb[2];
-                                    ldsm_x4(a0 + uint32_t(dy * 12 + dx) * U_PIX_B, a);
-                                    ldsm_x2(b0 + uint32_t(tap) * bstep, bb);
-                                    mma_16816<F16>(tacc[t][k], a, bb);
-                                    if (++dx == 9) { dx = 0; ++dy; }
-                                }
-                            }
+                        const bool v0 = W0.valid && !W0.edge, v1 = W1.valid && !W1.edge;
+                        const uint32_t a0 = uni_s + U_OFF0 + ub * U_TILE_BYTES + arow;
+                        const uint32_t a1 = a0 + 144 * U_PIX_B;
+                        // two independent accumulation chains (the two windows), interleaved
+                        int dy = tap_lo / 9, dx = tap_lo - 9 * dy;
+#pragma unroll 1
+                        for (int j = 0; j < ntap; ++j) {
+                            const uint32_t ao = uint32_t(dy * 12 + dx) * U_PIX_B;
+                            uint32_t fa[4], fb[4], bb[2];
+                            ldsm_x2(b0 + uint32_t(j) * bstep, bb);
+                            if (v0) ldsm_x4(a0 + ao, fa);
+                            if (v1) ldsm_x4(a1 + ao, fb);
+                            if (v0) mma_16816<F16>(tacc[t][0], fa, bb);
+                            if (v1) mma_16816<F16>(tacc[t][1], fb, bb);
+                            if (++dx == 9) { dx = 0; ++dy; }
                         }
                         __syncwarp();
                         if (lane == 0) mbar_arrive(b_ubuf_free + 8 * ub);
+                        if (t == T - 1 && lane == 0) mbar_arrive(b_tw_empty + 8 * ts);   // quarter's TW consumed
+                        tr(14, u, t);
                         if (u == UP_QUARTERS - 1) {
                             const int gq = lane >> 2, tq = lane & 3;
 #pragma unroll
@@ -890,22 +949,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
                     }
                 }
             }
-            long long ce5 = clock64();
-            if (P.prof && (et == 0 || et == 256)) {
-                e_q += ce1 - ce0; e_i2c += ce2 - ce1; e_head += ce3 - ce2; e_body += cu - ce3; t_up += ce5 - cu;
-            }
+            tr(15, 0, 0);
             epi_bar();
-            if (P.prof && (et == 0 || et == 256)) e_end += clock64() - ce5;
-        }
-        if (P.prof && (et == 0 || et == 256)) {
-            const int o = et == 0 ? 0 : 8;
-            if (et == 0) atomicAdd(P.prof + 3, (unsigned long long)w_acc);
-            atomicAdd(P.prof + 4 + o, (unsigned long long)t_up);
-            atomicAdd(P.prof + 20 + o, (unsigned long long)e_q);
-            atomicAdd(P.prof + 21 + o, (unsigned long long)e_i2c);
-            atomicAdd(P.prof + 22 + o, (unsigned long long)e_head);
-            atomicAdd(P.prof + 23 + o, (unsigned long long)e_body);
-            atomicAdd(P.prof + 24 + o, (unsigned long long)e_end);
+            tr(15, 1, 0);
         }
     }
     // teardown
@@ -1181,12 +1227,12 @@ extern "C" int mgsr_debug_tc_pass(const mgsr_gen *g, const double *c, int64_t nc
 }
 
 extern "C" int mgsr_debug_tc_prof(const mgsr_gen *g, const double *c, int64_t nc, double *fine,
-                                  unsigned long long *prof, void *stream) {
+                                  unsigned long long *prof, int32_t f16, void *stream) {
     const size_t wsb = mgsr::tc_workspace_bytes(nc);
     void *ws = nullptr;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (cudaMallocAsync(&ws, wsb, st) != cudaSuccess) return MGSR_E_CUDA;
-    int r = mgsr::launch_sr_pass_tc_dbg(g, c, nullptr, int(nc), -10.0, 7.0, fine, ws, wsb, nullptr, -1, st, prof);
+    int r = mgsr::launch_sr_pass_tc_dbg(g, c, nullptr, int(nc), -10.0, 7.0, fine, ws, wsb, nullptr, -1, st, prof, f16);
     cudaFreeAsync(ws, st);
     return r;
 }
