@@ -64,17 +64,21 @@ constexpr int GUARD = 16;            // guard rows around the act planes (tap sh
 constexpr int PLANE_ROWS = GUARD + T * ROWS + GUARD;
 constexpr int ACT_PLANE = PLANE_ROWS * 16;            // bytes per 8-channel plane
 constexpr int ACT_BYTES = 8 * ACT_PLANE;              // 55296
-constexpr int NSLOT = 10;                             // ring slots (> 9: next layer's first taps prefetch)
-constexpr int SLOT_BYTES = 8192;                      // 64 oc x 64 ic bf16 (one 3x3 tap)
-constexpr int RING_BYTES = NSLOT * SLOT_BYTES;        // 73728
+// CTA pair (cta_group::2): the leader CTA issues M = 256 MMAs whose A rows come 128 from each CTA's
+// activations and whose B (N = 64 output channels) is split along N, 32 channels in each CTA's ring.
+constexpr int NSLOT = 20;                             // ring slots (> 9: next layer's first taps prefetch)
+constexpr int TAP_BYTES = 8192;                       // one 3x3 tap in the blob: [half][32 oc][64 ic] bf16
+constexpr int SLOT_BYTES = 4096;                      // this CTA's half of a tap
+constexpr int RING_BYTES = NSLOT * SLOT_BYTES;        // 81920
 constexpr int UNION_BYTES = 69632;
 constexpr int MISC_BYTES = 8192;                      // q tables (6 x 36 floats) + head im2col index table
-constexpr int BAR_BYTES = 512;
+constexpr int BAR_BYTES = 1024;
 // union, head phase
 constexpr int HK = 88;                                   // head K (81 taps padded to a tf32 K multiple)
 constexpr int HPLANES = HK / 4;                          // 22 planes of 4 tf32
 constexpr int I2C_BYTES = HPLANES * ROWS * 16;           // 45056
-constexpr int HB_BYTES = HPLANES * 64 * 16;              // 22528, streamed through the ring (3 slots)
+constexpr int HB_BYTES = HPLANES * 64 * 16;              // 22528: two halves of 32 oc
+constexpr int HB_HALF = HB_BYTES / 2;                    // 11264, streamed through the ring (3 slots)
 constexpr int IDX_OFF = 1024;                            // in misc: uint8 [64 padded pixels][88 k] -> q index
 static_assert(I2C_BYTES <= UNION_BYTES, "union");
 // up phase (union): the up-conv quarter, pixel-shuffled, bf16 [window][12x12][16 ch] with a 48-byte
@@ -121,8 +125,8 @@ __host__ __device__ inline BlobLayout blob_layout(int blocks) {
     L.nl = 2 * blocks + 1;
     L.head_b = 0;
     L.body = L.head_b + HB_BYTES;
-    L.up = L.body + size_t(L.nl) * 9 * SLOT_BYTES;
-    L.tail = L.up + size_t(UP_QUARTERS) * 9 * SLOT_BYTES;
+    L.up = L.body + size_t(L.nl) * 9 * TAP_BYTES;
+    L.tail = L.up + size_t(UP_QUARTERS) * 9 * TAP_BYTES;
     L.tail_f32 = L.tail + size_t(UP_QUARTERS) * 7808;   // then [3][64][81] fp32 (edge kernel)
     L.consts = L.tail_f32 + sizeof(float) * 3 * 64 * 81;
     // fp16 operand set (body, up, tail) follows at +fmt_stride from the bf16 set
@@ -173,17 +177,35 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t addr, uint32_t lbo, uint3
 __device__ __forceinline__ void mma_bf16(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
     asm volatile(
         "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
         "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
 __device__ __forceinline__ void mma_tf32(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
     asm volatile(
         "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
         "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
+// completion of the pair's MMAs -> the barrier at this offset in BOTH CTAs
 __device__ __forceinline__ void umma_commit(uint32_t bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
+        "h"((unsigned short)3)
+        : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// arrive on the leader CTA's barrier at this offset (the leader's MMA warp waits on it)
+__device__ __forceinline__ void mbar_arrive_leader(uint32_t bar) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(bar));
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(r) : "memory");   // .release.cta (as CUTLASS)
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -288,15 +310,15 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
 __device__ __forceinline__ float bf16_lo(uint32_t u) { return __uint_as_float(u << 16); }
 __device__ __forceinline__ float bf16_hi(uint32_t u) { return __uint_as_float(u & 0xFFFF0000u); }
 
-// instruction descriptors: D fp32, K-major A and B, M = 128
+// instruction descriptors: D fp32, K-major A and B, M = 256 (CTA pair)
 __host__ __device__ constexpr uint32_t idesc_bf16(int n) {
-    return (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(n >> 3) << 17) | (uint32_t(128 >> 4) << 24);
+    return (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(n >> 3) << 17) | (uint32_t(256 >> 4) << 24);
 }
 __host__ __device__ constexpr uint32_t idesc_f16(int n) {   // a/b format 0 = F16
-    return (1u << 4) | (uint32_t(n >> 3) << 17) | (uint32_t(128 >> 4) << 24);
+    return (1u << 4) | (uint32_t(n >> 3) << 17) | (uint32_t(256 >> 4) << 24);
 }
 __host__ __device__ constexpr uint32_t idesc_tf32(int n) {
-    return (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(n >> 3) << 17) | (uint32_t(128 >> 4) << 24);
+    return (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(n >> 3) << 17) | (uint32_t(256 >> 4) << 24);
 }
 
 struct Params {
@@ -408,19 +430,27 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
     float *misc = reinterpret_cast<float *>(smem + OFF_MISC);
     float *cs = reinterpret_cast<float *>(smem + OFF_CONST);
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + OFF_BAR);
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + OFF_BAR + 480);
-    const uint32_t b_full = smem_u32(bars + 0);         // [NSLOT]
-    const uint32_t b_empty = smem_u32(bars + NSLOT);    // [NSLOT]
-    const uint32_t b_i2c_full = smem_u32(bars + 2 * NSLOT);
-    const uint32_t b_i2c_empty = smem_u32(bars + 2 * NSLOT + 1);
-    const uint32_t b_acc_full = smem_u32(bars + 2 * NSLOT + 2);    // [T] MMA -> epilogue: accumulator ready
-    const uint32_t b_act_ready = smem_u32(bars + 2 * NSLOT + 5);   // [T] epilogue -> MMA: accumulator drained, act written
-    const uint32_t b_ubuf_full = smem_u32(bars + 2 * NSLOT + 8);   // [2] drain warps -> tail warps: U buffer written
-    const uint32_t b_ubuf_free = smem_u32(bars + 2 * NSLOT + 10);  // [2] tail warps -> drain warps: U buffer consumed
-    const uint32_t b_tw_full = smem_u32(bars + 2 * NSLOT + 25);    // [4] producer -> tail warps: quarter weights landed
-    const uint32_t b_tw_empty = smem_u32(bars + 2 * NSLOT + 29);   // [4] tail warps -> producer: fragments taken
-    const uint32_t b_drained = smem_u32(bars + 2 * NSLOT + 16);    // [2][T] drain warps -> MMA: up accumulator buffer free
-    const uint32_t b_acc_full2 = smem_u32(bars + 2 * NSLOT + 22);  // [T] MMA -> drain: up accumulator buffer 1 ready
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + OFF_BAR + BAR_BYTES - 8);
+    // Barriers marked (leader) are waited on by the leader's MMA warp only and collect the arrivals of
+    // both CTAs; (both) are signalled in both CTAs by the leader's multicast commits; the rest are local.
+    const uint32_t b_full = smem_u32(bars + 0);                     // [NSLOT] this CTA's ring slot landed
+    const uint32_t b_empty = smem_u32(bars + NSLOT);                // [NSLOT] (both) slot consumed
+    const uint32_t b_peerfull = smem_u32(bars + 2 * NSLOT);         // [NSLOT] (leader) peer's slot landed
+    constexpr int BB = 3 * NSLOT;
+    const uint32_t b_i2c_full = smem_u32(bars + BB);                // (leader) both im2cols built
+    const uint32_t b_i2c_empty = smem_u32(bars + BB + 1);           // (both)
+    const uint32_t b_acc_full = smem_u32(bars + BB + 2);    // [T] (both) MMA -> epilogue: accumulator ready
+    const uint32_t b_act_ready = smem_u32(bars + BB + 5);   // [T] (leader) epilogues -> MMA: act written
+    const uint32_t b_ubuf_full = smem_u32(bars + BB + 8);   // [2] drain warps -> tail warps: U buffer written
+    const uint32_t b_ubuf_free = smem_u32(bars + BB + 10);  // [2] tail warps -> drain warps: U buffer consumed
+    const uint32_t b_tw_full = smem_u32(bars + BB + 25);    // [4] producer -> tail warps: quarter weights landed
+    const uint32_t b_tw_empty = smem_u32(bars + BB + 29);   // [4] tail warps -> producer: fragments taken
+    const uint32_t b_drained = smem_u32(bars + BB + 16);    // [2][T] (leader) drain warps -> MMA: up buffer free
+    const uint32_t b_acc_full2 = smem_u32(bars + BB + 22);  // [T] (both) MMA -> drain: up accumulator buffer 1 ready
+    const uint32_t rank = cluster_rank();
+    const bool leader = rank == 0;
+    const int pair = int(blockIdx.x >> 1), npairs = int(gridDim.x >> 1);
+    const int ngp = (P.ngroups + 1) >> 1;   // the pair processes groups 2 gp (leader) and 2 gp + 1 (peer)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int NL = P.nl, NLAYERS = P.nl;
@@ -436,19 +466,20 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
         for (int s = 0; s < NSLOT; ++s) {
             mbar_init(b_full + 8 * s, 1);
             mbar_init(b_empty + 8 * s, 1);
+            mbar_init(b_peerfull + 8 * s, 1);
         }
-        mbar_init(b_i2c_full, 1);
+        mbar_init(b_i2c_full, 2);
         mbar_init(b_i2c_empty, 1);
         for (int t = 0; t < T; ++t) {
             mbar_init(b_acc_full + 8 * t, 1);
-            mbar_init(b_act_ready + 8 * t, NEPI);
+            mbar_init(b_act_ready + 8 * t, 2 * NEPI);
             if (t < 2) {
                 mbar_init(b_ubuf_full + 8 * t, NEPI / 2);
                 mbar_init(b_ubuf_free + 8 * t, NEPI / 2);
             }
-            mbar_init(b_drained + 8 * t, NEPI / 2);
+            mbar_init(b_drained + 8 * t, NEPI);
             mbar_init(b_acc_full2 + 8 * t, 1);
-            mbar_init(b_drained + 8 * (T + t), NEPI / 2);
+            mbar_init(b_drained + 8 * (T + t), NEPI);
         }
         for (int u = 0; u < UP_QUARTERS_C; ++u) {
             mbar_init(b_tw_full + 8 * u, 1);
@@ -456,13 +487,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+    if (warp == 1) {   // both CTAs of the pair, same warp
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                      "r"(512));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
     }
     tc_fence_before();
-    __syncthreads();
+    cluster_sync();   // barriers of both CTAs initialised before any remote arrive
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
@@ -485,13 +516,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
             ph ^= 1u << slot;
             slot = slot == NSLOT - 1 ? 0 : slot + 1;
         };
-        for (int g = blockIdx.x; g < P.ngroups; g += gridDim.x) {
-            tr.buf = (P.prof && blockIdx.x == 0 && g == TRACE_GROUP * int(gridDim.x)) ? P.prof : nullptr;
+        for (int gp = pair; gp < ngp; gp += npairs) {
+            tr.buf = (P.prof && blockIdx.x == 0 && gp == TRACE_GROUP * npairs) ? P.prof : nullptr;
             seq = 0;
-            for (int h = 0; h < 3; ++h)   // head weights: planes 0-7, 8-15, 16-21
-                fill(wblob + BL.head_b + h * SLOT_BYTES, h < 2 ? SLOT_BYTES : HB_BYTES - 2 * SLOT_BYTES);
+            for (int h = 0; h < 3; ++h)   // this CTA's half of the head weights: planes 0-7, 8-15, 16-21
+                fill(wblob + BL.head_b + rank * HB_HALF + h * SLOT_BYTES, h < 2 ? SLOT_BYTES : HB_HALF - 2 * SLOT_BYTES);
             for (int L = 0; L < NLAYERS; ++L)
-                for (int tap = 0; tap < 9; ++tap) fill(wblob + P.wfmt + BL.body + (size_t(L) * 9 + tap) * SLOT_BYTES);
+                for (int tap = 0; tap < 9; ++tap)
+                    fill(wblob + P.wfmt + BL.body + (size_t(L) * 9 + tap) * TAP_BYTES + rank * SLOT_BYTES);
             for (int u = 0; u < UP_QUARTERS; ++u) {
                 {   // the quarter's tail weights -> TW[u] (union; free once last group's quarter u took them)
                     const int ts = u;
@@ -504,11 +536,25 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
                     }
                     __syncwarp();
                 }
-                for (int tap = 0; tap < 9; ++tap) fill(wblob + P.wfmt + BL.up + (size_t(u) * 9 + tap) * SLOT_BYTES);
+                for (int tap = 0; tap < 9; ++tap)
+                    fill(wblob + P.wfmt + BL.up + (size_t(u) * 9 + tap) * TAP_BYTES + rank * SLOT_BYTES);
             }
         }
+    } else if (warp == 1 && !leader) {
+        // ================= peer: forward "slot landed" to the leader =================
+        uint32_t ph = 0;
+        int slot = 0;
+        const int fills = 3 + (NLAYERS + UP_QUARTERS) * 9;
+        for (int gp = pair; gp < ngp; gp += npairs)
+            for (int i = 0; i < fills; ++i) {
+                mbar_wait(b_full + 8 * slot, (ph >> slot) & 1u);
+                if (elect_one()) mbar_arrive_leader(b_peerfull + 8 * slot);
+                __syncwarp();
+                ph ^= 1u << slot;
+                slot = slot == NSLOT - 1 ? 0 : slot + 1;
+            }
     } else if (warp == 1) {
-        // ================= MMA issuer (warp-uniform control, one elected lane issues) =================
+        // ================= MMA issuer (leader; warp-uniform control, one elected lane issues) =================
         uint32_t ph = 0, i2c_ph = 0;
         int slot0 = 0;   // ring slot of tap 0 of the current layer
         uint32_t ar_ph[T] = {0, 0, 0};
@@ -517,7 +563,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
         const uint32_t i2c_base = uni_base;
         const uint32_t id64 = F16 ? idesc_f16(64) : idesc_bf16(64);
         const uint64_t a_desc0 = make_desc(act_base, ACT_PLANE, 128);
-        const uint64_t b_desc0 = make_desc(ring_base, 1024, 128);        // 3x3 tap: 64-row planes
+        const uint64_t b_desc0 = make_desc(ring_base, 512, 128);         // half tap: 32-row planes
         Tracer tr{nullptr, 0};
         // one N = 64 3x3 layer over the three tiles (body, post, up quarter)
         // wait: 0 = act_ready (activations of this tile written), 1 = none, 2/3 = up accumulator
@@ -545,6 +591,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
                         s = s >= NSLOT ? s - NSLOT : s;
                         if (t == 0) {
                             mbar_wait(b_full + 8 * s, (ph >> s) & 1u);
+                            mbar_wait(b_peerfull + 8 * s, (ph >> s) & 1u);
                             if (tap == 0) tr(4, lid, 0);
                             tc_fence_after();
                         }
@@ -553,7 +600,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
                         const uint64_t b = b_desc0 + uint64_t(s * (SLOT_BYTES / 16));
 #pragma unroll
                         for (int ks = 0; ks < 4; ++ks)
-                            mma_bf16(d, a + uint64_t(ks * (2 * ACT_PLANE / 16)), b + uint64_t(ks * (2 * 1024 / 16)),
+                            mma_bf16(d, a + uint64_t(ks * (2 * ACT_PLANE / 16)), b + uint64_t(ks * (2 * 512 / 16)),
                                      id64, (tap | ks) > 0);
                         if (t == T - 1) umma_commit(b_empty + 8 * s);
                     }
@@ -573,8 +620,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
             slot0 += 9;
             slot0 = slot0 >= NSLOT ? slot0 - NSLOT : slot0;
         };
-        for (int g = blockIdx.x; g < P.ngroups; g += gridDim.x) {
-            tr.buf = (P.prof && blockIdx.x == 0 && g == TRACE_GROUP * int(gridDim.x)) ? P.prof + 4096 : nullptr;
+        for (int gp = pair; gp < ngp; gp += npairs) {
+            tr.buf = (P.prof && blockIdx.x == 0 && gp == TRACE_GROUP * npairs) ? P.prof + 4096 : nullptr;
             // head: D[t] = im2col(q) (128 x 88, tf32) x Wh^T (88 x 64)
             for (int t = 0; t < T; ++t) {
                 // the head accumulates into up buffer 0 of this tile (cols COL_ACC + 64 t)
@@ -593,10 +640,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
                         sl = sl >= NSLOT ? sl - NSLOT : sl;
                         if (t == 0 && (ks & 3) == 0) {
                             mbar_wait(b_full + 8 * sl, (ph >> sl) & 1u);
+                            mbar_wait(b_peerfull + 8 * sl, (ph >> sl) & 1u);
                             tc_fence_after();
                         }
                         uint64_t a = make_desc(i2c_base + 2 * ks * (ROWS * 16), ROWS * 16, 128);
-                        uint64_t b = make_desc(ring_base + sl * SLOT_BYTES + (ks & 3) * 2048, 64 * 16, 128);
+                        uint64_t b = make_desc(ring_base + sl * SLOT_BYTES + (ks & 3) * 1024, 32 * 16, 128);
                         mma_tf32(d, a, b, idesc_tf32(64), ks > 0);
                         if (t == T - 1 && ((ks & 3) == 3 || ks == HK / 8 - 1)) umma_commit(b_empty + 8 * sl);
                     }
@@ -638,7 +686,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
         uint32_t i2c_empty_ph = 0;
         bool first_build = true;
         if (lane == 0 && ew < NEPI / 2)
-            for (int t = 0; t < T; ++t) mbar_arrive(b_drained + 8 * t);   // up buffer 0 (= head accumulator) starts free
+            for (int t = 0; t < T; ++t) mbar_arrive_leader(b_drained + 8 * t);   // up buffer 0 (= head accumulator) starts free
         const float *head_a = cs;
         uint8_t *idx_tab = reinterpret_cast<uint8_t *>(smem + OFF_MISC + IDX_OFF);
         for (int i = et; i < 64 * HK; i += 32 * NEPI) {   // im2col index table (replicate-clamped 9x9 taps)
@@ -656,9 +704,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
         Tracer tr{nullptr, 0};
         uint32_t tw_full_ph = 0;   // tail warps: bit s = parity of the next completion of b_tw_full[s]
         uint32_t af2_ph = 0;       // drain warps: bit t = parity of the next completion of b_acc_full2[t]
-        for (int g = blockIdx.x; g < P.ngroups; g += gridDim.x) {
+        for (int gp = pair; gp < ngp; gp += npairs) {
+            const int g = 2 * gp + int(rank);
             const long long k0 = (long long)g * WPG;
-            tr.buf = (P.prof && blockIdx.x == 0 && g == TRACE_GROUP * int(gridDim.x) && lane == 0 &&
+            tr.buf = (P.prof && blockIdx.x == 0 && gp == TRACE_GROUP * npairs && lane == 0 &&
                       (warp == 2 || warp == 10)) ? P.prof + (warp == 2 ? 2 : 3) * 4096 : nullptr;
             tr(11, 0, 0);
             // ---- q tables of the 6 windows (fp64 normalise -> fp32) ----
@@ -695,7 +744,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
                 }
                 fence_async_smem();
                 epi_bar();
-                if (et == 0) mbar_arrive(b_i2c_full);
+                if (et == 0) mbar_arrive_leader(b_i2c_full);
                 tr(12, 0, t);
             }
             // ---- head + body + post epilogues ----
@@ -777,7 +826,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
                     fence_async_smem();
                     tc_fence_before();
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(b_act_ready + 8 * t);
+                    if (lane == 0) mbar_arrive_leader(b_act_ready + 8 * t);
                     tr(7, L + 1, t);
                 }
             }
@@ -816,7 +865,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
                         tmem_wait_ld();
                         tc_fence_before();
                         __syncwarp();
-                        if (lane == 0) mbar_arrive(b_drained + 8 * ((u & 1) * T + t));
+                        if (lane == 0) mbar_arrive_leader(b_drained + 8 * ((u & 1) * T + t));
                         mbar_wait(b_ubuf_free + 8 * ub, ((step >> 1) & 1) ^ 1);   // tail of step - 2 done
                         tr(9, u, t);
                         if (interior) {
@@ -956,9 +1005,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
     }
     // teardown
     tc_fence_before();
-    __syncthreads();
+    cluster_sync();
     tc_fence_after();
-    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
 }
 
 // q = clip((log10|c - shift| - log_lo)/span, 0, 1) * sign, rounded to tf32 (the head MMA operand)
@@ -1066,7 +1115,7 @@ int tc_pack_weights(mgsr_gen *g, const float *const *t) {
                         for (int c = 0; c < 3; ++c) s += double(w[((oc * 3 + c) * 9 + dy) * 9 + dx]);
                         v = tf32_rna(float(s));
                     }
-                    hb[(kc * 64 + oc) * 4 + e] = v;
+                    hb[(((oc >> 5) * HPLANES + kc) * 32 + (oc & 31)) * 4 + e] = v;   // [half][kc][32 oc][4]
                 }
     }
     auto conv_index = [&](int L) -> int {   // tensor index of body layer L's conv weight
@@ -1085,8 +1134,9 @@ int tc_pack_weights(mgsr_gen *g, const float *const *t) {
                 for (int e = 0; e < 8; ++e) {
                     int ic = 8 * kc + e;
                     const float v = float(double(w[(((oc0 + oc) * 64 + ic) * 3 + dy) * 3 + dx]) * k);
-                    dst[(kc * 64 + oc) * 8 + e] = f2bf(v);
-                    dst16[(kc * 64 + oc) * 8 + e] = f2h(v);
+                    const int o = (((oc >> 5) * 8 + kc) * 32 + (oc & 31)) * 8 + e;   // [half][kc][32 oc][8]
+                    dst[o] = f2bf(v);
+                    dst16[o] = f2h(v);
                 }
             }
     };
@@ -1097,11 +1147,11 @@ int tc_pack_weights(mgsr_gen *g, const float *const *t) {
     };
     for (int L = 0; L < BL.nl; ++L)
         for (int tap = 0; tap < 9; ++tap)
-            pack_tap(reinterpret_cast<uint16_t *>(blob.data() + BL.body + (size_t(L) * 9 + tap) * SLOT_BYTES),
+            pack_tap(reinterpret_cast<uint16_t *>(blob.data() + BL.body + (size_t(L) * 9 + tap) * TAP_BYTES),
                      t[conv_index(L)], 0, tap, bn_index(L));
     for (int u = 0; u < UP_QUARTERS; ++u)
         for (int tap = 0; tap < 9; ++tap)
-            pack_tap(reinterpret_cast<uint16_t *>(blob.data() + BL.up + (size_t(u) * 9 + tap) * SLOT_BYTES),
+            pack_tap(reinterpret_cast<uint16_t *>(blob.data() + BL.up + (size_t(u) * 9 + tap) * TAP_BYTES),
                      t[ip + 5], 64 * u, tap, -1);
     {
         // mma.sync tail operand: per quarter u, [tap = dy*9+dx][o][16 shuffled channels 16u..16u+15] bf16
@@ -1193,12 +1243,34 @@ int launch_sr_pass_tc_dbg(const mgsr_gen *g, const double *c, const double *c_sh
     MGSR_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
     MGSR_CUDA_TRY(cudaFuncSetAttribute(k_gen_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     MGSR_CUDA_TRY(cudaFuncSetAttribute(k_gen_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    const int grid = P.ngroups < nsm ? P.ngroups : nsm;
     k_normalize<<<grid_for((long long)nc * nc, 256), 256, 0, st>>>(c, c_shift, nc, log_lo, span, qgrid);
     MGSR_LAUNCH_CHECK();
-    if (f16) k_gen_tc<true><<<grid, NTHREADS, smem, st>>>(P);
-    else k_gen_tc<false><<<grid, NTHREADS, smem, st>>>(P);
-    MGSR_LAUNCH_CHECK();
+    // CTA pairs (clusters of 2), one CTA per SM, as many pairs as can be co-resident
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.blockDim = dim3(NTHREADS);
+    cfg.dynamicSmemBytes = size_t(smem);
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const int ngp = (P.ngroups + 1) / 2;
+    static int max_pairs[2] = {0, 0};
+    int &mp = max_pairs[f16 ? 1 : 0];
+    if (mp == 0) {
+        cfg.gridDim = dim3(2 * (nsm / 2));
+        int ncl = 0;
+        cudaError_t e = f16 ? cudaOccupancyMaxActiveClusters(&ncl, k_gen_tc<true>, &cfg)
+                            : cudaOccupancyMaxActiveClusters(&ncl, k_gen_tc<false>, &cfg);
+        mp = (e == cudaSuccess && ncl > 0) ? ncl : nsm / 2;
+    }
+    const int pairs = ngp < mp ? ngp : mp;
+    cfg.gridDim = dim3(2 * pairs);
+    if (f16) MGSR_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_gen_tc<true>, P));
+    else MGSR_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_gen_tc<false>, P));
     if (f16) k_tail_edge<true><<<edge_count(P.npos), 256, 0, st>>>(P);
     else k_tail_edge<false><<<edge_count(P.npos), 256, 0, st>>>(P);
     MGSR_LAUNCH_CHECK();
