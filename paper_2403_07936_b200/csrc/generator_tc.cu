@@ -18,8 +18,8 @@
 //     runs tile-major and each tile's epilogue overlaps the next tile's MMAs.
 //     Slots refill with the next layer's taps (cp.async.bulk + mbarrier
 //     complete_tx) as soon as the last tile has consumed them.
-//   * head 9x9 conv: tf32 MMA (K = 81 taps, the 3 identical input channels
-//     folded) on an im2col built per tile; PReLU in the epilogue.
+//   * head 9x9 conv: fp16 MMA (K = 81 taps padded to 96, the 3 identical input
+//     channels folded) on an im2col built per tile (two buffers); PReLU in the epilogue.
 //   * body: 2B+1 3x3 convs (bf16 x bf16 -> fp32, N = 64), BN folded into a
 //     per-channel affine; PReLU / residual add / global skip fused into the
 //     TMEM -> register -> smem epilogue.
@@ -74,13 +74,14 @@ constexpr int UNION_BYTES = 69632;
 constexpr int MISC_BYTES = 8192;                      // q tables (6 x 36 floats) + head im2col index table
 constexpr int BAR_BYTES = 1024;
 // union, head phase
-constexpr int HK = 88;                                   // head K (81 taps padded to a tf32 K multiple)
-constexpr int HPLANES = HK / 4;                          // 22 planes of 4 tf32
-constexpr int I2C_BYTES = HPLANES * ROWS * 16;           // 45056
-constexpr int HB_BYTES = HPLANES * 64 * 16;              // 22528: two halves of 32 oc
-constexpr int HB_HALF = HB_BYTES / 2;                    // 11264, streamed through the ring (3 slots)
-constexpr int IDX_OFF = 1024;                            // in misc: uint8 [64 padded pixels][88 k] -> q index
-static_assert(I2C_BYTES <= UNION_BYTES, "union");
+constexpr int HK = 96;                                   // head K (81 taps padded to an f16 K multiple)
+constexpr int HPLANES = HK / 8;                          // 12 planes of 8 fp16
+constexpr int I2C_BYTES = HPLANES * ROWS * 16;           // 24576 per im2col buffer (two buffers)
+constexpr int HB_BYTES = HPLANES * 64 * 16;              // 12288: two halves of 32 oc
+constexpr int HB_HALF = HB_BYTES / 2;                    // 6144, streamed through the ring (2 slots)
+constexpr int IDX_OFF = 1024;                            // in misc: uint8 [64 padded pixels][96 k] -> q index
+static_assert(2 * I2C_BYTES <= UNION_BYTES, "union");
+static_assert(IDX_OFF + 64 * HK <= MISC_BYTES, "misc");
 // up phase (union): the up-conv quarter, pixel-shuffled, bf16 [window][12x12][16 ch] with a 48-byte
 // pixel stride (conflict-free ldmatrix rows), double-buffered over tiles; tail weights of the quarter
 // bf16 [tap 81][o 3][16 ch] (double-buffered over quarters); a zero row; the reduction scratch.
@@ -437,8 +438,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
     const uint32_t b_empty = smem_u32(bars + NSLOT);                // [NSLOT] (both) slot consumed
     const uint32_t b_peerfull = smem_u32(bars + 2 * NSLOT);         // [NSLOT] (leader) peer's slot landed
     constexpr int BB = 3 * NSLOT;
-    const uint32_t b_i2c_full = smem_u32(bars + BB);                // (leader) both im2cols built
-    const uint32_t b_i2c_empty = smem_u32(bars + BB + 1);           // (both)
+    const uint32_t b_i2c_full = smem_u32(bars + BB + 33);           // [2] (leader) im2col buffer built (both CTAs)
+    const uint32_t b_i2c_empty = smem_u32(bars + BB + 35);          // [2] (both) im2col buffer consumed
     const uint32_t b_acc_full = smem_u32(bars + BB + 2);    // [T] (both) MMA -> epilogue: accumulator ready
     const uint32_t b_act_ready = smem_u32(bars + BB + 5);   // [T] (leader) epilogues -> MMA: act written
     const uint32_t b_ubuf_full = smem_u32(bars + BB + 8);   // [2] drain warps -> tail warps: U buffer written
@@ -468,8 +469,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
             mbar_init(b_empty + 8 * s, 1);
             mbar_init(b_peerfull + 8 * s, 1);
         }
-        mbar_init(b_i2c_full, 2);
-        mbar_init(b_i2c_empty, 1);
+        for (int b2 = 0; b2 < 2; ++b2) {
+            mbar_init(b_i2c_full + 8 * b2, 2);
+            mbar_init(b_i2c_empty + 8 * b2, 1);
+        }
         for (int t = 0; t < T; ++t) {
             mbar_init(b_acc_full + 8 * t, 1);
             mbar_init(b_act_ready + 8 * t, 2 * NEPI);
@@ -519,8 +522,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
         for (int gp = pair; gp < ngp; gp += npairs) {
             tr.buf = (P.prof && blockIdx.x == 0 && gp == TRACE_GROUP * npairs) ? P.prof : nullptr;
             seq = 0;
-            for (int h = 0; h < 3; ++h)   // this CTA's half of the head weights: planes 0-7, 8-15, 16-21
-                fill(wblob + BL.head_b + rank * HB_HALF + h * SLOT_BYTES, h < 2 ? SLOT_BYTES : HB_HALF - 2 * SLOT_BYTES);
+            for (int h = 0; h < 2; ++h)   // this CTA's half of the head weights: planes 0-7, 8-11
+                fill(wblob + BL.head_b + rank * HB_HALF + h * SLOT_BYTES, h < 1 ? SLOT_BYTES : HB_HALF - SLOT_BYTES);
             for (int L = 0; L < NLAYERS; ++L)
                 for (int tap = 0; tap < 9; ++tap)
                     fill(wblob + P.wfmt + BL.body + (size_t(L) * 9 + tap) * TAP_BYTES + rank * SLOT_BYTES);
@@ -544,7 +547,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
         // ================= peer: forward "slot landed" to the leader =================
         uint32_t ph = 0;
         int slot = 0;
-        const int fills = 3 + (NLAYERS + UP_QUARTERS) * 9;
+        const int fills = 2 + (NLAYERS + UP_QUARTERS) * 9;
         for (int gp = pair; gp < ngp; gp += npairs)
             for (int i = 0; i < fills; ++i) {
                 mbar_wait(b_full + 8 * slot, (ph >> slot) & 1u);
@@ -555,7 +558,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
             }
     } else if (warp == 1) {
         // ================= MMA issuer (leader; warp-uniform control, one elected lane issues) =================
-        uint32_t ph = 0, i2c_ph = 0;
+        uint32_t ph = 0, i2c_ph = 0;   // i2c_ph bit b: parity of the next completion of b_i2c_full[b]
         int slot0 = 0;   // ring slot of tap 0 of the current layer
         uint32_t ar_ph[T] = {0, 0, 0};
         uint32_t dr_ph = 0;   // bit t: parity of the next completion of b_drained[0][t]
@@ -622,20 +625,21 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
         };
         for (int gp = pair; gp < ngp; gp += npairs) {
             tr.buf = (P.prof && blockIdx.x == 0 && gp == TRACE_GROUP * npairs) ? P.prof + 4096 : nullptr;
-            // head: D[t] = im2col(q) (128 x 88, tf32) x Wh^T (88 x 64)
+            // head: D[t] = im2col(q) (128 x 96, fp16) x Wh^T (96 x 64); im2col buffer t & 1
             for (int t = 0; t < T; ++t) {
+                const int ib = t & 1;
                 // the head accumulates into up buffer 0 of this tile (cols COL_ACC + 64 t)
                 mbar_wait(b_drained + 8 * t, (dr_ph >> t) & 1u);
                 dr_ph ^= 1u << t;
                 if (lane == 0) tr(2, 0, t);
-                mbar_wait(b_i2c_full, i2c_ph);
+                mbar_wait(b_i2c_full + 8 * ib, (i2c_ph >> ib) & 1u);
                 if (lane == 0) tr(5, 0, t);
-                i2c_ph ^= 1;
+                i2c_ph ^= 1u << ib;
                 tc_fence_after();
                 const uint32_t d = tmem + COL_ACC + 64 * t;
                 if (elect_one()) {
 #pragma unroll
-                    for (int ks = 0; ks < HK / 8; ++ks) {
+                    for (int ks = 0; ks < HK / 16; ++ks) {
                         int sl = slot0 + (ks >> 2);
                         sl = sl >= NSLOT ? sl - NSLOT : sl;
                         if (t == 0 && (ks & 3) == 0) {
@@ -643,24 +647,24 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
                             mbar_wait(b_peerfull + 8 * sl, (ph >> sl) & 1u);
                             tc_fence_after();
                         }
-                        uint64_t a = make_desc(i2c_base + 2 * ks * (ROWS * 16), ROWS * 16, 128);
+                        uint64_t a = make_desc(i2c_base + ib * I2C_BYTES + 2 * ks * (ROWS * 16), ROWS * 16, 128);
                         uint64_t b = make_desc(ring_base + sl * SLOT_BYTES + (ks & 3) * 1024, 32 * 16, 128);
-                        mma_tf32(d, a, b, idesc_tf32(64), ks > 0);
-                        if (t == T - 1 && ((ks & 3) == 3 || ks == HK / 8 - 1)) umma_commit(b_empty + 8 * sl);
+                        mma_bf16(d, a, b, idesc_f16(64), ks > 0);
+                        if (t == T - 1 && ((ks & 3) == 3 || ks == HK / 16 - 1)) umma_commit(b_empty + 8 * sl);
                     }
                     umma_commit(b_acc_full + 8 * t);
-                    umma_commit(b_i2c_empty);
+                    umma_commit(b_i2c_empty + 8 * ib);
                 }
                 __syncwarp();
                 if (lane == 0) tr(3, 0, t);
             }
 #pragma unroll
-            for (int h = 0; h < 3; ++h) {
+            for (int h = 0; h < 2; ++h) {
                 int sl = slot0 + h;
                 sl = sl >= NSLOT ? sl - NSLOT : sl;
                 ph ^= 1u << sl;
             }
-            slot0 += 3;
+            slot0 += 2;
             slot0 = slot0 >= NSLOT ? slot0 - NSLOT : slot0;
 #pragma unroll 1
             for (int L = 0; L < NLAYERS; ++L) conv_layer(L + 1, 0, COL_ACC);
@@ -683,8 +687,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
         const bool interior = py >= 1 && py <= 6 && px >= 1 && px <= 6;
         const uint32_t lane_addr = uint32_t(32 * q) << 16;
         uint32_t af_ph[T] = {0, 0, 0};
-        uint32_t i2c_empty_ph = 0;
-        bool first_build = true;
+        int i2c_uses[2] = {0, 0};   // builds into im2col buffer b so far
         if (lane == 0 && ew < NEPI / 2)
             for (int t = 0; t < T; ++t) mbar_arrive_leader(b_drained + 8 * t);   // up buffer 0 (= head accumulator) starts free
         const float *head_a = cs;
@@ -718,33 +721,34 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
             }
             epi_bar();
             tr(11, 1, 0);
-            // ---- head: im2col per tile (tf32) + head weights ----
+            // ---- head: im2col per tile (fp16, two buffers: tile t + 1 builds while tile t multiplies) ----
             for (int t = 0; t < T; ++t) {
-                if (!first_build) {
-                    mbar_wait(b_i2c_empty, i2c_empty_ph);
-                    i2c_empty_ph ^= 1;
-                }
-                first_build = false;
+                const int ib = t & 1;
+                if (i2c_uses[ib] > 0) mbar_wait(b_i2c_empty + 8 * ib, uint32_t(i2c_uses[ib] - 1) & 1u);
+                ++i2c_uses[ib];
                 {
                     const int r = et & 127, part4 = et >> 7;
                     const int rw = r >> 6, rp = r & 63;
                     const float *qt = misc + (t * WPT + rw) * 36;
-                    const uint32_t *ix = reinterpret_cast<const uint32_t *>(idx_tab + rp * HK);
-                    const int kc_end = min(part4 * 6 + 6, HPLANES);
-                    for (int kc = part4 * 6; kc < kc_end; ++kc) {
-                        const uint32_t i4 = ix[kc];
-                        float v[4];
+                    const uint2 *ix = reinterpret_cast<const uint2 *>(idx_tab + rp * HK);
+#pragma unroll
+                    for (int kk = 0; kk < HPLANES / 4; ++kk) {
+                        const int kc = part4 * (HPLANES / 4) + kk;
+                        const uint2 i8 = ix[kc];
+                        uint32_t w[4];
 #pragma unroll
                         for (int e = 0; e < 4; ++e) {
-                            const uint32_t id = (i4 >> (8 * e)) & 0xFFu;
-                            v[e] = id < 36 ? qt[id] : 0.f;
+                            const uint32_t src = e < 2 ? i8.x : i8.y;
+                            const uint32_t id0 = (src >> (16 * (e & 1))) & 0xFFu, id1 = (src >> (16 * (e & 1) + 8)) & 0xFFu;
+                            w[e] = pack_op<true>(id0 < 36 ? qt[id0] : 0.f, id1 < 36 ? qt[id1] : 0.f);
                         }
-                        *reinterpret_cast<float4 *>(uni + kc * (ROWS * 16) + r * 16) = make_float4(v[0], v[1], v[2], v[3]);
+                        *reinterpret_cast<uint4 *>(uni + ib * I2C_BYTES + kc * (ROWS * 16) + r * 16) =
+                            make_uint4(w[0], w[1], w[2], w[3]);
                     }
                 }
                 fence_async_smem();
                 epi_bar();
-                if (et == 0) mbar_arrive_leader(b_i2c_full);
+                if (et == 0) mbar_arrive_leader(b_i2c_full + 8 * ib);
                 tr(12, 0, t);
             }
             // ---- head + body + post epilogues ----
@@ -1010,13 +1014,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
     if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
 }
 
-// q = clip((log10|c - shift| - log_lo)/span, 0, 1) * sign, rounded to tf32 (the head MMA operand)
+// q = clip((log10|c - shift| - log_lo)/span, 0, 1) * sign (rounded to fp16 in the head im2col)
 __global__ void k_normalize(const double *__restrict__ c, const double *shift, int nc, double log_lo, double span,
                             float *__restrict__ q) {
     const double sh = shift ? *shift : 0.0;
     const long long total = (long long)nc * nc;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x)
-        q[i] = to_tf32(float(normalize_q(c[i] - sh, log_lo, span)));
+        q[i] = float(normalize_q(c[i] - sh, log_lo, span));
 }
 
 // Tail of the edge windows (kept band touching the grid edge), exact fp32 with
@@ -1084,14 +1088,6 @@ static inline uint16_t f2bf(float f) {
     uint32_t r = u + 0x7FFFu + ((u >> 16) & 1u);   // round to nearest even
     return uint16_t(r >> 16);
 }
-static inline float tf32_rna(float f) {
-    uint32_t u;
-    std::memcpy(&u, &f, 4);
-    u = (u + 0x1000u) & 0xFFFFE000u;
-    float r;
-    std::memcpy(&r, &u, 4);
-    return r;
-}
 
 // Pack the MGSR1 tensors (host f32, expected_tensor_shapes order) into the
 // kernel's weight blob: UMMA core-matrix layout (K-major, 8-element planes).
@@ -1100,22 +1096,22 @@ int tc_pack_weights(mgsr_gen *g, const float *const *t) {
     const int B = g->blocks;
     BlobLayout BL = blob_layout(B);
     std::vector<uint8_t> blob(BL.total, 0);
-    // head B: 22 planes x 64 oc x 4 tf32 (3 identical input channels folded)
+    // head B: 12 planes x 64 oc x 8 fp16 (3 identical input channels folded), split in two 32-oc halves
     {
-        float *hb = reinterpret_cast<float *>(blob.data() + BL.head_b);
+        uint16_t *hb = reinterpret_cast<uint16_t *>(blob.data() + BL.head_b);
         const float *w = t[0];
         for (int kc = 0; kc < HPLANES; ++kc)
             for (int oc = 0; oc < 64; ++oc)
-                for (int e = 0; e < 4; ++e) {
-                    int k = 4 * kc + e;
+                for (int e = 0; e < 8; ++e) {
+                    int k = 8 * kc + e;
                     float v = 0.f;
                     if (k < 81) {
                         int dy = k / 9, dx = k % 9;
                         double s = 0.0;
                         for (int c = 0; c < 3; ++c) s += double(w[((oc * 3 + c) * 9 + dy) * 9 + dx]);
-                        v = tf32_rna(float(s));
+                        v = float(s);
                     }
-                    hb[(((oc >> 5) * HPLANES + kc) * 32 + (oc & 31)) * 4 + e] = v;   // [half][kc][32 oc][4]
+                    hb[(((oc >> 5) * HPLANES + kc) * 32 + (oc & 31)) * 8 + e] = f2h(v);   // [half][kc][32 oc][8] fp16
                 }
     }
     auto conv_index = [&](int L) -> int {   // tensor index of body layer L's conv weight
