@@ -137,6 +137,19 @@ int32_t mgsr_plan_levels(const mgsr_plan *plan, int64_t *sides_out /* >= 32 entr
 int mgsr_plan_vcycle(mgsr_plan *plan, double *p, const double *f, int32_t use_sr,
                      double *stats_dev, void *stream);
 
+/* Device-resident solve loop: up to n_iter V-cycles in ONE graph launch (a WHILE
+ * conditional node; per iteration the operator follows schedule_operator and the
+ * latch rule on device, the cycle runs, and the logging pass's stats are
+ * recorded).  mode: 0 spline, 1 sr, 2 hybrid.  Hybrid cadence: cadence =
+ * max(1, round(N_GAN)) (or of 1/N_GAN), first_sr = 1 when N_GAN >= 1, ngan_one =
+ * (N_GAN == 1).  records_dev: n_iter x 4 doubles (diff_norm, residual rms,
+ * operator 1=sr/0=spline, latched before the iteration); iterations_dev: one
+ * int32, the number of iterations run (stop when diff_norm < tol).
+ * Replaces solver.solve's loop (solver.py:280-330). */
+int mgsr_plan_solve(mgsr_plan *plan, double *p, const double *f, int32_t mode, int32_t n_iter, double tol,
+                    double s_thres, int32_t cadence, int32_t first_sr, int32_t ngan_one,
+                    double *records_dev, int32_t *iterations_dev, void *stream);
+
 /* Instrumentation for bench.py.  mgsr_plan_timing_enable(plan, k): the next k
  * V-cycle launches record CUDA events (event-record nodes inside the graph,
  * re-targeted per launch) around (0) the finest-level generator kernel,

@@ -55,6 +55,15 @@ struct mgsr_plan {
         int kernel_nodes = 0;
     };
     std::map<std::tuple<double *, const double *, int>, Graph> graphs;
+    // device-resident solve loops: graph per (p, f, schedule) with conditional nodes
+    struct SolveGraph {
+        cudaGraph_t graph = nullptr;
+        cudaGraphExec_t exec = nullptr;
+    };
+    std::map<std::tuple<double *, const double *, int, int, double, double, int, int, int>, SolveGraph> solves;
+    int *solve_state = nullptr;      // [4] it, latched, op, iterations (device)
+    double *solve_rec = nullptr;     // [rec_cap][4] diff_norm, residual_rms, op, latched (device)
+    int rec_cap = 0;
     // instrumentation: placeholder events captured as event-record nodes
     cudaEvent_t cap_ev[6] = {};
     bool capturing_markers = false;
@@ -224,6 +233,12 @@ extern "C" int mgsr_plan_destroy(mgsr_plan *pl) {
         cudaGraphExecDestroy(kv.second.exec);
         cudaGraphDestroy(kv.second.graph);
     }
+    for (auto &kv : pl->solves) {
+        cudaGraphExecDestroy(kv.second.exec);
+        cudaGraphDestroy(kv.second.graph);
+    }
+    if (pl->solve_state) cudaFree(pl->solve_state);
+    if (pl->solve_rec) cudaFree(pl->solve_rec);
     for (auto ev : pl->cap_ev) if (ev) cudaEventDestroy(ev);
     for (auto ev : pl->pool) cudaEventDestroy(ev);
     if (pl->cap) cudaStreamDestroy(pl->cap);
@@ -341,4 +356,167 @@ extern "C" int32_t mgsr_plan_kernel_nodes(mgsr_plan *pl, int32_t use_sr) {
     for (auto &kv : pl->graphs)
         if (std::get<2>(kv.first) == int(use_sr != 0)) return kv.second.kernel_nodes;
     return 0;
+}
+
+// ---------------------------------------------------------------------------
+// Device-resident solve loop (solver.py:280-330).  One graph launch runs the
+// whole loop: a WHILE conditional node whose body is
+//   k_solve_pre  -> operator of this iteration (schedule_operator,
+//                   solver.py:122-144: N_GAN cadence, latch -> second operator)
+//   IF(sr)       -> the captured SR V-cycle
+//   IF(spline)   -> the captured spline V-cycle
+//   k_solve_post -> record (diff_norm, residual rms, operator, latched), latch
+//                   on diff <= S_thres, continue while diff >= tol and
+//                   iterations < N_iter.
+// No host round trip per cycle; the ConvergenceLog is read back once.
+
+namespace {
+
+__global__ void k_solve_init(int *state) {
+    state[0] = 0;   // iterations done
+    state[1] = 0;   // latched
+    state[2] = 0;   // operator of the current iteration
+    state[3] = 0;   // iterations (output)
+}
+
+__global__ void k_solve_pre(int *state, int mode, int cadence, int first_sr, int ngan_one,
+                            cudaGraphConditionalHandle h_sr, cudaGraphConditionalHandle h_sp) {
+    const int it = state[0] + 1;
+    const int latched = state[1];
+    int sr;
+    if (mode == 0) sr = 0;
+    else if (mode == 1) sr = 1;
+    else if (latched) sr = !first_sr;
+    else if (ngan_one) sr = it & 1;
+    else sr = (it % cadence != 0) ? first_sr : !first_sr;
+    state[2] = sr;
+    cudaGraphSetConditional(h_sr, sr ? 1u : 0u);
+    cudaGraphSetConditional(h_sp, sr ? 0u : 1u);
+}
+
+__global__ void k_solve_post(int *state, const double *stats, double *rec, int n_iter, double tol, double s_thres,
+                             cudaGraphConditionalHandle h_while) {
+    const int it = state[0] + 1;
+    const double d = stats[0];
+    double *r = rec + 4 * (it - 1);
+    r[0] = d;
+    r[1] = stats[1];
+    r[2] = double(state[2]);
+    r[3] = double(state[1]);
+    if (!state[1] && d <= s_thres) state[1] = 1;
+    state[0] = it;
+    state[3] = it;
+    cudaGraphSetConditional(h_while, (!(d < tol) && it < n_iter) ? 1u : 0u);
+}
+
+int add_kernel(cudaGraph_t g, cudaGraphNode_t *node, const cudaGraphNode_t *deps, size_t ndeps, void *func,
+               void **args) {
+    cudaKernelNodeParams kp{};
+    kp.func = func;
+    kp.gridDim = dim3(1);
+    kp.blockDim = dim3(1);
+    kp.sharedMemBytes = 0;
+    kp.kernelParams = args;
+    MGSR_CUDA_TRY(cudaGraphAddKernelNode(node, g, deps, ndeps, &kp));
+    return MGSR_OK;
+}
+
+int add_if(cudaGraph_t g, cudaGraphNode_t *node, const cudaGraphNode_t *dep, cudaGraphConditionalHandle h,
+           cudaGraphConditionalNodeType type, cudaGraph_t *body) {
+    cudaGraphNodeParams np{};
+    np.type = cudaGraphNodeTypeConditional;
+    np.conditional.handle = h;
+    np.conditional.type = type;
+    np.conditional.size = 1;
+    MGSR_CUDA_TRY(cudaGraphAddNode(node, g, dep, dep ? 1 : 0, &np));
+    *body = np.conditional.phGraph_out[0];
+    return MGSR_OK;
+}
+
+// capture one V-cycle's kernel sequence into an existing (conditional body) graph
+int capture_cycle_into(mgsr_plan *pl, cudaGraph_t body, double *p, const double *f, int use_sr) {
+    MGSR_CUDA_TRY(cudaStreamBeginCaptureToGraph(pl->cap, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+    const bool mk = pl->capturing_markers;
+    pl->capturing_markers = false;
+    int r = record_vcycle(pl, p, f, use_sr, pl->cap);
+    pl->capturing_markers = mk;
+    cudaGraph_t out = nullptr;
+    cudaError_t e = cudaStreamEndCapture(pl->cap, &out);
+    if (r) return r;
+    if (e != cudaSuccess) { set_error(std::string("solve body capture: ") + cudaGetErrorString(e)); return MGSR_E_CUDA; }
+    return MGSR_OK;
+}
+
+}  // namespace
+
+extern "C" int mgsr_plan_solve(mgsr_plan *pl, double *p, const double *f, int32_t mode, int32_t n_iter, double tol,
+                               double s_thres, int32_t cadence, int32_t first_sr, int32_t ngan_one,
+                               double *records_dev, int32_t *iterations_dev, void *stream) {
+    if (!pl || !p || !f || !records_dev || !iterations_dev || n_iter < 1 || mode < 0 || mode > 2 || cadence < 1) {
+        set_error("bad argument");
+        return MGSR_E_BAD_ARG;
+    }
+    if (mode != 0 && !pl->gen) { set_error("SR prolongation requires generator weights"); return MGSR_E_BAD_ARG; }
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (!pl->solve_state) MGSR_CUDA_TRY(cudaMalloc(&pl->solve_state, 4 * sizeof(int)));
+    if (pl->rec_cap < n_iter) {
+        // records are baked into the graphs: drop them with the old buffer
+        for (auto &kv : pl->solves) {
+            cudaGraphExecDestroy(kv.second.exec);
+            cudaGraphDestroy(kv.second.graph);
+        }
+        pl->solves.clear();
+        if (pl->solve_rec) cudaFree(pl->solve_rec);
+        MGSR_CUDA_TRY(cudaMalloc(&pl->solve_rec, 4 * sizeof(double) * size_t(n_iter)));
+        pl->rec_cap = n_iter;
+    }
+    auto key = std::make_tuple(p, f, int(mode), int(n_iter), tol, s_thres, int(cadence), int(first_sr), int(ngan_one));
+    auto it = pl->solves.find(key);
+    if (it == pl->solves.end()) {
+        MGSR_CUDA_TRY(cudaStreamSynchronize(st));
+        cudaGraph_t g = nullptr;
+        MGSR_CUDA_TRY(cudaGraphCreate(&g, 0));
+        cudaGraphConditionalHandle hw, hs, hp;
+        MGSR_CUDA_TRY(cudaGraphConditionalHandleCreate(&hw, g, 1, cudaGraphCondAssignDefault));
+        MGSR_CUDA_TRY(cudaGraphConditionalHandleCreate(&hs, g, 0, cudaGraphCondAssignDefault));
+        MGSR_CUDA_TRY(cudaGraphConditionalHandleCreate(&hp, g, 0, cudaGraphCondAssignDefault));
+        int *state = pl->solve_state;
+        double *rec = pl->solve_rec;
+        double *stats = sc(pl, SC_STATS);
+        cudaGraphNode_t n_init, n_while, n_pre, n_if_sr, n_if_sp, n_post;
+        void *a_init[] = {&state};
+        int r = add_kernel(g, &n_init, nullptr, 0, reinterpret_cast<void *>(k_solve_init), a_init);
+        cudaGraph_t body = nullptr, body_sr = nullptr, body_sp = nullptr;
+        if (!r) r = add_if(g, &n_while, &n_init, hw, cudaGraphCondTypeWhile, &body);
+        int mode_ = mode, cad = cadence, fs_ = first_sr, g1 = ngan_one, nit = n_iter;
+        double tol_ = tol, sth = s_thres;
+        void *a_pre[] = {&state, &mode_, &cad, &fs_, &g1, &hs, &hp};
+        if (!r) r = add_kernel(body, &n_pre, nullptr, 0, reinterpret_cast<void *>(k_solve_pre), a_pre);
+        cudaGraphNode_t last = n_pre;   // pure modes carry only their own cycle
+        if (!r && mode != 0) {
+            r = add_if(body, &n_if_sr, &last, hs, cudaGraphCondTypeIf, &body_sr);
+            last = n_if_sr;
+        }
+        if (!r && mode != 1) {
+            r = add_if(body, &n_if_sp, &last, hp, cudaGraphCondTypeIf, &body_sp);
+            last = n_if_sp;
+        }
+        void *a_post[] = {&state, &stats, &rec, &nit, &tol_, &sth, &hw};
+        if (!r) r = add_kernel(body, &n_post, &last, 1, reinterpret_cast<void *>(k_solve_post), a_post);
+        if (!r && mode != 0) r = capture_cycle_into(pl, body_sr, p, f, 1);
+        if (!r && mode != 1) r = capture_cycle_into(pl, body_sp, p, f, 0);
+        mgsr_plan::SolveGraph SG;
+        SG.graph = g;
+        if (!r) {
+            cudaError_t e = cudaGraphInstantiate(&SG.exec, g, 0);
+            if (e != cudaSuccess) { set_error(std::string("solve graph instantiate: ") + cudaGetErrorString(e)); r = MGSR_E_CUDA; }
+        }
+        if (r) { cudaGraphDestroy(g); return r; }
+        it = pl->solves.emplace(key, SG).first;
+    }
+    MGSR_CUDA_TRY(cudaGraphLaunch(it->second.exec, st));
+    MGSR_CUDA_TRY(cudaMemcpyAsync(records_dev, pl->solve_rec, 4 * sizeof(double) * size_t(n_iter),
+                                  cudaMemcpyDeviceToDevice, st));
+    MGSR_CUDA_TRY(cudaMemcpyAsync(iterations_dev, pl->solve_state + 3, sizeof(int), cudaMemcpyDeviceToDevice, st));
+    return MGSR_OK;
 }

@@ -162,3 +162,26 @@ def test_solve_hybrid_fp16_matches_fp32_schedule(cuda, orc):
     _, l16 = solver.solve(PoissonProblem(Grid(f)), cfg, w, precision="fp16")
     assert [r.operator for r in l16.records] == [r.operator for r in l32.records]
     assert l16.iterations == l32.iterations and l16.converged(1e-10)
+
+
+@pytest.mark.parametrize("mode,n", [("spline", 64), ("spline", 256), ("hybrid", 256)])
+def test_resident_solve_matches_host_loop(cuda, orc, mode, n):
+    """The single-launch device loop (WHILE conditional graph node, mgsr_plan_solve) runs the
+    same cycles as the per-cycle host loop: identical histories, operators, latches and count."""
+    import os
+    from paper_2403_07936_b200 import solver, srmodel
+    from paper_2403_07936_b200.grid import Grid
+    from paper_2403_07936_b200.smoother import PoissonProblem
+    from conftest import ROOT
+    w = srmodel.load_weights(os.path.join(ROOT, "artifacts", "trained_b8.mgsr")) if mode == "hybrid" else None
+    f = orc.scale_to_p_rms(orc.sine_modes_rhs(n, 0), 1e-4)
+    cfg = cfg_(mode=mode, N_GAN=1.0, S_thres=5e-4)
+    p_a, la = solver.solve(PoissonProblem(Grid(f)), cfg, w, resident=True)
+    p_b, lb = solver.solve(PoissonProblem(Grid(f)), cfg, w, resident=False)
+    assert la.iterations == lb.iterations
+    assert [r.operator for r in la.records] == [r.operator for r in lb.records]
+    assert [r.switch_latched for r in la.records] == [r.switch_latched for r in lb.records]
+    a = np.array([[r.diff_norm, r.residual_norm] for r in la.records])
+    b = np.array([[r.diff_norm, r.residual_norm] for r in lb.records])
+    assert np.array_equal(a, b)
+    assert np.array_equal(p_a.data, p_b.data)
