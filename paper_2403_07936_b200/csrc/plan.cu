@@ -492,17 +492,12 @@ extern "C" int mgsr_plan_solve(mgsr_plan *pl, double *p, const double *f, int32_
         double tol_ = tol, sth = s_thres;
         void *a_pre[] = {&state, &mode_, &cad, &fs_, &g1, &hs, &hp};
         if (!r) r = add_kernel(body, &n_pre, nullptr, 0, reinterpret_cast<void *>(k_solve_pre), a_pre);
-        cudaGraphNode_t last = n_pre;   // pure modes carry only their own cycle
-        if (!r && mode != 0) {
-            r = add_if(body, &n_if_sr, &last, hs, cudaGraphCondTypeIf, &body_sr);
-            last = n_if_sr;
-        }
-        if (!r && mode != 1) {
-            r = add_if(body, &n_if_sp, &last, hp, cudaGraphCondTypeIf, &body_sp);
-            last = n_if_sp;
-        }
+        // both IF nodes always exist (every handle the controller sets must belong to a node); a pure
+        // mode leaves the other operator's body empty
+        if (!r) r = add_if(body, &n_if_sr, &n_pre, hs, cudaGraphCondTypeIf, &body_sr);
+        if (!r) r = add_if(body, &n_if_sp, &n_if_sr, hp, cudaGraphCondTypeIf, &body_sp);
         void *a_post[] = {&state, &stats, &rec, &nit, &tol_, &sth, &hw};
-        if (!r) r = add_kernel(body, &n_post, &last, 1, reinterpret_cast<void *>(k_solve_post), a_post);
+        if (!r) r = add_kernel(body, &n_post, &n_if_sp, 1, reinterpret_cast<void *>(k_solve_post), a_post);
         if (!r && mode != 0) r = capture_cycle_into(pl, body_sr, p, f, 1);
         if (!r && mode != 1) r = capture_cycle_into(pl, body_sp, p, f, 0);
         mgsr_plan::SolveGraph SG;

@@ -185,3 +185,21 @@ def test_resident_solve_matches_host_loop(cuda, orc, mode, n):
     b = np.array([[r.diff_norm, r.residual_norm] for r in lb.records])
     assert np.array_equal(a, b)
     assert np.array_equal(p_a.data, p_b.data)
+
+
+def test_solve_batch_matches_single_solves(cuda, orc):
+    """Concurrent multi-RHS solves (one plan + stream each) give exactly the single-solve results."""
+    import os
+    from paper_2403_07936_b200 import solver, srmodel
+    from paper_2403_07936_b200.grid import Grid
+    from paper_2403_07936_b200.smoother import PoissonProblem
+    from conftest import ROOT
+    w = srmodel.load_weights(os.path.join(ROOT, "artifacts", "trained_b8.mgsr"))
+    fs = [orc.scale_to_p_rms(orc.sine_modes_rhs(128, s), 1e-4) for s in range(3)]
+    cfg = cfg_(mode="hybrid", N_GAN=1.0, S_thres=5e-4)
+    batch = solver.solve_batch([PoissonProblem(Grid(f)) for f in fs], cfg, w)
+    for f, (pb, lb) in zip(fs, batch):
+        ps, ls = solver.solve(PoissonProblem(Grid(f)), cfg, w)
+        assert lb.iterations == ls.iterations and lb.converged(1e-10)
+        assert [r.operator for r in lb.records] == [r.operator for r in ls.records]
+        assert np.array_equal(pb.data, ps.data)
