@@ -128,7 +128,8 @@ __global__ void __launch_bounds__(kTbThreads, 3) k_gs_tb(const double *__restric
                                                       double *rc_mean_out) {
     constexpr int H = 2 * K + (RC ? 1 : 0);
     constexpr int W = kTbTX + 2 * H, HH = kTbTY + 2 * H;
-    constexpr int WH = W / 2, PL = WH * HH;
+    // plane rows padded to an even stride so a pair of same-colour cells is one 16-byte access
+    constexpr int WH = W / 2, WP = (WH + 1) & ~1, PL = WP * HH, NPR = WP / 2;
     static_assert(W % 2 == 0, "tile width must be even");
     extern __shared__ double sm[];
     double *const sp = sm;            // planes 0,1 of p
@@ -137,7 +138,6 @@ __global__ void __launch_bounds__(kTbThreads, 3) k_gs_tb(const double *__restric
     const double sh = fs.load_shift();
     const int tiles_x = n / kTbTX, ntiles = tiles_x * (n / kTbTY);
     constexpr int NE = W * HH, PER = (NE + kTbThreads - 1) / kTbThreads;
-    constexpr int RW = WH - 1;   // cells of one colour per row strictly inside [1, W-2]
     double v[2] = {0.0, 0.0};     // grid sum of the new iterate, of the coarse residual
     // Persistent: the block walks tiles blockIdx.x, +gridDim.x, ... (row-major, so
     // concurrently resident blocks share halos in L2) and reduces once at the end.
@@ -168,7 +168,7 @@ __global__ void __launch_bounds__(kTbThreads, 3) k_gs_tb(const double *__restric
             const int idx = tid + u * kTbThreads;
             if (idx < NE) {
                 const int ly = idx / W, lx = idx - ly * W;
-                const int o = ((ly + lx) & 1) * PL + ly * WH + (lx >> 1);
+                const int o = ((ly + lx) & 1) * PL + ly * WP + (lx >> 1);
                 sp[o] = rp[u];
                 sf[o] = rf[u];
             }
@@ -184,14 +184,28 @@ __global__ void __launch_bounds__(kTbThreads, 3) k_gs_tb(const double *__restric
             const double *const po = sp + (1 - c) * PL;
             const double *const fc = sf + c * PL;
             const int r0 = 1 + hs, nrows = HH - 2 - 2 * hs;
-            for (int idx = tid; idx < nrows * RW; idx += kTbThreads) {
-                const int rr = idx / RW;
+            // pairs of same-colour cells k = 2m, 2m + 1 (lx = 2k + par); the pairs also update the tile's
+            // edge columns and the pad slot, which only feed cells that are invalid already
+            for (int idx = tid; idx < nrows * NPR; idx += kTbThreads) {
+                const int rr = idx / NPR;
                 const int ly = r0 + rr;
                 const int par = (c + ly) & 1;              // lx parity of colour-c cells in this row
-                const int k = idx - rr * RW + 1 - par;     // lx = 2k + par in [1, W-2]
-                const int o = ly * WH + k;
-                double nb = ((po[o - WH] + po[o + WH]) + po[o - 1 + par]) + po[o + par];
-                pc[o] = (nb - h2 * fc[o]) * 0.25;
+                const int o = ly * WP + 2 * (idx - rr * NPR);
+                const double2 up = *reinterpret_cast<const double2 *>(po + o - WP);
+                const double2 dn = *reinterpret_cast<const double2 *>(po + o + WP);
+                const double2 mid = *reinterpret_cast<const double2 *>(po + o);
+                const double2 ff = *reinterpret_cast<const double2 *>(fc + o);
+                double l0, r0v, l1, r1;
+                if (par) {
+                    const double e2 = po[o + 2];
+                    l0 = mid.x; r0v = mid.y; l1 = mid.y; r1 = e2;
+                } else {
+                    const double em = po[o - 1];
+                    l0 = em; r0v = mid.x; l1 = mid.x; r1 = mid.y;
+                }
+                const double nb0 = ((up.x + dn.x) + l0) + r0v;
+                const double nb1 = ((up.y + dn.y) + l1) + r1;
+                *reinterpret_cast<double2 *>(pc + o) = make_double2((nb0 - h2 * ff.x) * 0.25, (nb1 - h2 * ff.y) * 0.25);
             }
             __syncthreads();
         }
@@ -200,7 +214,7 @@ __global__ void __launch_bounds__(kTbThreads, 3) k_gs_tb(const double *__restric
             const int gi = gy0 + H + iy, gj = gx0 + H + ix;
             const int ly = iy + H, lx = ix + H;
             const int c = (ly + lx) & 1;
-            const int o = ly * WH + (lx >> 1);
+            const int o = ly * WP + (lx >> 1);
             const double val = sp[c * PL + o];
             pout[int64_t(gi) * n + gj] = val;
             v[0] += val;
@@ -208,7 +222,7 @@ __global__ void __launch_bounds__(kTbThreads, 3) k_gs_tb(const double *__restric
                 // (even, even) cell: colour 0; its neighbours are in plane 1
                 const double *po = sp + PL;
                 const int par = lx & 1;
-                double nb = ((po[o - WH] + po[o + WH]) + po[o - 1 + par]) + po[o + par];
+                double nb = ((po[o - WP] + po[o + WP]) + po[o - 1 + par]) + po[o + par];
                 double res = sf[o] - ((nb - 4.0 * val) * inv_h2);
                 rc[int64_t(gi >> 1) * (n >> 1) + (gj >> 1)] = res;
                 v[1] += res;
@@ -541,7 +555,8 @@ int launch_gs(const double *p_in, double *p_out, double *tmp, FSrc fs, int n, do
             const int zi = (ci == 0) ? zero_init : 0;
             const int ntiles = (n / kTbTX) * (n / kTbTY);
             const int H = 2 * k + (rcl ? 1 : 0);
-            size_t smem = 2 * sizeof(double) * (kTbTX + 2 * H) * (kTbTY + 2 * H);
+            const int wp = (((kTbTX + 2 * H) / 2) + 1) & ~1;   // padded plane row (see k_gs_tb)
+            size_t smem = 4 * sizeof(double) * size_t(wp) * (kTbTY + 2 * H);
             double *mo = last ? mean_out : nullptr;
 #define MGSR_TB_LAUNCH(KK, RCV, RCP, RCM)                                                                  \
     {                                                                                                      \
