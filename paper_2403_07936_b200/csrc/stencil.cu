@@ -150,17 +150,32 @@ __global__ void __launch_bounds__(kTbThreads, 3) k_gs_tb(const double *__restric
         // store (the staging is latency-bound otherwise).
         __syncthreads();   // previous tile's reads of shared memory are done
         double rp[PER], rf[PER];
+        if (inner) {   // interior tile: no periodic wrap (the common case)
+            const int64_t org = int64_t(gy0) * n + gx0;
 #pragma unroll
-        for (int u = 0; u < PER; ++u) {
-            const int idx = tid + u * kTbThreads;
-            rp[u] = 0.0;
-            rf[u] = 0.0;
-            if (idx < NE) {
-                const int ly = idx / W, lx = idx - ly * W;
-                const int64_t g = inner ? int64_t(gy0 + ly) * n + (gx0 + lx)
-                                        : int64_t(wrap(gy0 + ly, n)) * n + wrap(gx0 + lx, n);
-                if (!zero_init) rp[u] = __ldg(pin + g);
-                rf[u] = fs.at(g, sh);
+            for (int u = 0; u < PER; ++u) {
+                const int idx = tid + u * kTbThreads;
+                rp[u] = 0.0;
+                rf[u] = 0.0;
+                if (idx < NE) {
+                    const int ly = idx / W, lx = idx - ly * W;
+                    const int64_t g = org + int64_t(ly) * n + lx;
+                    if (!zero_init) rp[u] = __ldg(pin + g);
+                    rf[u] = fs.at(g, sh);
+                }
+            }
+        } else {
+#pragma unroll
+            for (int u = 0; u < PER; ++u) {
+                const int idx = tid + u * kTbThreads;
+                rp[u] = 0.0;
+                rf[u] = 0.0;
+                if (idx < NE) {
+                    const int ly = idx / W, lx = idx - ly * W;
+                    const int64_t g = int64_t(wrap(gy0 + ly, n)) * n + wrap(gx0 + lx, n);
+                    if (!zero_init) rp[u] = __ldg(pin + g);
+                    rf[u] = fs.at(g, sh);
+                }
             }
         }
 #pragma unroll
