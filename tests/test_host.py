@@ -186,3 +186,34 @@ def test_replicas_gloo_world2(tmp_path):
         assert abs(r["f_mean"]) < 1e-12                # mean-free RHS
     d = res[0]["digests"]
     assert d == res[1]["digests"] and d[0] != d[1]     # each replica solves its own RHS
+
+
+@pytest.mark.parametrize("n_gan", [0.25, 0.5, 1.0, 2.0, 3.0, 1.5])
+def test_device_schedule_matches_schedule_operator(n_gan):
+    """The operator rule k_solve_pre evaluates on device (cadence, first_sr, N_GAN == 1; see
+    mgsr_plan_solve) reproduces schedule_operator (solver.py:122-144) for every iteration and latch."""
+    from paper_2403_07936_b200.solver import _cadence, schedule_operator
+    cad, first_sr, one = _cadence(n_gan)
+
+    def device_rule(it, latched):   # mirror of k_solve_pre for mode = hybrid
+        if latched:
+            sr = not first_sr
+        elif one:
+            sr = bool(it & 1)
+        else:
+            sr = bool(first_sr) if it % cad != 0 else not first_sr
+        return "sr" if sr else "spline"
+
+    for latched in (False, True):
+        for it in range(1, 40):
+            assert device_rule(it, latched) == schedule_operator(it, n_gan, latched)
+
+
+def test_solve_batch_rejects_mixed_sizes():
+    from paper_2403_07936_b200 import solver
+    from paper_2403_07936_b200.grid import Grid
+    from paper_2403_07936_b200.smoother import PoissonProblem
+    a = PoissonProblem(Grid(np.zeros((16, 16))))
+    b = PoissonProblem(Grid(np.zeros((32, 32))))
+    with pytest.raises(ValueError, match="same side"):
+        solver.solve_batch([a, b], solver.RunConfig())
