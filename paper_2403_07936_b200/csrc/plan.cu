@@ -120,6 +120,17 @@ int correction(mgsr_plan *pl, int l, int use_sr, cudaStream_t st) {
     const double h = 2.0 * M_PI / n;
     FSrc fs{pl->rc[l], rc_mean(pl, l), 0.5};
     int r;
+    if (n <= kSmallN && !std::getenv("MGSR_NO_FUSED_SMALL")) {
+        // the whole bottom of the ladder in one CTA, when it is ratio 2 and spline-prolonged
+        bool fusable = L - l <= 8;
+        for (int j = l; fusable && j < L - 1; ++j) {
+            if (pl->sides[j] != 2 * pl->sides[j + 1]) fusable = false;
+            if (use_sr && ((pl->cfg.sr_level_mask >> j) & 1u)) fusable = false;
+        }
+        if (fusable)
+            return launch_correction_small(pl->rc[l], rc_mean(pl, l), pl->d[l], pl->sides.data() + l, L - l,
+                                           pl->cfg.n_smooth, pl->cfg.coarse_sweeps, st);
+    }
     if (l == L - 1) {
         r = launch_gs(nullptr, pl->d[l], pl->tmp, fs, n, h * h, pl->cfg.coarse_sweeps, 1, nullptr, nullptr,
                       d_mean(pl, l), pl->red, st);

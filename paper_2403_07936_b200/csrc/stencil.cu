@@ -107,6 +107,150 @@ __global__ void __launch_bounds__(1024) k_gs_small(double *__restrict__ p, FSrc 
     if (tid == 0 && mean_out) *mean_out = 0.0;   // already gauge-fixed
 }
 
+// ---------------------------------------------------------------------------
+// Whole coarse sub-ladder in ONE CTA: correction(rhs, l) of solver.py:181-190 for
+// a level with side <= kSmallN and every level below it (ratio-2 ladder, spline
+// prolongation).  Per level: GS from zero with the exact per-sweep mean
+// subtraction (_stencil.pyx:38-45), the residual at the injected points and its
+// half-injection 0.5 (r - mean(r)) as the next level's RHS; the coarsest level
+// relaxes coarse_sweeps times; then each level adds the Keys ratio-2
+// prolongation of the level below (the k_prolong2_add arithmetic).  Replaces
+// ~4 launches per level on the latency-bound bottom of every V-cycle.
+constexpr int kSmallMaxLev = 8;
+struct SmallLadder {
+    int nlev;
+    int side[kSmallMaxLev];
+};
+
+__device__ double block_sum_1024(double v, double *sred) {
+    const int tid = threadIdx.x, nt = blockDim.x;
+    v = warp_sum(v);
+    __syncthreads();
+    if ((tid & 31) == 0) sred[tid >> 5] = v;
+    __syncthreads();
+    if (tid < 32) {
+        double w = tid < (nt >> 5) ? sred[tid] : 0.0;
+        w = warp_sum(w);
+        if (tid == 0) sred[32] = w;
+    }
+    __syncthreads();
+    return sred[32];
+}
+
+__global__ void __launch_bounds__(1024) k_correction_small(const double *__restrict__ rc0, const double *rc0_mean,
+                                                           double *__restrict__ d0, SmallLadder L, int n_smooth,
+                                                           int coarse_sweeps) {
+    extern __shared__ double sm[];
+    __shared__ double sred[33];
+    const int tid = threadIdx.x, nt = blockDim.x;
+    double *D[kSmallMaxLev], *F[kSmallMaxLev];
+    {
+        int off = 0;
+        for (int j = 0; j < L.nlev; ++j) {
+            const int nn = L.side[j] * L.side[j];
+            D[j] = sm + off;
+            F[j] = sm + off + nn;
+            off += 2 * nn;
+        }
+    }
+    {   // level 0 RHS: 0.5 * (rc0 - mean)
+        const int n = L.side[0], nn = n * n;
+        const double m = *rc0_mean;
+        for (int c = tid; c < nn; c += nt) F[0][c] = (rc0[c] - m) * 0.5;
+    }
+    for (int j = 0; j < L.nlev; ++j) {
+        const int n = L.side[j], nn = n * n, half = nn >> 1;
+        const double h = 2.0 * M_PI / n, h2 = h * h;
+        double *sp = D[j];
+        const double *sf = F[j];
+        for (int c = tid; c < nn; c += nt) sp[c] = 0.0;
+        __syncthreads();
+        const int sweeps = j == L.nlev - 1 ? coarse_sweeps : n_smooth;
+        for (int s = 0; s < sweeps; ++s) {
+            for (int color = 0; color < 2; ++color) {
+                for (int t = tid; t < half; t += nt) {
+                    int i = t / (n >> 1);
+                    int jj = 2 * (t % (n >> 1)) + ((i + color) & 1);
+                    int im1 = i > 0 ? i - 1 : n - 1, ip1 = i < n - 1 ? i + 1 : 0;
+                    int jm1 = jj > 0 ? jj - 1 : n - 1, jp1 = jj < n - 1 ? jj + 1 : 0;
+                    double nb = ((sp[im1 * n + jj] + sp[ip1 * n + jj]) + sp[i * n + jm1]) + sp[i * n + jp1];
+                    sp[i * n + jj] = (nb - h2 * sf[i * n + jj]) * 0.25;
+                }
+                __syncthreads();
+            }
+            double acc = 0.0;
+            for (int c = tid; c < nn; c += nt) acc += sp[c];
+            const double mean = block_sum_1024(acc, sred) * (1.0 / double(nn));
+            for (int c = tid; c < nn; c += nt) sp[c] -= mean;
+            __syncthreads();
+        }
+        if (j < L.nlev - 1) {   // residual at the injected (even, even) points -> next RHS
+            const int nc = n >> 1, ncc = nc * nc;
+            const double inv_h2 = 1.0 / h2;
+            double *fr = F[j + 1];
+            double acc = 0.0;
+            for (int t = tid; t < ncc; t += nt) {
+                const int ic = t / nc, jc = t - ic * nc;
+                const int i = 2 * ic, jj = 2 * jc;
+                const int im1 = i > 0 ? i - 1 : n - 1, ip1 = i < n - 1 ? i + 1 : 0;
+                const int jm1 = jj > 0 ? jj - 1 : n - 1, jp1 = jj < n - 1 ? jj + 1 : 0;
+                const int c = i * n + jj;
+                double nb = ((sp[im1 * n + jj] + sp[ip1 * n + jj]) + sp[i * n + jm1]) + sp[i * n + jp1];
+                const double res = sf[c] - ((nb - 4.0 * sp[c]) * inv_h2);
+                fr[t] = res;
+                acc += res;
+            }
+            const double mean = block_sum_1024(acc, sred) * (1.0 / double(ncc));
+            for (int t = tid; t < ncc; t += nt) fr[t] = (fr[t] - mean) * 0.5;
+            __syncthreads();
+        }
+    }
+    // ascend: D[j] += P2(D[j + 1])
+    const double w0 = -0.0625, w1 = 0.5625;
+    for (int j = L.nlev - 2; j >= 0; --j) {
+        const int nc = L.side[j + 1], n = 2 * nc;
+        const double *c = D[j + 1];
+        double *out = D[j];
+        for (int t = tid; t < nc * nc; t += nt) {
+            const int bi = t / nc, bj = t - bi * nc;
+            int ri[4];
+#pragma unroll
+            for (int o = 0; o < 4; ++o) {
+                const int r = bi + o - 1;
+                ri[o] = r < 0 ? r + nc : (r >= nc ? r - nc : r);
+            }
+            double R0[4], R1[4];
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                int cb = bj + b - 1;
+                cb = cb < 0 ? cb + nc : (cb >= nc ? cb - nc : cb);
+                const double c0 = c[ri[0] * nc + cb], c1 = c[ri[1] * nc + cb];
+                const double c2 = c[ri[2] * nc + cb], c3 = c[ri[3] * nc + cb];
+                R0[b] = c1;
+                double row = 0.0;
+                row += w0 * c0;
+                row += w1 * c1;
+                row += w1 * c2;
+                row += w0 * c3;
+                R1[b] = row;
+            }
+            double a01 = 0.0, a11 = 0.0;
+            a01 += w0 * R0[0]; a01 += w1 * R0[1]; a01 += w1 * R0[2]; a01 += w0 * R0[3];
+            a11 += w0 * R1[0]; a11 += w1 * R1[1]; a11 += w1 * R1[2]; a11 += w0 * R1[3];
+            const int t0 = (2 * bi) * n + 2 * bj, t1 = t0 + n;
+            out[t0] = (out[t0] - 0.0) + R0[1];
+            out[t0 + 1] = (out[t0 + 1] - 0.0) + a01;
+            out[t1] = (out[t1] - 0.0) + R1[1];
+            out[t1 + 1] = (out[t1 + 1] - 0.0) + a11;
+        }
+        __syncthreads();
+    }
+    {
+        const int nn = L.side[0] * L.side[0];
+        for (int c = tid; c < nn; c += nt) d0[c] = D[0][c];
+    }
+}
+
 // Temporally blocked K-sweep GS.  A TY x TX tile plus a halo of H cells is
 // staged in shared memory; 2K half-sweeps run there (the invalid outer ring
 // grows by one cell per half-sweep and never reaches the interior +- 1), the
@@ -664,6 +808,26 @@ int launch_finalize(const double *out, const double *mean_ptr, double *p, FSrc f
     k_finalize<<<grid_2d(n, n), 256, 0, st>>>(out, mean_ptr, p, fs, n, 1.0 / (h * h), sl, acc3);
     MGSR_LAUNCH_CHECK();
     k_stats_sqrt<<<1, 1, 0, st>>>(acc3, stats2);
+    MGSR_LAUNCH_CHECK();
+    return MGSR_OK;
+}
+
+int launch_correction_small(const double *rc0, const double *rc0_mean, double *d0, const int *sides, int nlev,
+                            int n_smooth, int coarse_sweeps, cudaStream_t st) {
+    if (nlev < 1 || nlev > kSmallMaxLev || sides[0] > kSmallN) {
+        set_error("correction_small: bad ladder");
+        return MGSR_E_BAD_ARG;
+    }
+    SmallLadder L{};
+    L.nlev = nlev;
+    size_t smem = 0;
+    for (int j = 0; j < nlev; ++j) {
+        L.side[j] = sides[j];
+        if (j > 0 && sides[j] * 2 != sides[j - 1]) { set_error("correction_small: ratio-2 ladder only"); return MGSR_E_BAD_ARG; }
+        smem += 2 * sizeof(double) * size_t(sides[j]) * sides[j];
+    }
+    cudaFuncSetAttribute(k_correction_small, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    k_correction_small<<<1, 1024, smem, st>>>(rc0, rc0_mean, d0, L, n_smooth, coarse_sweeps);
     MGSR_LAUNCH_CHECK();
     return MGSR_OK;
 }
