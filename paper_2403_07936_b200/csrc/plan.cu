@@ -282,6 +282,14 @@ extern "C" int mgsr_plan_vcycle(mgsr_plan *pl, double *p, const double *f, int32
     }
     auto key = std::make_tuple(p, f, int(use_sr != 0));
     auto it = pl->graphs.find(key);
+    if (it == pl->graphs.end() && pl->graphs.size() >= 16) {
+        // bounded cache: callers cycling through many buffers re-capture instead of growing without end
+        for (auto &kv : pl->graphs) {
+            cudaGraphExecDestroy(kv.second.exec);
+            cudaGraphDestroy(kv.second.graph);
+        }
+        pl->graphs.clear();
+    }
     if (it == pl->graphs.end()) {
         // capture on the plan's own stream, then instantiate once
         MGSR_CUDA_TRY(cudaStreamSynchronize(st));
@@ -483,6 +491,13 @@ extern "C" int mgsr_plan_solve(mgsr_plan *pl, double *p, const double *f, int32_
     }
     auto key = std::make_tuple(p, f, int(mode), int(n_iter), tol, s_thres, int(cadence), int(first_sr), int(ngan_one));
     auto it = pl->solves.find(key);
+    if (it == pl->solves.end() && pl->solves.size() >= 8) {
+        for (auto &kv : pl->solves) {
+            cudaGraphExecDestroy(kv.second.exec);
+            cudaGraphDestroy(kv.second.graph);
+        }
+        pl->solves.clear();
+    }
     if (it == pl->solves.end()) {
         MGSR_CUDA_TRY(cudaStreamSynchronize(st));
         cudaGraph_t g = nullptr;
