@@ -685,6 +685,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
         const int row = 32 * q + lane;         // row within a tile
         const int wt = row >> 6, pix = row & 63, py = pix >> 3, px = pix & 7;
         const bool interior = py >= 1 && py <= 6 && px >= 1 && px <= 6;
+        // lane holding the interior pixel this row replicates (itself when interior); always the same warp
+        const int pad_src = (min(max(py, 1), 6) * 8 + min(max(px, 1), 6)) - 32 * (q & 1);
         const uint32_t lane_addr = uint32_t(32 * q) << 16;
         uint32_t af_ph[T] = {0, 0, 0};
         int i2c_uses[2] = {0, 0};   // builds into im2col buffer b so far
@@ -818,7 +820,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
                     uint32_t pk[8];
 #pragma unroll
                     for (int j = 0; j < 8; ++j) pk[j] = pack_op<F16>(y[2 * j], y[2 * j + 1]);
-                    store_row<true>(act, t, row, 2 * cq, pk);
+                    {   // replicate padding without partial stores: a ring row takes the packed values of its
+                        // clamped interior source row (same warp) by shuffle, then every lane writes its own
+                        // row -- two full-warp contiguous 16-byte stores per tile-layer
+                        uint32_t sv[8];
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) sv[j] = __shfl_sync(0xffffffffu, pk[j], pad_src);
+                        uint8_t *dst = act + (2 * cq) * ACT_PLANE + (GUARD + t * ROWS + row) * 16;
+                        *reinterpret_cast<uint4 *>(dst) = make_uint4(sv[0], sv[1], sv[2], sv[3]);
+                        *reinterpret_cast<uint4 *>(dst + ACT_PLANE) = make_uint4(sv[4], sv[5], sv[6], sv[7]);
+                    }
                     if (P.dbg && P.dbg_layer == L + 1 && interior) {
                         const long long k = k0 + t * WPT + wt;
                         if (k < P.nwin) {
