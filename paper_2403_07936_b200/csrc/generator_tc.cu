@@ -1038,7 +1038,9 @@ __global__ void k_normalize(const double *__restrict__ c, const double *shift, i
 // the reference's replicate clamping (srmodel.py:285-289) on the 12x12 field.
 template <bool F16>
 __global__ void __launch_bounds__(256) k_tail_edge(Params P) {
-    __shared__ float U[64 * 144];   // [c][Y][X]
+    __shared__ float U[64 * 144];       // [c][Y][X]
+    __shared__ float Wt[3 * 8 * 81];    // weights of one 8-channel chunk [o][c][tap]
+    __shared__ float part[144 * 3];     // per (pixel, o) results (<= 144 kept pixels: the npos = 1 window)
     const int e = blockIdx.x;
     // invert edge_index
     int wi, wj;
@@ -1053,32 +1055,62 @@ __global__ void __launch_bounds__(256) k_tail_edge(Params P) {
         const int Y = 2 * (pp / 6) + ii, X = 2 * (pp % 6) + jj;
         U[c * 144 + Y * 12 + X] = op_lo<F16>(uint32_t(src[i]));
     }
-    __syncthreads();
     const BlobLayout BL = blob_layout((P.nl - 1) / 2);
     const float *w = reinterpret_cast<const float *>(P.blob + BL.tail_f32);   // [3][64][81]
     const float *bias = reinterpret_cast<const float *>(P.blob + BL.consts) + 64 + 192 * P.nl + 64;
     const int last = P.npos - 1;
     const int lo_i = wi == 0 ? 0 : 2, hi_i = wi == last ? 6 : 4, lo_j = wj == 0 ? 0 : 2, hi_j = wj == last ? 6 : 4;
-    const int wk = 2 * (hi_j - lo_j), npix = 2 * (hi_i - lo_i) * wk;
-    for (int idx = threadIdx.x; idx < npix; idx += blockDim.x) {
-        const int fy = 2 * lo_i + idx / wk, fx = 2 * lo_j + idx % wk;
-        double m = 0.0;
-        for (int o = 0; o < 3; ++o) {
-            float acc = 0.f;
-            for (int c = 0; c < 64; ++c) {
-                const float *wc = w + (o * 64 + c) * 81;
-                const float *uc = U + c * 144;
-                for (int dy = 0; dy < 9; ++dy) {
-                    const int Y = min(max(fy + dy - 4, 0), 11);
+    const int wk = 2 * (hi_j - lo_j), npix = 2 * (hi_i - lo_i) * wk;   // <= 144 kept pixels
+    // work item = (pixel, output o), up to two per thread; weights staged per 8-channel chunk, U reused
+    // from shared memory
+    int yo[2][9], xo[2][9], wo[2];
+    bool act[2];
+    float acc[2] = {0.f, 0.f};
 #pragma unroll
-                    for (int dx = 0; dx < 9; ++dx) acc = fmaf(uc[Y * 12 + min(max(fx + dx - 4, 0), 11)], __ldg(wc + dy * 9 + dx), acc);
-                }
+    for (int h = 0; h < 2; ++h) {
+        const int item = threadIdx.x + h * blockDim.x, idx = item / 3;
+        wo[h] = item - 3 * idx;
+        act[h] = idx < npix;
+        const int fy = act[h] ? 2 * lo_i + idx / wk : 0, fx = act[h] ? 2 * lo_j + idx % wk : 0;
+#pragma unroll
+        for (int d = 0; d < 9; ++d) {
+            yo[h][d] = min(max(fy + d - 4, 0), 11) * 12;
+            xo[h][d] = min(max(fx + d - 4, 0), 11);
+        }
+    }
+    for (int ck = 0; ck < 8; ++ck) {
+        __syncthreads();   // U staged / previous chunk's weights consumed
+        for (int i = threadIdx.x; i < 3 * 8 * 81; i += blockDim.x) {
+            const int oo = i / (8 * 81), rem = i - oo * 8 * 81;
+            Wt[i] = __ldg(w + (oo * 64 + 8 * ck) * 81 + rem);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            if (!act[h]) continue;
+            for (int c = 0; c < 8; ++c) {
+                const float *uc = U + (8 * ck + c) * 144;
+                const float *wc = Wt + (wo[h] * 8 + c) * 81;
+#pragma unroll
+                for (int dy = 0; dy < 9; ++dy)
+#pragma unroll
+                    for (int dx = 0; dx < 9; ++dx) acc[h] = fmaf(uc[yo[h][dy] + xo[h][dx]], wc[dy * 9 + dx], acc[h]);
             }
-            const float pre = acc + __ldg(bias + o);
+        }
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+        if (act[h]) part[threadIdx.x + h * blockDim.x] = acc[h];
+    __syncthreads();
+    for (int i = threadIdx.x; i < npix; i += blockDim.x) {
+        const int gy = 2 * lo_i + i / wk, gx = 2 * lo_j + i % wk;
+        double m = 0.0;
+        for (int oo = 0; oo < 3; ++oo) {
+            const float pre = part[i * 3 + oo] + __ldg(bias + oo);
             m += double(P.tanh_s * tanhf(pre / P.tanh_s));
         }
         m = m / 3.0;
-        P.fine[(long long)(2 * (2 * wi) + fy) * P.nf + 2 * (2 * wj) + fx] = denormalize_q(m, P.log_lo, P.span);
+        P.fine[(long long)(2 * (2 * wi) + gy) * P.nf + 2 * (2 * wj) + gx] = denormalize_q(m, P.log_lo, P.span);
     }
 }
 
