@@ -82,21 +82,22 @@ constexpr int HB_HALF = HB_BYTES / 2;                    // 6144, streamed throu
 constexpr int IDX_OFF = 1024;                            // in misc: uint8 [64 padded pixels][96 k] -> q index
 static_assert(2 * I2C_BYTES <= UNION_BYTES, "union");
 static_assert(IDX_OFF + 64 * HK <= MISC_BYTES, "misc");
-// up phase (union): the up-conv quarter, pixel-shuffled, bf16 [window][12x12][16 ch] with a 48-byte
-// pixel stride (conflict-free ldmatrix rows), double-buffered over tiles; tail weights of the quarter
-// bf16 [tap 81][o 3][16 ch] (double-buffered over quarters); a zero row; the reduction scratch.
+// up phase (union): per tile, the up-conv quarter pixel-shuffled onto the 12x12 fine window, as the A
+// operand of the tail: 2 planes (8 channels each) x [Y 12][window 2][X 16] pixel rows of 16 B (X 12..15
+// are never written: they only feed discarded rows).  A tail MMA's A rows are (y - 4, window, X) for the
+// kept rows y = 4..7, so the vertical tap dy is a 32-row descriptor shift; the horizontal tap dx and the
+// output o go along N (n = 3 dx + o, 27 of 32).  Tail weights: per quarter, this CTA's 16 N rows,
+// [dy 9][k 2][16 n][8] (the producer streams one slot per quarter).
 constexpr int UQ = 16;
 constexpr int UP_QUARTERS_C = 4;
-constexpr int U_PIX_B = 48;
-constexpr int U_TILE_BYTES = WPT * 144 * U_PIX_B;      // 13824
-
-constexpr int U_OFF0 = 0;
-constexpr int TW_OFF0 = 2 * U_TILE_BYTES;              // 27648
-constexpr int TW_SLOTS = UP_QUARTERS_C;                // one tail-weight slot per up quarter
-constexpr int ZERO_OFF = TW_OFF0 + TW_SLOTS * 7808;    // 58880
-constexpr int RED_OFF = ZERO_OFF + 64;                 // 58944
-constexpr int RED_BYTES = 16 * 16 * 8 * 4;             // 8192: [unit 16][row 16][8] fp32
-static_assert(RED_OFF + RED_BYTES <= UNION_BYTES, "union");
+constexpr int U_PIX = 12 * WPT * 16;                   // 384 pixel rows per tile
+constexpr int U_PLANE = U_PIX * 16;                    // 6144
+constexpr int U_BUF = 2 * U_PLANE;                     // 12288: one tile's 16 channels
+constexpr int U_OFF0 = 0;                              // T buffers, one per tile
+constexpr int TW_HALF = 9 * 512;                       // 4608: this CTA's half of a quarter's tail weights
+constexpr int TW_QBYTES = 2 * TW_HALF;                 // a quarter in the blob (both halves)
+constexpr int TW_OFF0 = T * U_BUF;                     // 36864
+static_assert(TW_OFF0 + UP_QUARTERS_C * TW_HALF <= UNION_BYTES, "union");
 constexpr int OFF_ACT = 0;
 constexpr int OFF_RING = OFF_ACT + ACT_BYTES;
 constexpr int OFF_UNION = OFF_RING + RING_BYTES;
@@ -105,6 +106,7 @@ constexpr int OFF_BAR = OFF_MISC + MISC_BYTES;
 constexpr int OFF_CONST = OFF_BAR + BAR_BYTES;
 // TMEM columns
 constexpr int COL_ACC = 0, COL_RES = 192, COL_SKIP = 384;
+constexpr int COL_Z = COL_SKIP;   // tail accumulators (32 per tile) reuse the skip columns once the post layer read them
 
 constexpr int NEPI = 16;                       // epilogue warps
 constexpr int NTHREADS = 64 + 32 * NEPI;       // 576
@@ -128,7 +130,7 @@ __host__ __device__ inline BlobLayout blob_layout(int blocks) {
     L.body = L.head_b + HB_BYTES;
     L.up = L.body + size_t(L.nl) * 9 * TAP_BYTES;
     L.tail = L.up + size_t(UP_QUARTERS) * 9 * TAP_BYTES;
-    L.tail_f32 = L.tail + size_t(UP_QUARTERS) * 7808;   // then [3][64][81] fp32 (edge kernel)
+    L.tail_f32 = L.tail + size_t(UP_QUARTERS) * TW_QBYTES;   // then [3][64][81] fp32 (edge kernel)
     L.consts = L.tail_f32 + sizeof(float) * 3 * 64 * 81;
     // fp16 operand set (body, up, tail) follows at +fmt_stride from the bf16 set
     L.fmt_stride = ((L.consts + sizeof(float) * const_floats(L.nl)) + 1023) & ~size_t(1023);
@@ -243,29 +245,6 @@ __device__ __forceinline__ bool elect_one() {
     return pred != 0;
 }
 
-__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t (&r)[4]) {
-    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
-                 : "r"(addr));
-}
-__device__ __forceinline__ void ldsm_x2(uint32_t addr, uint32_t (&r)[2]) {
-    asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0,%1}, [%2];" : "=r"(r[0]), "=r"(r[1]) : "r"(addr));
-}
-template <bool F16>
-__device__ __forceinline__ void mma_16816(float (&c)[4], const uint32_t (&a)[4], const uint32_t (&b)[2]) {
-    if (F16)
-        asm volatile(
-            "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-            "{%0,%1,%2,%3};"
-            : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-            : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
-    else
-        asm volatile(
-            "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-            "{%0,%1,%2,%3};"
-            : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-            : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
-}
 __device__ __forceinline__ void lds16(const float *src, float (&dst)[16]) {
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -442,10 +421,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
     const uint32_t b_i2c_empty = smem_u32(bars + BB + 35);          // [2] (both) im2col buffer consumed
     const uint32_t b_acc_full = smem_u32(bars + BB + 2);    // [T] (both) MMA -> epilogue: accumulator ready
     const uint32_t b_act_ready = smem_u32(bars + BB + 5);   // [T] (leader) epilogues -> MMA: act written
-    const uint32_t b_ubuf_full = smem_u32(bars + BB + 8);   // [2] drain warps -> tail warps: U buffer written
-    const uint32_t b_ubuf_free = smem_u32(bars + BB + 10);  // [2] tail warps -> drain warps: U buffer consumed
-    const uint32_t b_tw_full = smem_u32(bars + BB + 25);    // [4] producer -> tail warps: quarter weights landed
-    const uint32_t b_tw_empty = smem_u32(bars + BB + 29);   // [4] tail warps -> producer: fragments taken
+    const uint32_t b_ubuf_full = smem_u32(bars + BB + 37);  // [T] (leader) drains -> MMA: tile's U written (both CTAs)
+    const uint32_t b_ubuf_free = smem_u32(bars + BB + 40);  // [T] (both) tail MMAs -> drains: tile's U consumed
+    const uint32_t b_zfull = smem_u32(bars + BB + 43);      // [T] (both) last tail MMAs -> epilogue: Z ready
+    const uint32_t b_tw_full = smem_u32(bars + BB + 25);    // [4] this CTA's quarter tail weights landed
+    const uint32_t b_tw_peerfull = smem_u32(bars + BB + 46);   // [4] (leader) the peer's landed
+    const uint32_t b_tw_empty = smem_u32(bars + BB + 29);   // [4] (both) tail MMAs of the quarter done
     const uint32_t b_drained = smem_u32(bars + BB + 16);    // [2][T] (leader) drain warps -> MMA: up buffer free
     const uint32_t b_acc_full2 = smem_u32(bars + BB + 22);  // [T] (both) MMA -> drain: up accumulator buffer 1 ready
     const uint32_t rank = cluster_rank();
@@ -476,17 +457,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
         for (int t = 0; t < T; ++t) {
             mbar_init(b_acc_full + 8 * t, 1);
             mbar_init(b_act_ready + 8 * t, 2 * NEPI);
-            if (t < 2) {
-                mbar_init(b_ubuf_full + 8 * t, NEPI / 2);
-                mbar_init(b_ubuf_free + 8 * t, NEPI / 2);
-            }
-            mbar_init(b_drained + 8 * t, NEPI);
+            mbar_init(b_ubuf_full + 8 * t, 2 * NEPI);
+            mbar_init(b_ubuf_free + 8 * t, 1);
+            mbar_init(b_zfull + 8 * t, 1);
+            mbar_init(b_drained + 8 * t, 2 * NEPI);
             mbar_init(b_acc_full2 + 8 * t, 1);
-            mbar_init(b_drained + 8 * (T + t), NEPI);
+            mbar_init(b_drained + 8 * (T + t), 2 * NEPI);
         }
         for (int u = 0; u < UP_QUARTERS_C; ++u) {
             mbar_init(b_tw_full + 8 * u, 1);
-            mbar_init(b_tw_empty + 8 * u, NEPI / 2);
+            mbar_init(b_tw_peerfull + 8 * u, 1);
+            mbar_init(b_tw_empty + 8 * u, 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -528,14 +509,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
                 for (int tap = 0; tap < 9; ++tap)
                     fill(wblob + P.wfmt + BL.body + (size_t(L) * 9 + tap) * TAP_BYTES + rank * SLOT_BYTES);
             for (int u = 0; u < UP_QUARTERS; ++u) {
-                {   // the quarter's tail weights -> TW[u] (union; free once last group's quarter u took them)
-                    const int ts = u;
-                    mbar_wait(b_tw_empty + 8 * ts, tw_ph[ts] ^ 1u);
-                    tw_ph[ts] ^= 1u;
+                {   // this CTA's half of the quarter's tail weights -> TW[u] (union; free once the last
+                    // group's tail MMAs of quarter u completed)
+                    mbar_wait(b_tw_empty + 8 * u, tw_ph[u] ^ 1u);
+                    tw_ph[u] ^= 1u;
                     if (elect_one()) {
-                        mbar_expect_tx(b_tw_full + 8 * ts, 7808);
-                        bulk_g2s(smem_u32(uni + TW_OFF0 + ts * 7808), wblob + P.wfmt + BL.tail + size_t(u) * 7808, 7808,
-                                 b_tw_full + 8 * ts);
+                        mbar_expect_tx(b_tw_full + 8 * u, TW_HALF);
+                        bulk_g2s(smem_u32(uni + TW_OFF0 + u * TW_HALF),
+                                 wblob + P.wfmt + BL.tail + size_t(u) * TW_QBYTES + rank * TW_HALF, TW_HALF,
+                                 b_tw_full + 8 * u);
                     }
                     __syncwarp();
                 }
@@ -545,17 +527,27 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
         }
     } else if (warp == 1 && !leader) {
         // ================= peer: forward "slot landed" to the leader =================
-        uint32_t ph = 0;
+        uint32_t ph = 0, twp = 0;
         int slot = 0;
-        const int fills = 2 + (NLAYERS + UP_QUARTERS) * 9;
-        for (int gp = pair; gp < ngp; gp += npairs)
-            for (int i = 0; i < fills; ++i) {
+        auto fwd = [&](int nfills) {
+            for (int i = 0; i < nfills; ++i) {
                 mbar_wait(b_full + 8 * slot, (ph >> slot) & 1u);
                 if (elect_one()) mbar_arrive_leader(b_peerfull + 8 * slot);
                 __syncwarp();
                 ph ^= 1u << slot;
                 slot = slot == NSLOT - 1 ? 0 : slot + 1;
             }
+        };
+        for (int gp = pair; gp < ngp; gp += npairs) {   // same order as the producer's fills
+            fwd(2 + NLAYERS * 9);
+            for (int u = 0; u < UP_QUARTERS; ++u) {
+                mbar_wait(b_tw_full + 8 * u, twp);
+                if (elect_one()) mbar_arrive_leader(b_tw_peerfull + 8 * u);
+                __syncwarp();
+                fwd(9);
+            }
+            twp ^= 1u;
+        }
     } else if (warp == 1) {
         // ================= MMA issuer (leader; warp-uniform control, one elected lane issues) =================
         uint32_t ph = 0, i2c_ph = 0;   // i2c_ph bit b: parity of the next completion of b_i2c_full[b]
@@ -623,6 +615,33 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
             slot0 += 9;
             slot0 = slot0 >= NSLOT ? slot0 - NSLOT : slot0;
         };
+        // pruned 9x9 tail, quarter u: Z[t] (M = 256 kept-row pixels, N = 32 = 3 dx + o) += sum over dy of
+        // U[t] shifted by dy rows x TW[u][dy]; 9 MMAs per tile
+        const uint32_t idz = F16 ? idesc_f16(32) : idesc_bf16(32);
+        uint32_t grp_ph = 0;   // parity of this pair's group iteration (one TW / Z completion per group)
+        auto tail_mma = [&](int u) {
+            mbar_wait(b_tw_full + 8 * u, grp_ph);
+            mbar_wait(b_tw_peerfull + 8 * u, grp_ph);
+#pragma unroll 1
+            for (int t = 0; t < T; ++t) {
+                mbar_wait(b_ubuf_full + 8 * t, uint32_t(u & 1));
+                if (lane == 0) tr(16, u, t);
+                tc_fence_after();
+                if (elect_one()) {
+                    const uint32_t d = tmem + COL_Z + 32 * t;
+#pragma unroll
+                    for (int dy = 0; dy < 9; ++dy) {
+                        const uint64_t a = make_desc(uni_base + U_OFF0 + t * U_BUF + dy * (32 * 16), U_PLANE, 128);
+                        const uint64_t b = make_desc(uni_base + TW_OFF0 + u * TW_HALF + dy * 512, 256, 128);
+                        mma_bf16(d, a, b, idz, (u | dy) > 0);
+                    }
+                    umma_commit(b_ubuf_free + 8 * t);
+                    if (u == UP_QUARTERS - 1) umma_commit(b_zfull + 8 * t);
+                    if (t == T - 1) umma_commit(b_tw_empty + 8 * u);
+                }
+                __syncwarp();
+            }
+        };
         for (int gp = pair; gp < ngp; gp += npairs) {
             tr.buf = (P.prof && blockIdx.x == 0 && gp == TRACE_GROUP * npairs) ? P.prof + 4096 : nullptr;
             // head: D[t] = im2col(q) (128 x 96, fp16) x Wh^T (96 x 64); im2col buffer t & 1
@@ -670,10 +689,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
             for (int L = 0; L < NLAYERS; ++L) conv_layer(L + 1, 0, COL_ACC);
             // up quarters, accumulators double-buffered over cols [0, 192) and [192, 384) (the residual
             // stream and skip are dead after the post layer): quarter u + 1 runs while u drains
+            // the tail of quarter u issues after up quarter u + 1, once quarter u is drained into U
             conv_layer(40, 0, COL_ACC);
             conv_layer(41, 1, COL_RES);
+            tail_mma(0);
             conv_layer(42, 2, COL_ACC);
+            tail_mma(1);
             conv_layer(43, 3, COL_RES);
+            tail_mma(2);
+            tail_mma(3);
+            grp_ph ^= 1u;
         }
     } else {
         // ================= epilogue (warps 2..17) =================
@@ -690,7 +715,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
         const uint32_t lane_addr = uint32_t(32 * q) << 16;
         uint32_t af_ph[T] = {0, 0, 0};
         int i2c_uses[2] = {0, 0};   // builds into im2col buffer b so far
-        if (lane == 0 && ew < NEPI / 2)
+        if (lane == 0)
             for (int t = 0; t < T; ++t) mbar_arrive_leader(b_drained + 8 * t);   // up buffer 0 (= head accumulator) starts free
         const float *head_a = cs;
         uint8_t *idx_tab = reinterpret_cast<uint8_t *>(smem + OFF_MISC + IDX_OFF);
@@ -707,8 +732,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
         const float *up_a = cs + 64 + 192 * NL;
         const float *tail_b = up_a + 64;
         Tracer tr{nullptr, 0};
-        uint32_t tw_full_ph = 0;   // tail warps: bit s = parity of the next completion of b_tw_full[s]
-        uint32_t af2_ph = 0;       // drain warps: bit t = parity of the next completion of b_acc_full2[t]
+        uint32_t af2_ph = 0;   // bit t = parity of the next completion of b_acc_full2[t]
+        uint32_t z_ph = 0;     // parity of the next completion of b_zfull (one per group)
         for (int gp = pair; gp < ngp; gp += npairs) {
             const int g = 2 * gp + int(rank);
             const long long k0 = (long long)g * WPG;
@@ -845,176 +870,116 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
                     tr(7, L + 1, t);
                 }
             }
-            // ---- up quarters.  Roles split for this phase:
-            //  * drain warps (ew < 8: quadrant q, 32 columns each) read the up accumulator, apply PReLU and
-            //    write the pixel-shuffled quarter (bf16, 16 channels) into U buffer (step & 1); edge windows
-            //    also spill their unshuffled output for k_tail_edge;
-            //  * tail warps (ew >= 8) run the pruned 9x9 tail of interior windows on mma.sync m16n8k16:
-            //    A rows = the window's 16 kept pixels gathered by ldmatrix (kept outputs read only in-window
-            //    pixels, so no clamping), B = the tap's weights (n = o, 3 of 8 used); unit = (window, group of
-            //    ~10 taps), two per warp; fp32 accumulators stay in registers across the four quarters.
-            //  U buffers hand off through mbarriers (ubuf_full / ubuf_free), so draining runs ahead. ----
-            const uint32_t uni_s = smem_u32(uni);
-            if (ew < NEPI / 2) {
-                const int ch = ew >> 2;   // column half: quarter columns 32 ch .. 32 ch + 31
-                for (int u = 0; u < UP_QUARTERS; ++u) {
-                    float ua[8];
+            // ---- up quarters: every epilogue warp drains 16 columns (4 shuffled channels x 4 sub-pixels) of
+            // its lane quadrant: PReLU, then the quarter goes pixel-shuffled into U[t], the A operand of the
+            // tail MMAs (edge windows also spill it for k_tail_edge).  U[t] is rewritten for quarter u once
+            // the tail MMAs of quarter u - 1 released it. ----
+            for (int u = 0; u < UP_QUARTERS; ++u) {
+                float ua[4];
 #pragma unroll
-                    for (int m = 0; m < 8; ++m) ua[m] = up_a[UQ * u + 8 * ch + m];
+                for (int m = 0; m < 4; ++m) ua[m] = up_a[UQ * u + 4 * cq + m];
 #pragma unroll
-                    for (int t = 0; t < T; ++t) {
-                        const int step = u * T + t, ub = step & 1;
-                        if (u & 1) {
-                            mbar_wait(b_acc_full2 + 8 * t, (af2_ph >> t) & 1u);
-                            af2_ph ^= 1u << t;
-                        } else {
-                            mbar_wait(b_acc_full + 8 * t, af_ph[t]);
-                            af_ph[t] ^= 1;
-                        }
-                        tr(8, u, t);
-                        tc_fence_after();
-                        uint32_t v0[16], v1[16];
-                        const uint32_t ucol = (u & 1 ? COL_RES : COL_ACC) + 64 * t + 32 * ch;
-                        TMEM_LD16(tmem + lane_addr + ucol, v0);
-                        TMEM_LD16(tmem + lane_addr + ucol + 16, v1);
-                        tmem_wait_ld();
-                        tc_fence_before();
-                        __syncwarp();
-                        if (lane == 0) mbar_arrive_leader(b_drained + 8 * ((u & 1) * T + t));
-                        mbar_wait(b_ubuf_free + 8 * ub, ((step >> 1) & 1) ^ 1);   // tail of step - 2 done
-                        tr(9, u, t);
-                        if (interior) {
-                            // column j = 32 ch + jj -> up channel 64 u + j -> shuffled c = 16 u + 8 ch + jj/4,
-                            // sub-pixel (i, j') = ((jj >> 1) & 1, jj & 1)
-                            uint8_t *Uw = uni + U_OFF0 + ub * U_TILE_BYTES + wt * (144 * U_PIX_B);
-                            const long long k = k0 + t * WPT + wt;
-                            const Win W = window_of(P, k);
-                            const int pp = (py - 1) * 6 + (px - 1);
-#pragma unroll
-                            for (int hf = 0; hf < 2; ++hf) {
-                                float y[16];
-#pragma unroll
-                                for (int j = 0; j < 16; ++j) {
-                                    const float x = __uint_as_float(hf ? v1[j] : v0[j]);
-                                    y[j] = x > 0.f ? x : ua[4 * hf + (j >> 2)] * x;
-                                }
-#pragma unroll
-                                for (int sub = 0; sub < 4; ++sub) {
-                                    const int Y = 2 * (py - 1) + (sub >> 1), X = 2 * (px - 1) + (sub & 1);
-                                    *reinterpret_cast<uint2 *>(Uw + (Y * 12 + X) * U_PIX_B + 16 * ch + 8 * hf) =
-                                        make_uint2(pack_op<F16>(y[sub], y[4 + sub]), pack_op<F16>(y[8 + sub], y[12 + sub]));
-                                }
-                                if (W.valid && W.edge) {
-                                    uint32_t pk[8];
-#pragma unroll
-                                    for (int j = 0; j < 8; ++j) pk[j] = pack_op<F16>(y[2 * j], y[2 * j + 1]);
-                                    uint4 *dst = reinterpret_cast<uint4 *>(P.edge_u +
-                                        (size_t(edge_index(W.wi, W.wj, P.npos)) * 36 + pp) * 256 + 64 * u + 32 * ch + 16 * hf);
-                                    dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-                                    dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
-                                }
-                                if (P.dbg && P.dbg_layer == NL + 1 && W.valid) {
-#pragma unroll
-                                    for (int j = 0; j < 16; ++j) {
-                                        const int c = UQ * u + 8 * ch + 4 * hf + (j >> 2), Y = 2 * (py - 1) + ((j >> 1) & 1),
-                                                  X = 2 * (px - 1) + (j & 1);
-                                        P.dbg[(k * 144 + Y * 12 + X) * 64 + c] = y[j];
-                                    }
-                                }
-                            }
-                        }
-                        __syncwarp();
-                        if (lane == 0) mbar_arrive(b_ubuf_full + 8 * ub);
-                        tr(10, u, t);
+                for (int t = 0; t < T; ++t) {
+                    if (u & 1) {
+                        mbar_wait(b_acc_full2 + 8 * t, (af2_ph >> t) & 1u);
+                        af2_ph ^= 1u << t;
+                    } else {
+                        mbar_wait(b_acc_full + 8 * t, af_ph[t]);
+                        af_ph[t] ^= 1;
                     }
-                }
-            } else {
-                const int tw = ew - NEPI / 2;                                        // 0..7
-                const int r = (lane & 7) + ((lane >> 3) & 1) * 8, kh = lane >> 4;   // A row / k half of this lane
-                const int n = lane & 7, kb = (lane >> 3) & 1;                      // B row / k half
-                // this warp's tap group (the same for both windows of a tile): taps [tap_lo, tap_lo + ntap)
-                const int tap_lo = (81 * tw) >> 3, ntap = ((81 * (tw + 1)) >> 3) - tap_lo;   // 10 or 11
-                float tacc[T][2][4];   // [tile][window][fragment]
+                    tr(8, u, t);
+                    tc_fence_after();
+                    uint32_t v[16];
+                    TMEM_LD16(tmem + lane_addr + (u & 1 ? COL_RES : COL_ACC) + 64 * t + cb, v);
+                    tmem_wait_ld();
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_leader(b_drained + 8 * ((u & 1) * T + t));
+                    if (u > 0) mbar_wait(b_ubuf_free + 8 * t, uint32_t(u - 1) & 1u);
+                    tr(9, u, t);
+                    if (interior) {
+                        // column 16 cq + j -> shuffled channel 16 u + 4 cq + j / 4, sub-pixel ((j >> 1) & 1, j & 1)
+                        float y[16];
 #pragma unroll
-                for (int t = 0; t < T; ++t)
-#pragma unroll
-                    for (int k = 0; k < 2; ++k)
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) tacc[t][k][e] = 0.f;
-                if (tw == 0 && lane < 4) reinterpret_cast<uint4 *>(uni + ZERO_OFF)[lane] = make_uint4(0, 0, 0, 0);
-                asm volatile("bar.sync 2, 256;" ::: "memory");   // zero row visible
-                const uint32_t arow = uint32_t((r >> 2) * 12 + (r & 3)) * U_PIX_B + kh * 16;
-                for (int u = 0; u < UP_QUARTERS; ++u) {
-                    // the quarter's tail weights (TW[u], filled by the producer)
-                    const int ts = u;
-                    mbar_wait(b_tw_full + 8 * ts, (tw_full_ph >> ts) & 1u);
-                    tw_full_ph ^= 1u << ts;
-                    const uint32_t tw_s = uni_s + TW_OFF0 + ts * 7808;
-                    const uint32_t bstep = n < 3 ? 3 * 32 : 0;
-                    const uint32_t b0 = (n < 3 ? tw_s + uint32_t(n * 32 + kb * 16) : uni_s + ZERO_OFF) + tap_lo * bstep;
-#pragma unroll
-                    for (int t = 0; t < T; ++t) {
-                        const int step = u * T + t, ub = step & 1;
-                        mbar_wait(b_ubuf_full + 8 * ub, (step >> 1) & 1);
-                        tr(13, u, t);
-                        const Win W0 = window_of(P, k0 + t * WPT), W1 = window_of(P, k0 + t * WPT + 1);
-                        const bool v0 = W0.valid && !W0.edge, v1 = W1.valid && !W1.edge;
-                        const uint32_t a0 = uni_s + U_OFF0 + ub * U_TILE_BYTES + arow;
-                        const uint32_t a1 = a0 + 144 * U_PIX_B;
-                        // two independent accumulation chains (the two windows), interleaved
-                        int dy = tap_lo / 9, dx = tap_lo - 9 * dy;
-#pragma unroll 1
-                        for (int j = 0; j < ntap; ++j) {
-                            const uint32_t ao = uint32_t(dy * 12 + dx) * U_PIX_B;
-                            uint32_t fa[4], fb[4], bb[2];
-                            ldsm_x2(b0 + uint32_t(j) * bstep, bb);
-                            if (v0) ldsm_x4(a0 + ao, fa);
-                            if (v1) ldsm_x4(a1 + ao, fb);
-                            if (v0) mma_16816<F16>(tacc[t][0], fa, bb);
-                            if (v1) mma_16816<F16>(tacc[t][1], fb, bb);
-                            if (++dx == 9) { dx = 0; ++dy; }
+                        for (int j = 0; j < 16; ++j) {
+                            const float x = __uint_as_float(v[j]);
+                            y[j] = x > 0.f ? x : ua[j >> 2] * x;
                         }
-                        __syncwarp();
-                        if (lane == 0) mbar_arrive(b_ubuf_free + 8 * ub);
-                        if (t == T - 1 && lane == 0) mbar_arrive(b_tw_empty + 8 * ts);   // quarter's TW consumed
-                        tr(14, u, t);
-                        if (u == UP_QUARTERS - 1) {
-                            const int gq = lane >> 2, tq = lane & 3;
+                        uint8_t *Ub = uni + U_OFF0 + t * U_BUF + (cq >> 1) * U_PLANE + 8 * (cq & 1);
 #pragma unroll
-                            for (int k = 0; k < 2; ++k) {
-                                float *ru = reinterpret_cast<float *>(uni + RED_OFF) + (tw + 8 * k) * 128;
-                                ru[gq * 8 + 2 * tq] = tacc[t][k][0];
-                                ru[gq * 8 + 2 * tq + 1] = tacc[t][k][1];
-                                ru[(gq + 8) * 8 + 2 * tq] = tacc[t][k][2];
-                                ru[(gq + 8) * 8 + 2 * tq + 1] = tacc[t][k][3];
+                        for (int sub = 0; sub < 4; ++sub) {
+                            const int Y = 2 * (py - 1) + (sub >> 1), X = 2 * (px - 1) + (sub & 1);
+                            *reinterpret_cast<uint2 *>(Ub + ((Y * WPT + wt) * 16 + X) * 16) =
+                                make_uint2(pack_op<F16>(y[sub], y[4 + sub]), pack_op<F16>(y[8 + sub], y[12 + sub]));
+                        }
+                        const long long k = k0 + t * WPT + wt;
+                        const Win W = window_of(P, k);
+                        const int pp = (py - 1) * 6 + (px - 1);
+                        if (W.valid && W.edge) {
+                            uint32_t pk[8];
+#pragma unroll
+                            for (int j = 0; j < 8; ++j) pk[j] = pack_op<F16>(y[2 * j], y[2 * j + 1]);
+                            uint4 *dst = reinterpret_cast<uint4 *>(
+                                P.edge_u + (size_t(edge_index(W.wi, W.wj, P.npos)) * 36 + pp) * 256 + 64 * u + cb);
+                            dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                            dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+                        }
+                        if (P.dbg && P.dbg_layer == NL + 1 && W.valid) {
+#pragma unroll
+                            for (int j = 0; j < 16; ++j) {
+                                const int c = UQ * u + 4 * cq + (j >> 2), Y = 2 * (py - 1) + ((j >> 1) & 1),
+                                          X = 2 * (px - 1) + (j & 1);
+                                P.dbg[(k * 144 + Y * 12 + X) * 64 + c] = y[j];
                             }
-                            asm volatile("bar.sync 2, 256;" ::: "memory");
-                            if (et - 256 < 32) {
-                                const int w = (et - 256) >> 4, rr = (et - 256) & 15;
-                                const Win Wn = w ? W1 : W0;
-                                if (Wn.valid && !Wn.edge) {
-                                    const float *rd = reinterpret_cast<const float *>(uni + RED_OFF) + (w * 8) * 128 + rr * 8;
-                                    double m = 0.0;
-#pragma unroll
-                                    for (int o = 0; o < 3; ++o) {
-                                        float pre = tail_b[o];
-#pragma unroll
-                                        for (int d = 0; d < 8; ++d) pre += rd[d * 128 + o];
-                                        m += double(P.tanh_s * tanhf(pre / P.tanh_s));
-                                    }
-                                    m = m / 3.0;
-                                    const int fy = 4 + (rr >> 2), fx = 4 + (rr & 3);
-                                    P.fine[(long long)(2 * Wn.iw + fy) * P.nf + 2 * Wn.jw + fx] =
-                                        denormalize_q(m, P.log_lo, P.span);
-                                }
-                            }
-                            asm volatile("bar.sync 2, 256;" ::: "memory");   // red reusable
                         }
                     }
+                    fence_async_smem();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_leader(b_ubuf_full + 8 * t);
+                    tr(10, u, t);
                 }
             }
+            // ---- stitched pixels: warps of channel quarter cq = t finish tile t.  Lane (quadrant q, lane)
+            // holds Z row (y = 4 + q, window lane / 16, X = lane % 16); the kept pixel X in 4..7 sums
+            // Z[X + dx - 4][3 dx + o] over dx by shuffles, then bias + s tanh(./s), channel mean,
+            // denormalise, straight into the fine grid.  Edge windows are k_tail_edge's. ----
+            if (cq < T) {
+                const int t = cq;
+                mbar_wait(b_zfull + 8 * t, z_ph);
+                tr(13, 0, t);
+                tc_fence_after();
+                uint32_t z0[16], z1[16];
+                TMEM_LD16(tmem + lane_addr + COL_Z + 32 * t, z0);
+                TMEM_LD16(tmem + lane_addr + COL_Z + 32 * t + 16, z1);
+                tmem_wait_ld();
+                const int X = lane & 15;
+                float pre[3] = {tail_b[0], tail_b[1], tail_b[2]};
+#pragma unroll
+                for (int dx = 0; dx < 9; ++dx) {
+                    const int src = (lane & 16) | ((X + dx - 4) & 15);
+#pragma unroll
+                    for (int o = 0; o < 3; ++o) {
+                        const int n = 3 * dx + o;
+                        pre[o] += __shfl_sync(0xffffffffu, __uint_as_float(n < 16 ? z0[n] : z1[n - 16]), src);
+                    }
+                }
+                if (X >= 4 && X < 8) {
+                    const Win W = window_of(P, k0 + t * WPT + (lane >> 4));
+                    if (W.valid && !W.edge) {
+                        double m = 0.0;
+#pragma unroll
+                        for (int o = 0; o < 3; ++o) m += double(P.tanh_s * tanhf(pre[o] / P.tanh_s));
+                        m = m / 3.0;
+                        P.fine[(long long)(2 * W.iw + 4 + q) * P.nf + 2 * W.jw + X] = denormalize_q(m, P.log_lo, P.span);
+                    }
+                }
+                tr(14, 0, t);
+            }
+            z_ph ^= 1u;
+            tc_fence_before();
             tr(15, 0, 0);
             epi_bar();
+            tc_fence_after();
             tr(15, 1, 0);
         }
     }
@@ -1193,19 +1158,23 @@ int tc_pack_weights(mgsr_gen *g, const float *const *t) {
             pack_tap(reinterpret_cast<uint16_t *>(blob.data() + BL.up + (size_t(u) * 9 + tap) * TAP_BYTES),
                      t[ip + 5], 64 * u, tap, -1);
     {
-        // mma.sync tail operand: per quarter u, [tap = dy*9+dx][o][16 shuffled channels 16u..16u+15] bf16
+        // tail B operand: per quarter u and CTA half h, [dy 9][k 2][16 n][8] with n = 16 h + n' = 3 dx + o
+        // (27 of 32 used) and k = shuffled channel 16 u + 8 k + e
         const float *w = t[ip + 7];   // tail.conv.weight 3 x 64 x 9 x 9
-        for (int u = 0; u < UP_QUARTERS; ++u) {
-            uint16_t *dst = reinterpret_cast<uint16_t *>(blob.data() + BL.tail + size_t(u) * 7808);
-            uint16_t *dst16 = reinterpret_cast<uint16_t *>(blob.data() + BL.fmt_stride + BL.tail + size_t(u) * 7808);
-            for (int tap = 0; tap < 81; ++tap)
-                for (int o = 0; o < 3; ++o)
-                    for (int cl = 0; cl < UQ; ++cl) {
-                        const float v = w[((o * 64 + UQ * u + cl) * 9 + tap / 9) * 9 + tap % 9];
-                        dst[(tap * 3 + o) * UQ + cl] = f2bf(v);
-                        dst16[(tap * 3 + o) * UQ + cl] = f2h(v);
-                    }
-        }
+        uint16_t *dst = reinterpret_cast<uint16_t *>(blob.data() + BL.tail);
+        uint16_t *dst16 = reinterpret_cast<uint16_t *>(blob.data() + BL.fmt_stride + BL.tail);
+        for (int u = 0; u < UP_QUARTERS; ++u)
+            for (int h = 0; h < 2; ++h)
+                for (int dy = 0; dy < 9; ++dy)
+                    for (int kc = 0; kc < 2; ++kc)
+                        for (int nl = 0; nl < 16; ++nl)
+                            for (int e = 0; e < 8; ++e) {
+                                const int n = 16 * h + nl, dx = n / 3, o = n % 3, c = UQ * u + 8 * kc + e;
+                                const float v = n < 27 ? w[((o * 64 + c) * 9 + dy) * 9 + dx] : 0.f;
+                                const size_t i = (((size_t(u * 2 + h) * 9 + dy) * 2 + kc) * 16 + nl) * 8 + e;
+                                dst[i] = f2bf(v);
+                                dst16[i] = f2h(v);
+                            }
         float *wf = reinterpret_cast<float *>(blob.data() + BL.tail_f32);
         std::memcpy(wf, w, sizeof(float) * 3 * 64 * 81);
     }
