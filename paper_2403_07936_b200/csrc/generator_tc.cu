@@ -57,56 +57,60 @@ namespace mgsr {
 namespace tc {
 
 constexpr int T = 3;                 // M tiles per group
-constexpr int WPT = 2;               // windows per tile
-constexpr int WPG = T * WPT;         // windows per group
-constexpr int ROWS = 128;            // rows per tile (2 x 8x8 padded windows)
-constexpr int GUARD = 16;            // guard rows around the act planes (tap shifts are within +-9)
-constexpr int PLANE_ROWS = GUARD + T * ROWS + GUARD;
+constexpr int WPG = 8;               // windows per group (per CTA)
+constexpr int ROWS = 128;            // rows per tile
+// Activations: per 8-channel plane, the group's 8 windows as replicate-padded 8x8 images interleaved by
+// image row: plane row GUARD + (py * 8 + w) * 8 + px for padded row py, window w, padded column px.  Tile
+// tau holds rows py = 2 tau + 1 and 2 tau + 2 of all 8 windows (M = 2 x 8 x 8 = 128), so the pad rows
+// py = 0, 7 are stored but never computed: 48 rows per window instead of 64.  Tap (dy, dx) is the
+// descriptor shift dy * 64 + dx rows.  Two buffers (ping-pong: layer L reads buffer L % 2), because a
+// tile's taps read its neighbours' rows.
+constexpr int IMG_ROWS = 8 * WPG * 8;                 // 512
+constexpr int GUARD = 8;                              // tap shifts reach one row past the image
+constexpr int PLANE_ROWS = GUARD + IMG_ROWS + GUARD;  // 528
 constexpr int ACT_PLANE = PLANE_ROWS * 16;            // bytes per 8-channel plane
-constexpr int ACT_BYTES = 8 * ACT_PLANE;              // 55296
+constexpr int ACT_BYTES = 8 * ACT_PLANE;              // 67584 per buffer
 // CTA pair (cta_group::2): the leader CTA issues M = 256 MMAs whose A rows come 128 from each CTA's
 // activations and whose B (N = 64 output channels) is split along N, 32 channels in each CTA's ring.
-constexpr int NSLOT = 20;                             // ring slots (> 9: next layer's first taps prefetch)
+constexpr int NSLOT = 16;                             // ring slots (> 9: next layer's first taps prefetch)
 constexpr int TAP_BYTES = 8192;                       // one 3x3 tap in the blob: [half][32 oc][64 ic] bf16
 constexpr int SLOT_BYTES = 4096;                      // this CTA's half of a tap
-constexpr int RING_BYTES = NSLOT * SLOT_BYTES;        // 81920
-constexpr int UNION_BYTES = 69632;
-constexpr int MISC_BYTES = 8192;                      // q tables (6 x 36 floats) + head im2col index table
+constexpr int RING_BYTES = NSLOT * SLOT_BYTES;        // 65536
+constexpr int MISC_BYTES = 8192;                      // q tables (8 x 36 floats) + head im2col index table
 constexpr int BAR_BYTES = 1024;
-// union, head phase
+// head phase, in activation buffer 1 (free until layer 0's epilogue): im2col, two buffers
 constexpr int HK = 96;                                   // head K (81 taps padded to an f16 K multiple)
 constexpr int HPLANES = HK / 8;                          // 12 planes of 8 fp16
 constexpr int I2C_BYTES = HPLANES * ROWS * 16;           // 24576 per im2col buffer (two buffers)
 constexpr int HB_BYTES = HPLANES * 64 * 16;              // 12288: two halves of 32 oc
 constexpr int HB_HALF = HB_BYTES / 2;                    // 6144, streamed through the ring (2 slots)
-constexpr int IDX_OFF = 1024;                            // in misc: uint8 [64 padded pixels][96 k] -> q index
-static_assert(2 * I2C_BYTES <= UNION_BYTES, "union");
-static_assert(IDX_OFF + 64 * HK <= MISC_BYTES, "misc");
-// up phase (union): per tile, the up-conv quarter pixel-shuffled onto the 12x12 fine window, as the A
-// operand of the tail: 2 planes (8 channels each) x [Y 12][window 2][X 16] pixel rows of 16 B (X 12..15
-// are never written: they only feed discarded rows).  A tail MMA's A rows are (y - 4, window, X) for the
-// kept rows y = 4..7, so the vertical tap dy is a 32-row descriptor shift; the horizontal tap dx and the
-// output o go along N (n = 3 dx + o, 27 of 32).  Tail weights: per quarter, this CTA's 16 N rows,
-// [dy 9][k 2][16 n][8] (the producer streams one slot per quarter).
+constexpr int IDX_OFF = 2048;                            // in misc: uint8 [64 padded pixels][96 k] -> q index
+static_assert(2 * I2C_BYTES <= ACT_BYTES, "im2col");
+static_assert(WPG * 36 * 4 <= IDX_OFF && IDX_OFF + 64 * HK <= MISC_BYTES, "misc");
+// up phase, in activation buffer 0 (free once the post layer's MMAs completed): the up-conv quarter
+// pixel-shuffled onto the 12x12 fine windows, as the tail's A operand: 2 planes (8 channels each) x
+// [Y 12][window 8][X 16] pixel rows of 16 B (X 12..15 never written: they only feed discarded rows).
+// Z tile j holds the kept fine row y = 4 + j of the 8 windows (A rows (window, X)), so the vertical tap dy
+// is a 128-row descriptor shift; the horizontal tap dx and the output o go along N (n = 3 dx + o, 27 of
+// 32).  Tail weights per quarter: this CTA's 16 N rows, [dy 9][k 2][16 n][8].
 constexpr int UQ = 16;
 constexpr int UP_QUARTERS_C = 4;
-constexpr int U_PIX = 12 * WPT * 16;                   // 384 pixel rows per tile
-constexpr int U_PLANE = U_PIX * 16;                    // 6144
-constexpr int U_BUF = 2 * U_PLANE;                     // 12288: one tile's 16 channels
-constexpr int U_OFF0 = 0;                              // T buffers, one per tile
+constexpr int ZT = 4;                                  // Z tiles (kept fine rows)
+constexpr int U_PIX = 12 * WPG * 16;                   // 1536 pixel rows
+constexpr int U_PLANE = U_PIX * 16;                    // 24576
+constexpr int U_BYTES = 2 * U_PLANE;                   // 49152: the quarter's 16 channels
 constexpr int TW_HALF = 9 * 512;                       // 4608: this CTA's half of a quarter's tail weights
 constexpr int TW_QBYTES = 2 * TW_HALF;                 // a quarter in the blob (both halves)
-constexpr int TW_OFF0 = T * U_BUF;                     // 36864
-static_assert(TW_OFF0 + UP_QUARTERS_C * TW_HALF <= UNION_BYTES, "union");
-constexpr int OFF_ACT = 0;
-constexpr int OFF_RING = OFF_ACT + ACT_BYTES;
-constexpr int OFF_UNION = OFF_RING + RING_BYTES;
-constexpr int OFF_MISC = OFF_UNION + UNION_BYTES;
+constexpr int TW_OFF0 = U_BYTES;
+static_assert(TW_OFF0 + UP_QUARTERS_C * TW_HALF <= ACT_BYTES, "up phase");
+constexpr int OFF_ACT = 0;                             // two buffers
+constexpr int OFF_RING = OFF_ACT + 2 * ACT_BYTES;
+constexpr int OFF_MISC = OFF_RING + RING_BYTES;
 constexpr int OFF_BAR = OFF_MISC + MISC_BYTES;
 constexpr int OFF_CONST = OFF_BAR + BAR_BYTES;
 // TMEM columns
 constexpr int COL_ACC = 0, COL_RES = 192, COL_SKIP = 384;
-constexpr int COL_Z = COL_SKIP;   // tail accumulators (32 per tile) reuse the skip columns once the post layer read them
+constexpr int COL_Z = COL_SKIP;   // tail accumulators (32 per Z tile, 4 tiles) reuse the skip columns + the spare 32
 
 constexpr int NEPI = 16;                       // epilogue warps
 constexpr int NTHREADS = 64 + 32 * NEPI;       // 576
@@ -373,62 +377,37 @@ __device__ __forceinline__ double denormalize_q(double q, double log_lo, double 
     return q > 0.0 ? mag : -mag;
 }
 
-// Write one row's 16 channels (bf16, planes kc0, kc0+1) of tile t into the
-// planes at `row`, plus (replicas) its replicate-padding images.
-template <bool REPLICAS>
-__device__ __forceinline__ void store_row(uint8_t *buf, int t, int row, int kc0, const uint32_t (&pk)[8]) {
-    const int w = row >> 6, pix = row & 63, py = pix >> 3, px = pix & 7;
-    if (py < 1 || py > 6 || px < 1 || px > 6) return;
-    const uint4 v0 = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-    const uint4 v1 = make_uint4(pk[4], pk[5], pk[6], pk[7]);
-    if (!REPLICAS) {
-        const int r = GUARD + t * ROWS + row;
-        *reinterpret_cast<uint4 *>(buf + kc0 * ACT_PLANE + r * 16) = v0;
-        *reinterpret_cast<uint4 *>(buf + (kc0 + 1) * ACT_PLANE + r * 16) = v1;
-        return;
-    }
-    const int ty[2] = {py, py == 1 ? 0 : (py == 6 ? 7 : -1)};
-    const int tx[2] = {px, px == 1 ? 0 : (px == 6 ? 7 : -1)};
-#pragma unroll
-    for (int a = 0; a < 2; ++a) {
-#pragma unroll
-        for (int b = 0; b < 2; ++b) {
-            if (ty[a] < 0 || tx[b] < 0) continue;
-            const int r = GUARD + t * ROWS + w * 64 + ty[a] * 8 + tx[b];
-            *reinterpret_cast<uint4 *>(buf + kc0 * ACT_PLANE + r * 16) = v0;
-            *reinterpret_cast<uint4 *>(buf + (kc0 + 1) * ACT_PLANE + r * 16) = v1;
-        }
-    }
-}
-
 template <bool F16>
 __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
     extern __shared__ __align__(128) uint8_t smem[];
-    uint8_t *act = smem + OFF_ACT;
+    uint8_t *act = smem + OFF_ACT;   // two buffers of ACT_BYTES
     uint8_t *ring = smem + OFF_RING;
-    uint8_t *uni = smem + OFF_UNION;
     float *misc = reinterpret_cast<float *>(smem + OFF_MISC);
     float *cs = reinterpret_cast<float *>(smem + OFF_CONST);
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + OFF_BAR);
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + OFF_BAR + BAR_BYTES - 8);
+    uint8_t *i2c = act + ACT_BYTES;   // head phase: im2col in buffer 1
+    uint8_t *ubuf = act;              // up phase: U + tail weights in buffer 0
     // Barriers marked (leader) are waited on by the leader's MMA warp only and collect the arrivals of
     // both CTAs; (both) are signalled in both CTAs by the leader's multicast commits; the rest are local.
     const uint32_t b_full = smem_u32(bars + 0);                     // [NSLOT] this CTA's ring slot landed
     const uint32_t b_empty = smem_u32(bars + NSLOT);                // [NSLOT] (both) slot consumed
     const uint32_t b_peerfull = smem_u32(bars + 2 * NSLOT);         // [NSLOT] (leader) peer's slot landed
     constexpr int BB = 3 * NSLOT;
-    const uint32_t b_i2c_full = smem_u32(bars + BB + 33);           // [2] (leader) im2col buffer built (both CTAs)
-    const uint32_t b_i2c_empty = smem_u32(bars + BB + 35);          // [2] (both) im2col buffer consumed
-    const uint32_t b_acc_full = smem_u32(bars + BB + 2);    // [T] (both) MMA -> epilogue: accumulator ready
-    const uint32_t b_act_ready = smem_u32(bars + BB + 5);   // [T] (leader) epilogues -> MMA: act written
-    const uint32_t b_ubuf_full = smem_u32(bars + BB + 37);  // [T] (leader) drains -> MMA: tile's U written (both CTAs)
-    const uint32_t b_ubuf_free = smem_u32(bars + BB + 40);  // [T] (both) tail MMAs -> drains: tile's U consumed
-    const uint32_t b_zfull = smem_u32(bars + BB + 43);      // [T] (both) last tail MMAs -> epilogue: Z ready
+    const uint32_t b_acc_full = smem_u32(bars + BB + 0);    // [T] (both) MMA -> epilogue: accumulator ready
+    const uint32_t b_act_ready = smem_u32(bars + BB + 3);   // [T] (leader) epilogues -> MMA: tile's rows written
+    const uint32_t b_acc_full2 = smem_u32(bars + BB + 6);   // [T] (both) MMA -> drain: up accumulator buffer 1 ready
+    const uint32_t b_drained = smem_u32(bars + BB + 9);     // [2][T] (leader) drain warps -> MMA: up buffer free
+    const uint32_t b_i2c_full = smem_u32(bars + BB + 15);   // [2] (leader) im2col buffer built (both CTAs)
+    const uint32_t b_i2c_empty = smem_u32(bars + BB + 17);  // [2] (both) im2col buffer consumed
+    const uint32_t b_ubuf_full = smem_u32(bars + BB + 19);  // (leader) drains -> MMA: the quarter's U written
+    const uint32_t b_ubuf_free = smem_u32(bars + BB + 20);  // (both) tail MMAs -> drains: U consumed
+    const uint32_t b_zfull = smem_u32(bars + BB + 21);      // [ZT] (both) last tail MMAs -> epilogue: Z ready
     const uint32_t b_tw_full = smem_u32(bars + BB + 25);    // [4] this CTA's quarter tail weights landed
-    const uint32_t b_tw_peerfull = smem_u32(bars + BB + 46);   // [4] (leader) the peer's landed
-    const uint32_t b_tw_empty = smem_u32(bars + BB + 29);   // [4] (both) tail MMAs of the quarter done
-    const uint32_t b_drained = smem_u32(bars + BB + 16);    // [2][T] (leader) drain warps -> MMA: up buffer free
-    const uint32_t b_acc_full2 = smem_u32(bars + BB + 22);  // [T] (both) MMA -> drain: up accumulator buffer 1 ready
+    const uint32_t b_tw_peerfull = smem_u32(bars + BB + 29);   // [4] (leader) the peer's landed
+    const uint32_t b_tw_empty = smem_u32(bars + BB + 33);   // [4] (both) tail MMAs of the quarter done
+    const uint32_t b_post_done = smem_u32(bars + BB + 37);  // (both) post layer's MMAs done: buffer 0 free
+    static_assert((BB + 38) * 8 <= BAR_BYTES - 8, "barriers");
     const uint32_t rank = cluster_rank();
     const bool leader = rank == 0;
     const int pair = int(blockIdx.x >> 1), npairs = int(gridDim.x >> 1);
@@ -457,13 +436,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
         for (int t = 0; t < T; ++t) {
             mbar_init(b_acc_full + 8 * t, 1);
             mbar_init(b_act_ready + 8 * t, 2 * NEPI);
-            mbar_init(b_ubuf_full + 8 * t, 2 * NEPI);
-            mbar_init(b_ubuf_free + 8 * t, 1);
-            mbar_init(b_zfull + 8 * t, 1);
             mbar_init(b_drained + 8 * t, 2 * NEPI);
             mbar_init(b_acc_full2 + 8 * t, 1);
             mbar_init(b_drained + 8 * (T + t), 2 * NEPI);
         }
+        mbar_init(b_ubuf_full, 2 * NEPI);
+        mbar_init(b_ubuf_free, 1);
+        mbar_init(b_post_done, 1);
+        for (int j = 0; j < ZT; ++j) mbar_init(b_zfull + 8 * j, 1);
         for (int u = 0; u < UP_QUARTERS_C; ++u) {
             mbar_init(b_tw_full + 8 * u, 1);
             mbar_init(b_tw_peerfull + 8 * u, 1);
@@ -486,12 +466,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
         uint32_t ph = 0;   // bit s = fill parity of slot s
         int slot = 0;      // taps stream through the ring in order: slot = global tap index mod NSLOT
         uint32_t tw_ph[UP_QUARTERS_C] = {0, 0, 0, 0};
-        Tracer tr{nullptr, 0};
-        int seq = 0;
+        uint32_t grp_ph = 0;
         auto fill = [&](const uint8_t *src, uint32_t bytes = SLOT_BYTES) {
             mbar_wait(b_empty + 8 * slot, ((ph >> slot) & 1u) ^ 1u);
-            if (lane == 0) tr(1, seq / 10, seq % 10);
-            ++seq;
             if (elect_one()) {
                 mbar_expect_tx(b_full + 8 * slot, bytes);
                 bulk_g2s(smem_u32(ring + slot * SLOT_BYTES), src, bytes, b_full + 8 * slot);
@@ -501,29 +478,27 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
             slot = slot == NSLOT - 1 ? 0 : slot + 1;
         };
         for (int gp = pair; gp < ngp; gp += npairs) {
-            tr.buf = (P.prof && blockIdx.x == 0 && gp == TRACE_GROUP * npairs) ? P.prof : nullptr;
-            seq = 0;
             for (int h = 0; h < 2; ++h)   // this CTA's half of the head weights: planes 0-7, 8-11
                 fill(wblob + BL.head_b + rank * HB_HALF + h * SLOT_BYTES, h < 1 ? SLOT_BYTES : HB_HALF - SLOT_BYTES);
             for (int L = 0; L < NLAYERS; ++L)
                 for (int tap = 0; tap < 9; ++tap)
                     fill(wblob + P.wfmt + BL.body + (size_t(L) * 9 + tap) * TAP_BYTES + rank * SLOT_BYTES);
             for (int u = 0; u < UP_QUARTERS; ++u) {
-                {   // this CTA's half of the quarter's tail weights -> TW[u] (union; free once the last
-                    // group's tail MMAs of quarter u completed)
-                    mbar_wait(b_tw_empty + 8 * u, tw_ph[u] ^ 1u);
-                    tw_ph[u] ^= 1u;
-                    if (elect_one()) {
-                        mbar_expect_tx(b_tw_full + 8 * u, TW_HALF);
-                        bulk_g2s(smem_u32(uni + TW_OFF0 + u * TW_HALF),
-                                 wblob + P.wfmt + BL.tail + size_t(u) * TW_QBYTES + rank * TW_HALF, TW_HALF,
-                                 b_tw_full + 8 * u);
-                    }
-                    __syncwarp();
-                }
                 for (int tap = 0; tap < 9; ++tap)
                     fill(wblob + P.wfmt + BL.up + (size_t(u) * 9 + tap) * TAP_BYTES + rank * SLOT_BYTES);
+                // this CTA's half of the quarter's tail weights -> buffer 0, once the post layer's MMAs
+                // released it and the last group's tail MMAs of quarter u completed
+                if (u == 0) mbar_wait(b_post_done, grp_ph);
+                mbar_wait(b_tw_empty + 8 * u, tw_ph[u] ^ 1u);
+                tw_ph[u] ^= 1u;
+                if (elect_one()) {
+                    mbar_expect_tx(b_tw_full + 8 * u, TW_HALF);
+                    bulk_g2s(smem_u32(ubuf + TW_OFF0 + u * TW_HALF),
+                             wblob + P.wfmt + BL.tail + size_t(u) * TW_QBYTES + rank * TW_HALF, TW_HALF, b_tw_full + 8 * u);
+                }
+                __syncwarp();
             }
+            grp_ph ^= 1u;
         }
     } else if (warp == 1 && !leader) {
         // ================= peer: forward "slot landed" to the leader =================
@@ -541,10 +516,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
         for (int gp = pair; gp < ngp; gp += npairs) {   // same order as the producer's fills
             fwd(2 + NLAYERS * 9);
             for (int u = 0; u < UP_QUARTERS; ++u) {
+                fwd(9);
                 mbar_wait(b_tw_full + 8 * u, twp);
                 if (elect_one()) mbar_arrive_leader(b_tw_peerfull + 8 * u);
                 __syncwarp();
-                fwd(9);
             }
             twp ^= 1u;
         }
@@ -552,23 +527,27 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
         // ================= MMA issuer (leader; warp-uniform control, one elected lane issues) =================
         uint32_t ph = 0, i2c_ph = 0;   // i2c_ph bit b: parity of the next completion of b_i2c_full[b]
         int slot0 = 0;   // ring slot of tap 0 of the current layer
-        uint32_t ar_ph[T] = {0, 0, 0};
+        uint32_t ar_ph = 0;   // bit t: parity of the next completion of b_act_ready[t]
         uint32_t dr_ph = 0;   // bit t: parity of the next completion of b_drained[0][t]
-        const uint32_t act_base = smem_u32(act), uni_base = smem_u32(uni), ring_base = smem_u32(ring);
-        const uint32_t i2c_base = uni_base;
+        const uint32_t act_base = smem_u32(act), ring_base = smem_u32(ring);
+        const uint32_t i2c_base = smem_u32(i2c), u_base = smem_u32(ubuf);
         const uint32_t id64 = F16 ? idesc_f16(64) : idesc_bf16(64);
-        const uint64_t a_desc0 = make_desc(act_base, ACT_PLANE, 128);
         const uint64_t b_desc0 = make_desc(ring_base, 512, 128);         // half tap: 32-row planes
         Tracer tr{nullptr, 0};
-        // one N = 64 3x3 layer over the three tiles (body, post, up quarter)
-        // wait: 0 = act_ready (activations of this tile written), 1 = none, 2/3 = up accumulator
-        // buffer 0/1 of this tile drained
-        auto conv_layer = [&](int lid, int wait, uint32_t dcol) {
+        auto wait_ar = [&](int t) {
+            mbar_wait(b_act_ready + 8 * t, (ar_ph >> t) & 1u);
+            ar_ph ^= 1u << t;
+        };
+        // one N = 64 3x3 layer over the three tiles (body, post, up quarter), reading buffer `buf`
+        // wait: 0 = act_ready (the rows this tile's taps read are written: tiles t - 1..t + 1), 1 = none,
+        // 2/3 = up accumulator buffer 0/1 of this tile drained
+        auto conv_layer = [&](int lid, int buf, int wait, uint32_t dcol) {
+            const uint64_t a_desc0 = make_desc(act_base + buf * ACT_BYTES, ACT_PLANE, 128);
 #pragma unroll
             for (int t = 0; t < T; ++t) {
                 if (wait == 0) {
-                    mbar_wait(b_act_ready + 8 * t, ar_ph[t]);
-                    ar_ph[t] ^= 1;
+                    if (t == 0) { wait_ar(0); wait_ar(1); }
+                    else if (t == 1) wait_ar(2);
                 } else if (wait == 2) {   // buffer 0: waited at every completion (u = 2 here, head next group)
                     mbar_wait(b_drained + 8 * t, (dr_ph >> t) & 1u);
                     dr_ph ^= 1u << t;
@@ -577,7 +556,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
                 }
                 if (lane == 0) tr(2, lid, t);
                 tc_fence_after();
-                const uint64_t a_t = a_desc0 + uint64_t(GUARD + t * ROWS);
+                const uint64_t a_t = a_desc0 + uint64_t(GUARD + (2 * t + 1) * 64);
                 const uint32_t d = tmem + dcol + 64 * t;
                 if (elect_one()) {
 #pragma unroll
@@ -590,7 +569,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
                             if (tap == 0) tr(4, lid, 0);
                             tc_fence_after();
                         }
-                        const int shift = (tap / 3 - 1) * 8 + (tap % 3 - 1);
+                        const int shift = (tap / 3 - 1) * 64 + (tap % 3 - 1);
                         const uint64_t a = a_t + uint64_t(int64_t(shift));
                         const uint64_t b = b_desc0 + uint64_t(s * (SLOT_BYTES / 16));
 #pragma unroll
@@ -602,6 +581,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
                     // separate completion barriers per up buffer: a tile's two buffers may complete
                     // back to back, which a single barrier could not tell apart
                     umma_commit((dcol == COL_RES ? b_acc_full2 : b_acc_full) + 8 * t);
+                    if (lid == NLAYERS && t == T - 1) umma_commit(b_post_done);   // buffer 0 no longer read
                 }
                 __syncwarp();
                 if (lane == 0) tr(3, lid, t);
@@ -615,32 +595,32 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
             slot0 += 9;
             slot0 = slot0 >= NSLOT ? slot0 - NSLOT : slot0;
         };
-        // pruned 9x9 tail, quarter u: Z[t] (M = 256 kept-row pixels, N = 32 = 3 dx + o) += sum over dy of
-        // U[t] shifted by dy rows x TW[u][dy]; 9 MMAs per tile
+        // pruned 9x9 tail, quarter u: Z[j] (M = 256 pixels of kept fine row 4 + j, N = 32 = 3 dx + o) +=
+        // sum over dy of U shifted by j + dy fine rows x TW[u][dy]; 36 MMAs
         const uint32_t idz = F16 ? idesc_f16(32) : idesc_bf16(32);
         uint32_t grp_ph = 0;   // parity of this pair's group iteration (one TW / Z completion per group)
         auto tail_mma = [&](int u) {
             mbar_wait(b_tw_full + 8 * u, grp_ph);
             mbar_wait(b_tw_peerfull + 8 * u, grp_ph);
+            mbar_wait(b_ubuf_full, uint32_t(u & 1));
+            if (lane == 0) tr(16, u, 0);
+            tc_fence_after();
+            if (elect_one()) {
 #pragma unroll 1
-            for (int t = 0; t < T; ++t) {
-                mbar_wait(b_ubuf_full + 8 * t, uint32_t(u & 1));
-                if (lane == 0) tr(16, u, t);
-                tc_fence_after();
-                if (elect_one()) {
-                    const uint32_t d = tmem + COL_Z + 32 * t;
+                for (int j = 0; j < ZT; ++j) {
+                    const uint32_t d = tmem + COL_Z + 32 * j;
 #pragma unroll
                     for (int dy = 0; dy < 9; ++dy) {
-                        const uint64_t a = make_desc(uni_base + U_OFF0 + t * U_BUF + dy * (32 * 16), U_PLANE, 128);
-                        const uint64_t b = make_desc(uni_base + TW_OFF0 + u * TW_HALF + dy * 512, 256, 128);
+                        const uint64_t a = make_desc(u_base + (j + dy) * (WPG * 16 * 16), U_PLANE, 128);
+                        const uint64_t b = make_desc(u_base + TW_OFF0 + u * TW_HALF + dy * 512, 256, 128);
                         mma_bf16(d, a, b, idz, (u | dy) > 0);
                     }
-                    umma_commit(b_ubuf_free + 8 * t);
-                    if (u == UP_QUARTERS - 1) umma_commit(b_zfull + 8 * t);
-                    if (t == T - 1) umma_commit(b_tw_empty + 8 * u);
+                    if (u == UP_QUARTERS - 1) umma_commit(b_zfull + 8 * j);
                 }
-                __syncwarp();
+                umma_commit(b_ubuf_free);
+                umma_commit(b_tw_empty + 8 * u);
             }
+            __syncwarp();
         };
         for (int gp = pair; gp < ngp; gp += npairs) {
             tr.buf = (P.prof && blockIdx.x == 0 && gp == TRACE_GROUP * npairs) ? P.prof + 4096 : nullptr;
@@ -686,16 +666,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
             slot0 += 2;
             slot0 = slot0 >= NSLOT ? slot0 - NSLOT : slot0;
 #pragma unroll 1
-            for (int L = 0; L < NLAYERS; ++L) conv_layer(L + 1, 0, COL_ACC);
-            // up quarters, accumulators double-buffered over cols [0, 192) and [192, 384) (the residual
-            // stream and skip are dead after the post layer): quarter u + 1 runs while u drains
-            // the tail of quarter u issues after up quarter u + 1, once quarter u is drained into U
-            conv_layer(40, 0, COL_ACC);
-            conv_layer(41, 1, COL_RES);
+            for (int L = 0; L < NLAYERS; ++L) conv_layer(L + 1, L & 1, 0, COL_ACC);
+            // up quarters (reading buffer NL & 1 = 1), accumulators double-buffered over cols [0, 192) and
+            // [192, 384) (the residual stream and skip are dead after the post layer): quarter u + 1 runs
+            // while u drains; the tail of quarter u issues after up quarter u + 1, once u is drained into U
+            conv_layer(40, 1, 0, COL_ACC);
+            conv_layer(41, 1, 1, COL_RES);
             tail_mma(0);
-            conv_layer(42, 2, COL_ACC);
+            conv_layer(42, 1, 2, COL_ACC);
             tail_mma(1);
-            conv_layer(43, 3, COL_RES);
+            conv_layer(43, 1, 3, COL_RES);
             tail_mma(2);
             tail_mma(3);
             grp_ph ^= 1u;
@@ -708,10 +688,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
         const int cb = 16 * cq;                // first channel of this thread
         const int et = threadIdx.x - 64;       // 0..511
         const int row = 32 * q + lane;         // row within a tile
-        const int wt = row >> 6, pix = row & 63, py = pix >> 3, px = pix & 7;
-        const bool interior = py >= 1 && py <= 6 && px >= 1 && px <= 6;
-        // lane holding the interior pixel this row replicates (itself when interior); always the same warp
-        const int pad_src = (min(max(py, 1), 6) * 8 + min(max(px, 1), 6)) - 32 * (q & 1);
+        const int pyl = row >> 6, wrow = (row >> 3) & 7, px = row & 7;   // tile row = (py - 2 t - 1, window, px)
+        const bool interior = px >= 1 && px <= 6;
+        // lane holding the interior pixel this pad column replicates (itself when interior): same warp
+        const int pad_src = lane + (px == 0 ? 1 : (px == 7 ? -1 : 0));
         const uint32_t lane_addr = uint32_t(32 * q) << 16;
         uint32_t af_ph[T] = {0, 0, 0};
         int i2c_uses[2] = {0, 0};   // builds into im2col buffer b so far
@@ -740,7 +720,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
             tr.buf = (P.prof && blockIdx.x == 0 && gp == TRACE_GROUP * npairs && lane == 0 &&
                       (warp == 2 || warp == 10)) ? P.prof + (warp == 2 ? 2 : 3) * 4096 : nullptr;
             tr(11, 0, 0);
-            // ---- q tables of the 6 windows (fp64 normalise -> fp32) ----
+            // ---- q tables of the 8 windows (fp64 normalise -> fp32) ----
             if (et < WPG * 36) {
                 const int wk = et / 36, pp = et % 36;
                 const Win W = window_of(P, k0 + wk);
@@ -755,8 +735,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
                 ++i2c_uses[ib];
                 {
                     const int r = et & 127, part4 = et >> 7;
-                    const int rw = r >> 6, rp = r & 63;
-                    const float *qt = misc + (t * WPT + rw) * 36;
+                    const int rp = (2 * t + 1 + (r >> 6)) * 8 + (r & 7);   // padded pixel (py, px)
+                    const float *qt = misc + ((r >> 3) & 7) * 36;
                     const uint2 *ix = reinterpret_cast<const uint2 *>(idx_tab + rp * HK);
 #pragma unroll
                     for (int kk = 0; kk < HPLANES / 4; ++kk) {
@@ -769,7 +749,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
                             const uint32_t id0 = (src >> (16 * (e & 1))) & 0xFFu, id1 = (src >> (16 * (e & 1) + 8)) & 0xFFu;
                             w[e] = pack_op<true>(id0 < 36 ? qt[id0] : 0.f, id1 < 36 ? qt[id1] : 0.f);
                         }
-                        *reinterpret_cast<uint4 *>(uni + ib * I2C_BYTES + kc * (ROWS * 16) + r * 16) =
+                        *reinterpret_cast<uint4 *>(i2c + ib * I2C_BYTES + kc * (ROWS * 16) + r * 16) =
                             make_uint4(w[0], w[1], w[2], w[3]);
                     }
                 }
@@ -778,8 +758,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
                 if (et == 0) mbar_arrive_leader(b_i2c_full + 8 * ib);
                 tr(12, 0, t);
             }
-            // ---- head + body + post epilogues ----
+            // ---- head + body + post epilogues: layer L (head = -1) writes buffer (L + 1) & 1 ----
             for (int L = -1; L < NL; ++L) {
+                uint8_t *obuf = act + ((L + 1) & 1) * ACT_BYTES;
                 for (int t = 0; t < T; ++t) {
                     mbar_wait(b_acc_full + 8 * t, af_ph[t]);
                     tr(6, L + 1, t);
@@ -845,20 +826,26 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
                     uint32_t pk[8];
 #pragma unroll
                     for (int j = 0; j < 8; ++j) pk[j] = pack_op<F16>(y[2 * j], y[2 * j + 1]);
-                    {   // replicate padding without partial stores: a ring row takes the packed values of its
-                        // clamped interior source row (same warp) by shuffle, then every lane writes its own
-                        // row -- two full-warp contiguous 16-byte stores per tile-layer
+                    {   // replicate padding without partial stores: a pad column takes the packed values of its
+                        // interior neighbour (lane +-1) by shuffle, then every lane writes its own row; the first
+                        // and last image rows (tiles 0 and 2) also write the pad rows py = 0 and 7
                         uint32_t sv[8];
 #pragma unroll
                         for (int j = 0; j < 8; ++j) sv[j] = __shfl_sync(0xffffffffu, pk[j], pad_src);
-                        uint8_t *dst = act + (2 * cq) * ACT_PLANE + (GUARD + t * ROWS + row) * 16;
-                        *reinterpret_cast<uint4 *>(dst) = make_uint4(sv[0], sv[1], sv[2], sv[3]);
-                        *reinterpret_cast<uint4 *>(dst + ACT_PLANE) = make_uint4(sv[4], sv[5], sv[6], sv[7]);
+                        uint8_t *dst = obuf + (2 * cq) * ACT_PLANE + (GUARD + (2 * t + 1) * 64 + row) * 16;
+                        const uint4 v0 = make_uint4(sv[0], sv[1], sv[2], sv[3]), v1 = make_uint4(sv[4], sv[5], sv[6], sv[7]);
+                        *reinterpret_cast<uint4 *>(dst) = v0;
+                        *reinterpret_cast<uint4 *>(dst + ACT_PLANE) = v1;
+                        if ((t == 0 && pyl == 0) || (t == T - 1 && pyl == 1)) {
+                            uint8_t *dp = dst + (t == 0 ? -64 : 64) * 16;
+                            *reinterpret_cast<uint4 *>(dp) = v0;
+                            *reinterpret_cast<uint4 *>(dp + ACT_PLANE) = v1;
+                        }
                     }
                     if (P.dbg && P.dbg_layer == L + 1 && interior) {
-                        const long long k = k0 + t * WPT + wt;
+                        const long long k = k0 + wrow;
                         if (k < P.nwin) {
-                            const int pp = (py - 1) * 6 + (px - 1);
+                            const int pp = (2 * t + pyl) * 6 + (px - 1);
 #pragma unroll
                             for (int j = 0; j < 16; ++j) P.dbg[(k * 36 + pp) * 64 + cb + j] = y[j];
                         }
@@ -871,9 +858,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
                 }
             }
             // ---- up quarters: every epilogue warp drains 16 columns (4 shuffled channels x 4 sub-pixels) of
-            // its lane quadrant: PReLU, then the quarter goes pixel-shuffled into U[t], the A operand of the
-            // tail MMAs (edge windows also spill it for k_tail_edge).  U[t] is rewritten for quarter u once
-            // the tail MMAs of quarter u - 1 released it. ----
+            // its lane quadrant: PReLU, then the quarter goes pixel-shuffled into U, the A operand of the
+            // tail MMAs (edge windows also spill it for k_tail_edge).  U is rewritten for quarter u once the
+            // tail MMAs of quarter u - 1 released it. ----
             for (int u = 0; u < UP_QUARTERS; ++u) {
                 float ua[4];
 #pragma unroll
@@ -895,24 +882,25 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive_leader(b_drained + 8 * ((u & 1) * T + t));
-                    if (u > 0) mbar_wait(b_ubuf_free + 8 * t, uint32_t(u - 1) & 1u);
+                    if (u > 0 && t == 0) mbar_wait(b_ubuf_free, uint32_t(u - 1) & 1u);
                     tr(9, u, t);
                     if (interior) {
                         // column 16 cq + j -> shuffled channel 16 u + 4 cq + j / 4, sub-pixel ((j >> 1) & 1, j & 1)
+                        const int py = 2 * t + 1 + pyl;
                         float y[16];
 #pragma unroll
                         for (int j = 0; j < 16; ++j) {
                             const float x = __uint_as_float(v[j]);
                             y[j] = x > 0.f ? x : ua[j >> 2] * x;
                         }
-                        uint8_t *Ub = uni + U_OFF0 + t * U_BUF + (cq >> 1) * U_PLANE + 8 * (cq & 1);
+                        uint8_t *Ub = ubuf + (cq >> 1) * U_PLANE + 8 * (cq & 1);
 #pragma unroll
                         for (int sub = 0; sub < 4; ++sub) {
                             const int Y = 2 * (py - 1) + (sub >> 1), X = 2 * (px - 1) + (sub & 1);
-                            *reinterpret_cast<uint2 *>(Ub + ((Y * WPT + wt) * 16 + X) * 16) =
+                            *reinterpret_cast<uint2 *>(Ub + ((Y * WPG + wrow) * 16 + X) * 16) =
                                 make_uint2(pack_op<F16>(y[sub], y[4 + sub]), pack_op<F16>(y[8 + sub], y[12 + sub]));
                         }
-                        const long long k = k0 + t * WPT + wt;
+                        const long long k = k0 + wrow;
                         const Win W = window_of(P, k);
                         const int pp = (py - 1) * 6 + (px - 1);
                         if (W.valid && W.edge) {
@@ -933,24 +921,24 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
                             }
                         }
                     }
-                    fence_async_smem();
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive_leader(b_ubuf_full + 8 * t);
                     tr(10, u, t);
                 }
+                fence_async_smem();
+                __syncwarp();
+                if (lane == 0) mbar_arrive_leader(b_ubuf_full);
             }
-            // ---- stitched pixels: warps of channel quarter cq = t finish tile t.  Lane (quadrant q, lane)
-            // holds Z row (y = 4 + q, window lane / 16, X = lane % 16); the kept pixel X in 4..7 sums
-            // Z[X + dx - 4][3 dx + o] over dx by shuffles, then bias + s tanh(./s), channel mean,
-            // denormalise, straight into the fine grid.  Edge windows are k_tail_edge's. ----
-            if (cq < T) {
-                const int t = cq;
-                mbar_wait(b_zfull + 8 * t, z_ph);
-                tr(13, 0, t);
+            // ---- stitched pixels: warps of channel quarter cq = j finish Z tile j (kept fine row y = 4 + j).
+            // Lane (quadrant q, lane) holds Z row (window 2 q + lane / 16, X = lane % 16); the kept pixel X
+            // in 4..7 sums Z[X + dx - 4][3 dx + o] over dx by shuffles, then bias + s tanh(./s), channel
+            // mean, denormalise, straight into the fine grid.  Edge windows are k_tail_edge's. ----
+            {
+                const int j = cq;
+                mbar_wait(b_zfull + 8 * j, z_ph);
+                tr(13, 0, j);
                 tc_fence_after();
                 uint32_t z0[16], z1[16];
-                TMEM_LD16(tmem + lane_addr + COL_Z + 32 * t, z0);
-                TMEM_LD16(tmem + lane_addr + COL_Z + 32 * t + 16, z1);
+                TMEM_LD16(tmem + lane_addr + COL_Z + 32 * j, z0);
+                TMEM_LD16(tmem + lane_addr + COL_Z + 32 * j + 16, z1);
                 tmem_wait_ld();
                 const int X = lane & 15;
                 float pre[3] = {tail_b[0], tail_b[1], tail_b[2]};
@@ -964,16 +952,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
                     }
                 }
                 if (X >= 4 && X < 8) {
-                    const Win W = window_of(P, k0 + t * WPT + (lane >> 4));
+                    const Win W = window_of(P, k0 + 2 * q + (lane >> 4));
                     if (W.valid && !W.edge) {
                         double m = 0.0;
 #pragma unroll
                         for (int o = 0; o < 3; ++o) m += double(P.tanh_s * tanhf(pre[o] / P.tanh_s));
                         m = m / 3.0;
-                        P.fine[(long long)(2 * W.iw + 4 + q) * P.nf + 2 * W.jw + X] = denormalize_q(m, P.log_lo, P.span);
+                        P.fine[(long long)(2 * W.iw + 4 + j) * P.nf + 2 * W.jw + X] = denormalize_q(m, P.log_lo, P.span);
                     }
                 }
-                tr(14, 0, t);
+                tr(14, 0, j);
             }
             z_ph ^= 1u;
             tc_fence_before();
