@@ -4,9 +4,12 @@
 // solve-loop logging pass.  Compiled with --fmad=false so every product and
 // sum rounds exactly as the reference's -ffp-contract=off C loops
 // (pkg/setup.py:37-39).
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <string>
 
 #include "common.cuh"
@@ -394,6 +397,243 @@ __global__ void __launch_bounds__(kTbThreads, 3) k_gs_tb(const double *__restric
 }
 
 // ---------------------------------------------------------------------------
+// Register-blocked, TMA-fed K-sweep GS (the large levels).  Same arithmetic and
+// outputs as k_gs_tb; different data movement:
+//   * a 64 x 64 window (tile interior + an even halo HE >= 2K (+1 with RC)) of
+//     p and f lands in shared memory by per-row cp.async.bulk copies (rows and
+//     the column wrap of edge tiles split into <= 2 segments per row), tracked
+//     by one mbarrier; as soon as the threads copied the window into registers,
+//     the NEXT tile's window is requested, so HBM streams while this tile
+//     relaxes (two CTAs per SM, each one tile ahead);
+//   * thread (warp w, lane l) holds rows 8w..8w+7, columns 2l, 2l+1 of the
+//     window in registers.  A half-sweep updates one cell per row (the colour
+//     parity of a row is a compile-time constant because the window origin is
+//     even): left/right neighbours come from the thread itself or lane l -+ 1
+//     by shuffle, up/down from its own rows, and across warps from the rows
+//     every warp publishes in shared memory after each half-sweep (one
+//     barrier per half-sweep, double-buffered);
+//   * interior written with 16-byte stores; tiles of the last row/column are
+//     shifted inwards (x0 = n - TX) rather than masked: they recompute cells
+//     of their neighbour bit for bit and only count their own cells in the sums.
+constexpr int kRbW = 64, kRbRows = 8, kRbWarps = 8, kRbThreads = 32 * kRbWarps, kRbMinN = 128;
+
+__device__ __forceinline__ void rb_mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 10000000;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void rb_bulk(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+
+__device__ __forceinline__ void rb_tma2d(uint32_t dst, const CUtensorMap *tm, int x, int y, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(bar)
+        : "memory");
+}
+
+// The window of one tile -> shared memory; the barrier was armed with the byte count.  Windows inside the
+// grid: one 2-D tensor copy per array (thread 0).  Windows that wrap (periodic edge tiles): per-row bulk
+// copies, rows w * 8 .. w * 8 + 7 issued by lanes 0..7 of warp w, each row in one or two column segments.
+__device__ __forceinline__ void rb_issue(const CUtensorMap *tm_p, const CUtensorMap *tm_f, const double *pin,
+                                         const double *f, int n, int X0, int Y0, bool load_p, uint32_t sp,
+                                         uint32_t sf, uint32_t bar, int w, int lane) {
+    if (X0 >= 0 && Y0 >= 0 && X0 + kRbW <= n && Y0 + kRbW <= n) {
+        if (w == 0 && lane == 0) {
+            rb_tma2d(sf, tm_f, X0, Y0, bar);
+            if (load_p) rb_tma2d(sp, tm_p, X0, Y0, bar);
+        }
+        return;
+    }
+    if (lane >= kRbRows) return;
+    const int r = w * kRbRows + lane;
+    int gy = Y0 + r;
+    gy = gy < 0 ? gy + n : (gy >= n ? gy - n : gy);
+    const int64_t row = int64_t(gy) * n;
+    const uint32_t so = uint32_t(r * kRbW * 8);
+    // column segments [X0, X0 + 64) mod n: one or two contiguous pieces (all even -> 16-byte aligned)
+    int a0 = X0, len0 = kRbW, len1 = 0;
+    if (X0 < 0) { a0 = X0 + n; len0 = -X0; len1 = kRbW + X0; }
+    else if (X0 + kRbW > n) { len0 = n - X0; len1 = kRbW - len0; }
+    rb_bulk(sf + so, f + row + a0, uint32_t(len0 * 8), bar);
+    if (len1) rb_bulk(sf + so + uint32_t(len0 * 8), f + row, uint32_t(len1 * 8), bar);
+    if (load_p) {
+        rb_bulk(sp + so, pin + row + a0, uint32_t(len0 * 8), bar);
+        if (len1) rb_bulk(sp + so + uint32_t(len0 * 8), pin + row, uint32_t(len1 * 8), bar);
+    }
+}
+
+template <int K, bool RC>
+__global__ void __launch_bounds__(kRbThreads, 2)
+    k_gs_rb(const __grid_constant__ CUtensorMap tm_p, const __grid_constant__ CUtensorMap tm_f,
+            const double *__restrict__ pin, double *__restrict__ pout, FSrc fs, int n, double h2, int zero_init,
+            double inv_h2, double *__restrict__ rc, RedSlot slot, double *mean_out, double *rc_mean_out) {
+    constexpr int H = 2 * K + (RC ? 1 : 0);
+    constexpr int HE = (H + 1) & ~1;            // even: 16-byte aligned rows, fixed colour parity per row
+    constexpr int TX = kRbW - 2 * HE, TY = kRbW - 2 * HE;
+    constexpr int R = kRbRows;
+    extern __shared__ __align__(128) double sm[];
+    double *const sp = sm;                        // [64][64] p window
+    double *const sf = sm + kRbW * kRbW;          // [64][64] f window
+    double2 *const xb = reinterpret_cast<double2 *>(sm + 2 * kRbW * kRbW);   // [2][warps][2][32] published rows
+    __shared__ __align__(8) uint64_t bar_storage;
+    const uint32_t bar = uint32_t(__cvta_generic_to_shared(&bar_storage));
+    const uint32_t sp_a = uint32_t(__cvta_generic_to_shared(sp)), sf_a = uint32_t(__cvta_generic_to_shared(sf));
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const double sh = fs.load_shift();
+    const bool shifted = fs.shift != nullptr;
+    const int tiles_x = (n + TX - 1) / TX, tiles_y = (n + TY - 1) / TY, ntiles = tiles_x * tiles_y;
+    const bool load_p = !zero_init;
+    const uint32_t tx_bytes = uint32_t(kRbW * kRbW * 8) * (load_p ? 2u : 1u);
+    auto origin = [&](int tile, int &x0, int &y0, int &xs, int &ys) {
+        const int by = tile / tiles_x, bx = tile - by * tiles_x;
+        xs = bx * TX;
+        ys = by * TY;
+        x0 = min(xs, n - TX);
+        y0 = min(ys, n - TY);
+    };
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (tid == 0 && int(blockIdx.x) < ntiles)
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(tx_bytes) : "memory");
+    __syncthreads();
+    if (int(blockIdx.x) < ntiles) {
+        int x0, y0, xs, ys;
+        origin(blockIdx.x, x0, y0, xs, ys);
+        rb_issue(&tm_p, &tm_f, pin, fs.f, n, x0 - HE, y0 - HE, load_p, sp_a, sf_a, bar, w, lane);
+    }
+    double v[2] = {0.0, 0.0};
+    uint32_t phase = 0;
+#pragma unroll 1
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        int x0, y0, xs, ys;
+        origin(tile, x0, y0, xs, ys);
+        double p[R][2], f[R][2], hu[2], hd[2];
+        rb_mbar_wait(bar, phase);
+        phase ^= 1u;
+        {
+            const int c2 = 2 * lane;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const int o = (w * R + r) * kRbW + c2;
+                const double2 ff = *reinterpret_cast<const double2 *>(sf + o);
+                f[r][0] = shifted ? (ff.x - sh) * fs.scale : ff.x;
+                f[r][1] = shifted ? (ff.y - sh) * fs.scale : ff.y;
+                if (load_p) {
+                    const double2 pp = *reinterpret_cast<const double2 *>(sp + o);
+                    p[r][0] = pp.x;
+                    p[r][1] = pp.y;
+                } else {
+                    p[r][0] = 0.0;
+                    p[r][1] = 0.0;
+                }
+            }
+            hu[0] = hu[1] = hd[0] = hd[1] = 0.0;
+            if (load_p) {
+                if (w > 0) {
+                    const double2 t = *reinterpret_cast<const double2 *>(sp + (w * R - 1) * kRbW + c2);
+                    hu[0] = t.x;
+                    hu[1] = t.y;
+                }
+                if (w < kRbWarps - 1) {
+                    const double2 t = *reinterpret_cast<const double2 *>(sp + (w * R + R) * kRbW + c2);
+                    hd[0] = t.x;
+                    hd[1] = t.y;
+                }
+            }
+        }
+        const bool more = tile + int(gridDim.x) < ntiles;
+        // arm the next phase before the barrier: every thread has passed this phase's wait by then, and
+        // no copy of the next window can complete before it is issued below
+        if (tid == 0 && more)
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(tx_bytes) : "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();   // window consumed: the next tile's copies may overwrite it
+        if (more) {
+            int nx0, ny0, nxs, nys;
+            origin(tile + gridDim.x, nx0, ny0, nxs, nys);
+            rb_issue(&tm_p, &tm_f, pin, fs.f, n, nx0 - HE, ny0 - HE, load_p, sp_a, sf_a, bar, w, lane);
+        }
+        // 2K half-sweeps; red (global (i + j) even) first.  The window origin (x0 - HE, y0 - HE) is even,
+        // so in window row r (even w * R) the colour-c cell of a thread's pair is element (c + r) & 1.
+#pragma unroll
+        for (int hs = 0; hs < 2 * K; ++hs) {
+            const int c = hs & 1;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const int e = (c + r) & 1;
+                const double up = r > 0 ? p[r - 1][e] : hu[e];
+                const double dn = r < R - 1 ? p[r + 1][e] : hd[e];
+                double left, right;
+                if (e == 0) {
+                    left = __shfl_up_sync(0xffffffffu, p[r][1], 1);
+                    right = p[r][1];
+                } else {
+                    left = p[r][0];
+                    right = __shfl_down_sync(0xffffffffu, p[r][0], 1);
+                }
+                const double nb = ((up + dn) + left) + right;
+                p[r][e] = (nb - h2 * f[r][e]) * 0.25;
+            }
+            if (hs < 2 * K - 1 || RC) {   // publish the boundary rows for the next half-sweep (or the residual)
+                double2 *xo = xb + (hs & 1) * (kRbWarps * 64);
+                xo[(w * 2 + 0) * 32 + lane] = make_double2(p[0][0], p[0][1]);
+                xo[(w * 2 + 1) * 32 + lane] = make_double2(p[R - 1][0], p[R - 1][1]);
+                __syncthreads();
+                if (w > 0) {
+                    const double2 t = xo[((w - 1) * 2 + 1) * 32 + lane];
+                    hu[0] = t.x;
+                    hu[1] = t.y;
+                }
+                if (w < kRbWarps - 1) {
+                    const double2 t = xo[((w + 1) * 2 + 0) * 32 + lane];
+                    hd[0] = t.x;
+                    hd[1] = t.y;
+                }
+            }
+        }
+        // interior: window rows [HE, HE + TY), columns [HE, HE + TX)
+        const bool col_in = 2 * lane >= HE && 2 * lane < HE + TX;
+        const int gj = x0 + 2 * lane - HE;
+        const bool col_own = col_in && gj >= xs;   // cells this tile counts (shifted edge tiles overlap)
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int lr = w * R + r;
+            const bool row_in = lr >= HE && lr < HE + TY;
+            const int gi = y0 + lr - HE;
+            if (row_in && col_in) {
+                *reinterpret_cast<double2 *>(pout + int64_t(gi) * n + gj) = make_double2(p[r][0], p[r][1]);
+                if (col_own && gi >= ys) v[0] += p[r][0] + p[r][1];
+            }
+            if (RC && !(r & 1)) {
+                // (even, even) cell = element 0 of an even row: colour 0; neighbours are the final black values
+                const double left = __shfl_up_sync(0xffffffffu, p[r][1], 1);
+                const double up = r > 0 ? p[r - 1][0] : hu[0];
+                const double dn = p[r + 1][0];
+                if (row_in && col_in) {
+                    const double nb = ((up + dn) + left) + p[r][1];
+                    const double res = f[r][0] - ((nb - 4.0 * p[r][0]) * inv_h2);
+                    rc[int64_t(gi >> 1) * (n >> 1) + (gj >> 1)] = res;
+                    if (col_own && gi >= ys) v[1] += res;
+                }
+            }
+        }
+    }
+    double *const outs[2] = {mean_out, RC ? rc_mean_out : nullptr};
+    const double scales[2] = {1.0 / (double(n) * double(n)), 4.0 / (double(n) * double(n))};
+    grid_reduce_to<2>(v, slot, outs, scales);
+}
+
+// ---------------------------------------------------------------------------
 // Residual / restriction.  Reference: smoother.py:52-57 (r = f - L p, minus
 // mean) and transfer.py:27-39 (coarse = fine[::s, ::s] minus mean).  Inside
 // the V-cycle only the injected points are needed; dropping the fine-grid mean
@@ -678,6 +918,32 @@ int grid_for(int64_t work, int threads) {
     return int(b);
 }
 
+// 2-D tensor map over an n x n fp64 row-major grid, 64 x 64 boxes, no swizzle (k_gs_rb windows)
+static int make_tmap_2d(CUtensorMap *tm, const double *base, int n) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        cudaDriverEntryPointQueryResult q;
+        void *fn = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn) {
+            set_error("cuTensorMapEncodeTiled unavailable");
+            return 1;
+        }
+        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    const cuuint64_t dims[2] = {cuuint64_t(n), cuuint64_t(n)};
+    const cuuint64_t strides[1] = {cuuint64_t(n) * sizeof(double)};
+    const cuuint32_t box[2] = {cuuint32_t(kRbW), cuuint32_t(kRbW)};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = encode(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(base), dims, strides, box,
+                              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        set_error("cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
+        return 1;
+    }
+    return 0;
+}
+
 int launch_gs(const double *p_in, double *p_out, double *tmp, FSrc fs, int n, double h2, int sweeps,
               int zero_init, double *rc, double *rc_mean, double *mean_out, void *red_ws, cudaStream_t st) {
     // red_ws: >= 3 reduction slots.  p_in is never written (unless p_in == p_out).
@@ -700,7 +966,10 @@ int launch_gs(const double *p_in, double *p_out, double *tmp, FSrc fs, int n, do
         }
         return MGSR_OK;
     }
-    if (n % kTbTX == 0 && n % kTbTY == 0 && sweeps >= 1 && p_in != p_out) {
+    // register-blocked TMA kernel for the large levels (MGSR_GS_TB=1 selects the shared-memory tiles)
+    static const bool force_tb = std::getenv("MGSR_GS_TB") != nullptr;
+    const bool use_rb = n >= kRbMinN && n % 2 == 0 && !force_tb;
+    if ((use_rb || (n % kTbTX == 0 && n % kTbTY == 0)) && sweeps >= 1 && p_in != p_out) {
         const int chunks = (sweeps + kTbMaxK - 1) / kTbMaxK;
         if (chunks > 1 && !tmp) { set_error("gs: chunked sweeps need a scratch buffer"); return MGSR_E_BAD_ARG; }
         int done = 0;
@@ -718,7 +987,20 @@ int launch_gs(const double *p_in, double *p_out, double *tmp, FSrc fs, int n, do
             size_t smem = 4 * sizeof(double) * size_t(wp) * (kTbTY + 2 * H);
             double *mo = last ? mean_out : nullptr;
 #define MGSR_TB_LAUNCH(KK, RCV, RCP, RCM)                                                                  \
-    {                                                                                                      \
+    if (use_rb) {                                                                                          \
+        auto kern = k_gs_rb<KK, RCV>;                                                                      \
+        constexpr int HE = (2 * KK + (RCV ? 1 : 0) + 1) & ~1, TX = kRbW - 2 * HE;                          \
+        const int tl = ((n + TX - 1) / TX) * ((n + TX - 1) / TX);                                          \
+        const size_t rsm = sizeof(double) * (2 * kRbW * kRbW + 2 * 2 * kRbWarps * 64);                     \
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(rsm));                 \
+        int occ = 0;                                                                                       \
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kRbThreads, rsm);                        \
+        int blocks = num_sms() * (occ > 0 ? occ : 1);                                                      \
+        if (blocks > tl) blocks = tl;                                                                      \
+        CUtensorMap tmp_, tmf_;                                                                            \
+        if (make_tmap_2d(&tmp_, src ? src : fs.f, n) || make_tmap_2d(&tmf_, fs.f, n)) return MGSR_E_CUDA; \
+        kern<<<blocks, kRbThreads, rsm, st>>>(tmp_, tmf_, src, dst, fs, n, h2, zi, inv_h2, RCP, s0, mo, RCM); \
+    } else {                                                                                               \
         auto kern = k_gs_tb<KK, RCV>;                                                                      \
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));                \
         int occ = 0;                                                                                       \

@@ -29,9 +29,11 @@ def test_gs_golden(cuda, golden, n):
     assert rel(p, golden[f"gs{n}_out"]) < 1e-13
 
 
-@pytest.mark.parametrize("n,sweeps", [(96, 3), (128, 2), (256, 5), (512, 9), (1024, 2), (2048, 4), (4096, 2)])
+@pytest.mark.parametrize("n,sweeps", [(96, 3), (128, 2), (130, 3), (200, 1), (256, 5), (512, 9), (1000, 4),
+                                      (1024, 2), (2048, 4), (4096, 1), (4096, 2)])
 def test_gs_large_vs_oracle(cuda, orc, n, sweeps):
-    """Temporally blocked (n % 64 == 0) and half-sweep (n = 96) paths vs the C oracle."""
+    """Register-blocked TMA tiles (n >= 128, incl. ragged n: shifted edge tiles), half-sweep (n = 96) paths
+    vs the C oracle."""
     from paper_2403_07936_b200 import kernels
     p, f, h2 = random_problem(n, n)
     exp = p.copy(); orc.gs_sweeps(exp, f, h2, sweeps)
