@@ -161,6 +161,17 @@ int mgsr_plan_timing_read(mgsr_plan *plan, double *ms_out /* 3 */, int32_t *laun
 /* Number of kernel nodes in the captured graph of an operator (0 if not captured yet). */
 int32_t mgsr_plan_kernel_nodes(mgsr_plan *plan, int32_t use_sr);
 
+/* ---- seeded start of solve() (solver.py:298-300) ---- */
+
+/* out[i] = U_i - mean(U) with U_i = low + (high - low) * d_i, d_i the i-th double of
+ * numpy's PCG64 stream whose 128-bit state / increment are default_rng(seed).bit_generator
+ * .state (the SeedSequence hashing stays on the host), mean = numpy's pairwise sum / count.
+ * Bit-exact with np.random.default_rng(seed).uniform(low, high, count) minus its .mean().
+ * count must be a power of two >= 128.  Replaces the host draw of solver.py:298-300. */
+size_t mgsr_initial_iterate_workspace_bytes(int64_t count);
+int mgsr_initial_iterate(double *out, int64_t count, uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi,
+                         uint64_t inc_lo, double low, double high, void *ws, size_t ws_bytes, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -55,6 +55,9 @@ SIGNATURES = {
     "mgsr_plan_timing_enable": (ctypes.c_int, [vp, i32]),
     "mgsr_plan_timing_read": (ctypes.c_int, [vp, c_double_p, ctypes.POINTER(i32)]),
     "mgsr_plan_kernel_nodes": (i32, [vp, i32]),
+    "mgsr_initial_iterate_workspace_bytes": (sz, [i64]),
+    "mgsr_initial_iterate": (ctypes.c_int, [vp, i64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
+                                            ctypes.c_uint64, f64, f64, vp, sz, vp]),
 }
 
 

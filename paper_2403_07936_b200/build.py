@@ -27,6 +27,7 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", f"-I{ROOT}/in
 SOURCES = {
     "stencil.cu": ["--fmad=false"],
     "plan.cu": ["--fmad=false"],
+    "rng.cu": ["--fmad=false"],
     "generator_simt.cu": [],
     "generator_tc.cu": ["-maxrregcount=112"],
 }

@@ -203,3 +203,13 @@ def test_solve_batch_matches_single_solves(cuda, orc):
         assert lb.iterations == ls.iterations and lb.converged(1e-10)
         assert [r.operator for r in lb.records] == [r.operator for r in ls.records]
         assert np.array_equal(pb.data, ps.data)
+
+
+@pytest.mark.parametrize("n,seed,pmax", [(16, 0, 1e-3), (64, 3, 1e-3), (256, 0, 2.5e-2), (2048, 11, 1e-3)])
+def test_device_initial_iterate_bitwise(cuda, n, seed, pmax):
+    """mgsr_initial_iterate == numpy default_rng(seed).uniform(-p_max, p_max) - mean, bit for bit."""
+    from paper_2403_07936_b200 import solver
+    cfg = solver.RunConfig(seed=seed, p_max=pmax)
+    exp = solver.initial_iterate(n, cfg)
+    got = solver.initial_iterate_device(n, cfg).cpu().numpy()
+    assert np.array_equal(got, exp)

@@ -217,3 +217,54 @@ def test_solve_batch_rejects_mixed_sizes():
     b = PoissonProblem(Grid(np.zeros((32, 32))))
     with pytest.raises(ValueError, match="same side"):
         solver.solve_batch([a, b], solver.RunConfig())
+
+
+# ---- the algorithm of mgsr_initial_iterate (csrc/rng.cu), restated with Python integers and
+# checked against numpy: PCG64 jump-ahead + XSL-RR output + uniform, and the pairwise mean ----
+
+_PCG_MULT = 0x2360ED051FC65DA44385DF649FCCF645
+_M128 = (1 << 128) - 1
+
+
+def _pcg_advance(state, delta, inc):
+    cur_mult, cur_plus, acc_mult, acc_plus = _PCG_MULT, inc, 1, 0
+    while delta > 0:
+        if delta & 1:
+            acc_mult = (acc_mult * cur_mult) & _M128
+            acc_plus = (acc_plus * cur_mult + cur_plus) & _M128
+        cur_plus = ((cur_mult + 1) * cur_plus) & _M128
+        cur_mult = (cur_mult * cur_mult) & _M128
+        delta >>= 1
+    return (acc_mult * state + acc_plus) & _M128
+
+
+def _pcg_draw(state, inc):
+    state = (state * _PCG_MULT + inc) & _M128
+    x = ((state >> 64) ^ state) & ((1 << 64) - 1)
+    rot = state >> 122
+    return state, ((x >> rot) | (x << ((64 - rot) & 63))) & ((1 << 64) - 1)
+
+
+@pytest.mark.parametrize("seed", [0, 7, 12345])
+def test_pcg64_jump_ahead_matches_numpy_stream(seed):
+    st = np.random.default_rng(seed).bit_generator.state["state"]
+    s0, inc = int(st["state"]), int(st["inc"])
+    ref = np.random.default_rng(seed).uniform(-1e-3, 1e-3, size=4096)
+    for off in (0, 1, 127, 128, 1000, 4095):   # a thread's leaf starts at a jump-ahead offset
+        s = _pcg_advance(s0, off, inc)
+        _, u = _pcg_draw(s, inc)
+        d = (u >> 11) * (1.0 / 9007199254740992.0)
+        assert -1e-3 + (1e-3 - (-1e-3)) * d == ref[off]
+
+
+@pytest.mark.parametrize("n", [16, 64, 256, 1024])
+def test_pairwise_leaf_tree_equals_numpy_mean(n):
+    a = np.random.default_rng(n).uniform(-1e-3, 1e-3, size=(n, n))
+    leaves = a.reshape(-1, 16, 8)             # 128 values per leaf, 8 interleaved accumulators
+    r = leaves[:, 0, :].copy()
+    for k in range(1, 16):
+        r = r + leaves[:, k, :]
+    s = ((r[:, 0] + r[:, 1]) + (r[:, 2] + r[:, 3])) + ((r[:, 4] + r[:, 5]) + (r[:, 6] + r[:, 7]))
+    while s.size > 1:
+        s = s[0::2] + s[1::2]
+    assert (0.0 + s[0]) / (n * n) == a.mean()
