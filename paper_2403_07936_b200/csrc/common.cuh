@@ -61,12 +61,13 @@ __device__ __forceinline__ double warp_sum(double v) {
 // reproducible for a fixed launch geometry.  blockDim.x must be a multiple of 32.
 // grid_reduce_to: component k goes to *outs[k] * scales[k] (null outs[k] skipped;
 // all null -> no-op).  One fence + one ticket per block for all NV sums.
+// Returns true in thread 0 of the last block, after it wrote the outputs.
 template <int NV>
-__device__ void grid_reduce_to(double (&v)[NV], RedSlot slot, double *const (&outs)[NV], const double (&scales)[NV]) {
+__device__ bool grid_reduce_to(double (&v)[NV], RedSlot slot, double *const (&outs)[NV], const double (&scales)[NV]) {
     bool any = false;
 #pragma unroll
     for (int k = 0; k < NV; ++k) any |= outs[k] != nullptr;
-    if (!any) return;   // uniform across the grid
+    if (!any) return false;   // uniform across the grid
     __shared__ double sred[NV][32];
     __shared__ bool s_last;
     const int tid = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
@@ -93,7 +94,7 @@ __device__ void grid_reduce_to(double (&v)[NV], RedSlot slot, double *const (&ou
         s_last = atomicAdd(slot.counter, 1u) == unsigned(nblocks - 1);
     }
     __syncthreads();
-    if (!s_last) return;
+    if (!s_last) return false;
     __threadfence();
     double acc[NV];
 #pragma unroll
@@ -118,6 +119,7 @@ __device__ void grid_reduce_to(double (&v)[NV], RedSlot slot, double *const (&ou
         }
     }
     if (tid == 0) *slot.counter = 0u;
+    return tid == 0;
 }
 
 template <int NV>

@@ -238,7 +238,8 @@ static size_t pass_ws_floats(int apps) {
 size_t sr_workspace_bytes(int64_t nc, int s, int precision) {
     // intermediate fine grid for two-pass ratios + fp32 chunk buffers + scalars
     size_t inter = (s == 8 || s == 16) ? sizeof(double) * size_t(nc * 4) * size_t(nc * 4) : 0;
-    size_t simt = sizeof(float) * pass_ws_floats(2) + 4096;
+    // the fp32 CUDA-core chunk buffers only for fp32 (the tensor-core precisions never fall back to them)
+    size_t simt = precision == MGSR_PREC_FP32 ? sizeof(float) * pass_ws_floats(s == 2 ? 1 : 2) + 4096 : 0;
     size_t tc = precision != MGSR_PREC_FP32 ? tc_workspace_bytes(nc) : 0;
     return inter + (simt > tc ? simt : tc) + 512;
 }
@@ -439,7 +440,8 @@ extern "C" int mgsr_generator_forward(const mgsr_gen *g, const double *x, int64_
 }
 
 extern "C" size_t mgsr_sr_workspace_bytes(int64_t nc, int32_t s) {
-    return sr_workspace_bytes(nc, s, MGSR_PREC_BF16) + kRedSlotBytes + 256;
+    const size_t a = sr_workspace_bytes(nc, s, MGSR_PREC_FP32), b = sr_workspace_bytes(nc, s, MGSR_PREC_BF16);
+    return (a > b ? a : b) + kRedSlotBytes + 256;
 }
 
 extern "C" int mgsr_sr_prolong(const mgsr_gen *g, const double *c, int64_t nc, int32_t s, double p_min,

@@ -869,6 +869,87 @@ __global__ void k_finalize(const double *__restrict__ out, const double *mean_pt
     grid_reduce<3>(v, slot, acc_out, 1.0 / double(total));
 }
 
+// Row-marching form of k_finalize (same per-cell arithmetic): thread = two adjacent columns, a
+// block = 256 column pairs x kFinRows rows; the out rows above / at / below stay in registers
+// (out is read once per cell), left / right neighbours come by shuffle (lanes 0 / 31 load theirs),
+// the next row's loads are issued before the current row is computed.  The last block also
+// writes stats (k_stats_sqrt folded in).  n % 64 == 0.
+constexpr int kFinRows = 32;
+__global__ void __launch_bounds__(256) k_finalize_rows(const double *__restrict__ out, const double *mean_ptr,
+                                                       double *__restrict__ p, FSrc fs, int n, double inv_h2,
+                                                       RedSlot slot, double *acc_out, double *stats) {
+    const int lane = threadIdx.x & 31;
+    const int pj = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool active = 2 * pj < n;   // whole warps (n / 2 is a multiple of 32)
+    const int c0 = 2 * pj;
+    const int cl = c0 == 0 ? n - 1 : c0 - 1, cr = c0 + 2 >= n ? c0 + 2 - n : c0 + 2;
+    const int r0 = blockIdx.y * kFinRows, r1 = min(r0 + kFinRows, n);
+    const double m = *mean_ptr;
+    const double sh = fs.load_shift();
+    const bool shifted = fs.shift != nullptr;
+    double v[3] = {0.0, 0.0, 0.0};
+    if (active) {
+        auto row2 = [&](const double *a, int i) {
+            return __ldg(reinterpret_cast<const double2 *>(a + int64_t(i) * n + c0));
+        };
+        double2 up = row2(out, r0 == 0 ? n - 1 : r0 - 1), cur = row2(out, r0);
+        double2 dn = row2(out, r0 + 1 >= n ? r0 + 1 - n : r0 + 1);
+        double2 pp = *reinterpret_cast<const double2 *>(p + int64_t(r0) * n + c0), ff = row2(fs.f, r0);
+        double el = 0.0, er = 0.0;
+        if (lane == 0) el = __ldg(out + int64_t(r0) * n + cl);
+        if (lane == 31) er = __ldg(out + int64_t(r0) * n + cr);
+#pragma unroll 1
+        for (int i = r0; i < r1; ++i) {
+            // next row's loads first
+            const int i1 = i + 1 >= n ? i + 1 - n : i + 1, i2 = i + 2 >= n ? i + 2 - n : i + 2;
+            const bool more = i + 1 < r1;
+            double2 dn2 = dn, pp2 = pp, ff2 = ff;
+            double el2 = 0.0, er2 = 0.0;
+            if (more) {
+                dn2 = row2(out, i2);
+                pp2 = *reinterpret_cast<const double2 *>(p + int64_t(i1) * n + c0);
+                ff2 = row2(fs.f, i1);
+                if (lane == 0) el2 = __ldg(out + int64_t(i1) * n + cl);
+                if (lane == 31) er2 = __ldg(out + int64_t(i1) * n + cr);
+            }
+            double left = __shfl_up_sync(0xffffffffu, cur.y, 1);
+            double right = __shfl_down_sync(0xffffffffu, cur.x, 1);
+            if (lane == 0) left = el;
+            if (lane == 31) right = er;
+            const double nb0 = ((up.x + dn.x) + left) + cur.y;
+            const double nb1 = ((up.y + dn.y) + cur.x) + right;
+            const double f0 = shifted ? (ff.x - sh) * fs.scale : ff.x;
+            const double f1 = shifted ? (ff.y - sh) * fs.scale : ff.y;
+            const double np0 = cur.x - m, np1 = cur.y - m;
+            const double d0 = np0 - pp.x, d1 = np1 - pp.y;
+            const double q0 = f0 - ((nb0 - 4.0 * cur.x) * inv_h2);
+            const double q1 = f1 - ((nb1 - 4.0 * cur.y) * inv_h2);
+            *reinterpret_cast<double2 *>(p + int64_t(i) * n + c0) = make_double2(np0, np1);
+            v[0] += d0 * d0;
+            v[0] += d1 * d1;
+            v[1] += q0;
+            v[1] += q1;
+            v[2] += q0 * q0;
+            v[2] += q1 * q1;
+            up = cur;
+            cur = dn;
+            dn = dn2;
+            pp = pp2;
+            ff = ff2;
+            el = el2;
+            er = er2;
+        }
+    }
+    double *const outs[3] = {acc_out, acc_out + 1, acc_out + 2};
+    const double inv = 1.0 / (double(n) * double(n));
+    const double scales[3] = {inv, inv, inv};
+    if (grid_reduce_to<3>(v, slot, outs, scales)) {
+        stats[0] = sqrt(acc_out[0]);
+        const double var = acc_out[2] - acc_out[1] * acc_out[1];
+        stats[1] = sqrt(var > 0.0 ? var : 0.0);
+    }
+}
+
 __global__ void k_stats_sqrt(const double *acc, double *stats) {
     stats[0] = sqrt(acc[0]);
     double var = acc[2] - acc[1] * acc[1];
@@ -1087,6 +1168,12 @@ int launch_finalize(const double *out, const double *mean_ptr, double *p, FSrc f
                     double *stats2, void *red_slot, cudaStream_t st) {
     RedSlot sl = red_slot_at(red_slot);
     double h = 2.0 * M_PI / n;
+    const dim3 g((n / 2 + 255) / 256, (n + kFinRows - 1) / kFinRows);
+    if (n % 64 == 0 && int64_t(g.x) * g.y <= kRedMaxBlocks) {
+        k_finalize_rows<<<g, 256, 0, st>>>(out, mean_ptr, p, fs, n, 1.0 / (h * h), sl, acc3, stats2);
+        MGSR_LAUNCH_CHECK();
+        return MGSR_OK;
+    }
     k_finalize<<<grid_2d(n, n), 256, 0, st>>>(out, mean_ptr, p, fs, n, 1.0 / (h * h), sl, acc3);
     MGSR_LAUNCH_CHECK();
     k_stats_sqrt<<<1, 1, 0, st>>>(acc3, stats2);

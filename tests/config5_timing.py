@@ -34,7 +34,7 @@ def main():
         for gl in (1, 2, 3):
             cfg = solver.RunConfig(N_step=1, r_min=8, N_smooth=nu, mode="hybrid", N_GAN=1.0, S_thres=5e-4,
                                    N_iter=100)
-            solver.solve_batch(probs[:1], cfg, w, precision="fp16", sr_levels=gl)   # plans, graphs
+            solver.solve_batch(probs, cfg, w, precision="fp16", sr_levels=gl)   # plans, graphs (not timed)
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             res = solver.solve_batch(probs, cfg, w, precision="fp16", sr_levels=gl)
