@@ -541,7 +541,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
         // one N = 64 3x3 layer over the three tiles (body, post, up quarter), reading buffer `buf`
         // wait: 0 = act_ready (the rows this tile's taps read are written: tiles t - 1..t + 1), 1 = none,
         // 2/3 = up accumulator buffer 0/1 of this tile drained
-        auto conv_layer = [&](int lid, int buf, int wait, uint32_t dcol) {
+        auto conv_layer = [&](int lid, int buf, int wait, uint32_t dcol, auto &&after_t0) {
             const uint64_t a_desc0 = make_desc(act_base + buf * ACT_BYTES, ACT_PLANE, 128);
 #pragma unroll
             for (int t = 0; t < T; ++t) {
@@ -585,6 +585,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
                 }
                 __syncwarp();
                 if (lane == 0) tr(3, lid, t);
+                if (t == 0) after_t0();
             }
 #pragma unroll
             for (int tap = 0; tap < 9; ++tap) {
@@ -665,18 +666,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
             }
             slot0 += 2;
             slot0 = slot0 >= NSLOT ? slot0 - NSLOT : slot0;
+            auto none = [] {};
 #pragma unroll 1
-            for (int L = 0; L < NLAYERS; ++L) conv_layer(L + 1, L & 1, 0, COL_ACC);
+            for (int L = 0; L < NLAYERS; ++L) conv_layer(L + 1, L & 1, 0, COL_ACC, none);
             // up quarters (reading buffer NL & 1 = 1), accumulators double-buffered over cols [0, 192) and
             // [192, 384) (the residual stream and skip are dead after the post layer): quarter u + 1 runs
-            // while u drains; the tail of quarter u issues after up quarter u + 1, once u is drained into U
-            conv_layer(40, 1, 0, COL_ACC);
-            conv_layer(41, 1, 1, COL_RES);
-            tail_mma(0);
-            conv_layer(42, 1, 2, COL_ACC);
-            tail_mma(1);
-            conv_layer(43, 1, 3, COL_RES);
-            tail_mma(2);
+            // while u drains; the tail of quarter u issues after tile 0 of up quarter u + 1 (u is drained
+            // into U by then), so it completes before that quarter's tiles 1, 2 and the drain of u + 1
+            // (which rewrites U) overlaps their MMAs
+            conv_layer(40, 1, 0, COL_ACC, none);
+            conv_layer(41, 1, 1, COL_RES, [&] { tail_mma(0); });
+            conv_layer(42, 1, 2, COL_ACC, [&] { tail_mma(1); });
+            conv_layer(43, 1, 3, COL_RES, [&] { tail_mma(2); });
             tail_mma(3);
             grp_ph ^= 1u;
         }
@@ -714,50 +715,61 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
         Tracer tr{nullptr, 0};
         uint32_t af2_ph = 0;   // bit t = parity of the next completion of b_acc_full2[t]
         uint32_t z_ph = 0;     // parity of the next completion of b_zfull (one per group)
+        // q tables of a group's 8 windows (fp64 normalise -> fp32) -> misc
+        auto load_q = [&](int gq) {
+            const long long kq = (long long)(2 * gq + int(rank)) * WPG;
+            if (et < WPG * 36) {
+                const int wk = et / 36, pp = et % 36;
+                const Win W = window_of(P, kq + wk);
+                misc[et] = __ldg(P.qgrid + (long long)(W.iw + pp / 6) * P.nc + W.jw + pp % 6);
+            }
+            epi_bar();
+        };
+        // head im2col of tile t from misc (fp16, two buffers: tile t + 1 builds while tile t multiplies)
+        auto build_i2c = [&](int t) {
+            const int ib = t & 1;
+            if (i2c_uses[ib] > 0) mbar_wait(b_i2c_empty + 8 * ib, uint32_t(i2c_uses[ib] - 1) & 1u);
+            ++i2c_uses[ib];
+            {
+                const int r = et & 127, part4 = et >> 7;
+                const int rp = (2 * t + 1 + (r >> 6)) * 8 + (r & 7);   // padded pixel (py, px)
+                const float *qt = misc + ((r >> 3) & 7) * 36;
+                const uint2 *ix = reinterpret_cast<const uint2 *>(idx_tab + rp * HK);
+#pragma unroll
+                for (int kk = 0; kk < HPLANES / 4; ++kk) {
+                    const int kc = part4 * (HPLANES / 4) + kk;
+                    const uint2 i8 = ix[kc];
+                    uint32_t w[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const uint32_t src = e < 2 ? i8.x : i8.y;
+                        const uint32_t id0 = (src >> (16 * (e & 1))) & 0xFFu, id1 = (src >> (16 * (e & 1) + 8)) & 0xFFu;
+                        w[e] = pack_op<true>(id0 < 36 ? qt[id0] : 0.f, id1 < 36 ? qt[id1] : 0.f);
+                    }
+                    *reinterpret_cast<uint4 *>(i2c + ib * I2C_BYTES + kc * (ROWS * 16) + r * 16) =
+                        make_uint4(w[0], w[1], w[2], w[3]);
+                }
+            }
+            fence_async_smem();
+            epi_bar();
+            if (et == 0) mbar_arrive_leader(b_i2c_full + 8 * ib);
+            tr(12, 0, t);
+        };
+        // A group's head im2col tiles are built before the previous group's stitched-pixel epilogue
+        // (activation buffer 1 is free once the last up quarter's MMAs completed), so the head MMAs of
+        // the next group issue right behind the last tail MMAs and overlap that epilogue; tile 2 reuses
+        // im2col buffer 0 once tile 0's head MMAs completed.
+        epi_bar();   // the index table is complete
+        if (pair < ngp) {
+            load_q(pair);
+            for (int t = 0; t < T; ++t) build_i2c(t);
+        }
         for (int gp = pair; gp < ngp; gp += npairs) {
             const int g = 2 * gp + int(rank);
             const long long k0 = (long long)g * WPG;
             tr.buf = (P.prof && blockIdx.x == 0 && gp == TRACE_GROUP * npairs && lane == 0 &&
                       (warp == 2 || warp == 10)) ? P.prof + (warp == 2 ? 2 : 3) * 4096 : nullptr;
             tr(11, 0, 0);
-            // ---- q tables of the 8 windows (fp64 normalise -> fp32) ----
-            if (et < WPG * 36) {
-                const int wk = et / 36, pp = et % 36;
-                const Win W = window_of(P, k0 + wk);
-                misc[et] = __ldg(P.qgrid + (long long)(W.iw + pp / 6) * P.nc + W.jw + pp % 6);
-            }
-            epi_bar();
-            tr(11, 1, 0);
-            // ---- head: im2col per tile (fp16, two buffers: tile t + 1 builds while tile t multiplies) ----
-            for (int t = 0; t < T; ++t) {
-                const int ib = t & 1;
-                if (i2c_uses[ib] > 0) mbar_wait(b_i2c_empty + 8 * ib, uint32_t(i2c_uses[ib] - 1) & 1u);
-                ++i2c_uses[ib];
-                {
-                    const int r = et & 127, part4 = et >> 7;
-                    const int rp = (2 * t + 1 + (r >> 6)) * 8 + (r & 7);   // padded pixel (py, px)
-                    const float *qt = misc + ((r >> 3) & 7) * 36;
-                    const uint2 *ix = reinterpret_cast<const uint2 *>(idx_tab + rp * HK);
-#pragma unroll
-                    for (int kk = 0; kk < HPLANES / 4; ++kk) {
-                        const int kc = part4 * (HPLANES / 4) + kk;
-                        const uint2 i8 = ix[kc];
-                        uint32_t w[4];
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            const uint32_t src = e < 2 ? i8.x : i8.y;
-                            const uint32_t id0 = (src >> (16 * (e & 1))) & 0xFFu, id1 = (src >> (16 * (e & 1) + 8)) & 0xFFu;
-                            w[e] = pack_op<true>(id0 < 36 ? qt[id0] : 0.f, id1 < 36 ? qt[id1] : 0.f);
-                        }
-                        *reinterpret_cast<uint4 *>(i2c + ib * I2C_BYTES + kc * (ROWS * 16) + r * 16) =
-                            make_uint4(w[0], w[1], w[2], w[3]);
-                    }
-                }
-                fence_async_smem();
-                epi_bar();
-                if (et == 0) mbar_arrive_leader(b_i2c_full + 8 * ib);
-                tr(12, 0, t);
-            }
             // ---- head + body + post epilogues: layer L (head = -1) writes buffer (L + 1) & 1 ----
             for (int L = -1; L < NL; ++L) {
                 uint8_t *obuf = act + ((L + 1) & 1) * ACT_BYTES;
@@ -927,6 +939,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
                 __syncwarp();
                 if (lane == 0) mbar_arrive_leader(b_ubuf_full);
             }
+            // ---- next group's q tables and head im2col (buffer 1: the up MMAs are complete) ----
+            if (gp + npairs < ngp) {
+                load_q(gp + npairs);
+                tr(11, 1, 0);
+                for (int t = 0; t < T; ++t) build_i2c(t);   // tile 2 reuses buffer 0 once head tile 0 multiplied
+            }
             // ---- stitched pixels: warps of channel quarter cq = j finish Z tile j (kept fine row y = 4 + j).
             // Lane (quadrant q, lane) holds Z row (window 2 q + lane / 16, X = lane % 16); the kept pixel X
             // in 4..7 sums Z[X + dx - 4][3 dx + o] over dx by shuffles, then bias + s tanh(./s), channel
@@ -958,7 +976,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
 #pragma unroll
                         for (int o = 0; o < 3; ++o) m += double(P.tanh_s * tanhf(pre[o] / P.tanh_s));
                         m = m / 3.0;
-                        P.fine[(long long)(2 * W.iw + 4 + j) * P.nf + 2 * W.jw + X] = denormalize_q(m, P.log_lo, P.span);
+                        // sign(q) 10^(log_lo + |q| span) in fp32 (exp2f; <= 3e-6 relative, far inside the fp16
+                        // operands' error), off the critical path's fp64 pow
+                        const float e = (float(P.log_lo) + float(fabs(m)) * float(P.span)) * 3.32192809488736f;
+                        const double mag = double(exp2f(e));
+                        P.fine[(long long)(2 * W.iw + 4 + j) * P.nf + 2 * W.jw + X] = m > 0.0 ? mag : (m < 0.0 ? -mag : 0.0);
                     }
                 }
                 tr(14, 0, j);
