@@ -328,11 +328,12 @@ struct Params {
 // Event trace of one steady-state group of CTA 0: role r (0 producer, 1 MMA, 2 epilogue warp 2,
 // 3 epilogue warp 10) appends (id, clock64) pairs at prof[r * 4096 + 2 i]; id = type * 1000 + a * 10 + b.
 constexpr int TRACE_GROUP = 3;
+template <bool ON>
 struct Tracer {
     unsigned long long *buf;
     int n;
     __device__ __forceinline__ void operator()(int type, int a, int b) {
-        if (buf && n < 2040) {
+        if (ON && buf && n < 2040) {
             buf[2 * n] = (unsigned long long)(type * 1000 + a * 10 + b);
             buf[2 * n + 1] = (unsigned long long)clock64();
             ++n;
@@ -377,7 +378,8 @@ __device__ __forceinline__ double denormalize_q(double q, double log_lo, double 
     return q > 0.0 ? mag : -mag;
 }
 
-template <bool F16>
+// INSTR: bring-up instrumentation (P.prof event trace, P.dbg layer dumps) compiled in
+template <bool F16, bool INSTR>
 __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
     extern __shared__ __align__(128) uint8_t smem[];
     uint8_t *act = smem + OFF_ACT;   // two buffers of ACT_BYTES
@@ -533,7 +535,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
         const uint32_t i2c_base = smem_u32(i2c), u_base = smem_u32(ubuf);
         const uint32_t id64 = F16 ? idesc_f16(64) : idesc_bf16(64);
         const uint64_t b_desc0 = make_desc(ring_base, 512, 128);         // half tap: 32-row planes
-        Tracer tr{nullptr, 0};
+        Tracer<INSTR> tr{nullptr, 0};
         auto wait_ar = [&](int t) {
             mbar_wait(b_act_ready + 8 * t, (ar_ph >> t) & 1u);
             ar_ph ^= 1u << t;
@@ -712,7 +714,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
         }
         const float *up_a = cs + 64 + 192 * NL;
         const float *tail_b = up_a + 64;
-        Tracer tr{nullptr, 0};
+        Tracer<INSTR> tr{nullptr, 0};
         uint32_t af2_ph = 0;   // bit t = parity of the next completion of b_acc_full2[t]
         uint32_t z_ph = 0;     // parity of the next completion of b_zfull (one per group)
         // q tables of a group's 8 windows (fp64 normalise -> fp32) -> misc
@@ -770,6 +772,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
             tr.buf = (P.prof && blockIdx.x == 0 && gp == TRACE_GROUP * npairs && lane == 0 &&
                       (warp == 2 || warp == 10)) ? P.prof + (warp == 2 ? 2 : 3) * 4096 : nullptr;
             tr(11, 0, 0);
+            const Win Wd = window_of(P, k0 + wrow);   // this thread's window in the up drains
             // ---- head + body + post epilogues: layer L (head = -1) writes buffer (L + 1) & 1 ----
             for (int L = -1; L < NL; ++L) {
                 uint8_t *obuf = act + ((L + 1) & 1) * ACT_BYTES;
@@ -854,7 +857,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
                             *reinterpret_cast<uint4 *>(dp + ACT_PLANE) = v1;
                         }
                     }
-                    if (P.dbg && P.dbg_layer == L + 1 && interior) {
+                    if (INSTR && P.dbg && P.dbg_layer == L + 1 && interior) {
                         const long long k = k0 + wrow;
                         if (k < P.nwin) {
                             const int pp = (2 * t + pyl) * 6 + (px - 1);
@@ -913,7 +916,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
                                 make_uint2(pack_op<F16>(y[sub], y[4 + sub]), pack_op<F16>(y[8 + sub], y[12 + sub]));
                         }
                         const long long k = k0 + wrow;
-                        const Win W = window_of(P, k);
+                        const Win &W = Wd;
                         const int pp = (py - 1) * 6 + (px - 1);
                         if (W.valid && W.edge) {
                             uint32_t pk[8];
@@ -924,7 +927,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
                             dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
                             dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
                         }
-                        if (P.dbg && P.dbg_layer == NL + 1 && W.valid) {
+                        if (INSTR && P.dbg && P.dbg_layer == NL + 1 && W.valid) {
 #pragma unroll
                             for (int j = 0; j < 16; ++j) {
                                 const int c = UQ * u + 4 * cq + (j >> 2), Y = 2 * (py - 1) + ((j >> 1) & 1),
@@ -1259,8 +1262,10 @@ int launch_sr_pass_tc_dbg(const mgsr_gen *g, const double *c, const double *c_sh
     int dev = 0, nsm = 0;
     MGSR_CUDA_TRY(cudaGetDevice(&dev));
     MGSR_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    MGSR_CUDA_TRY(cudaFuncSetAttribute(k_gen_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    MGSR_CUDA_TRY(cudaFuncSetAttribute(k_gen_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    const bool instr = dbg != nullptr || prof != nullptr;
+    auto kern = f16 ? (instr ? k_gen_tc<true, true> : k_gen_tc<true, false>)
+                    : (instr ? k_gen_tc<false, true> : k_gen_tc<false, false>);
+    MGSR_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     k_normalize<<<grid_for((long long)nc * nc, 256), 256, 0, st>>>(c, c_shift, nc, log_lo, span, qgrid);
     MGSR_LAUNCH_CHECK();
     // CTA pairs (clusters of 2), one CTA per SM, as many pairs as can be co-resident
@@ -1281,14 +1286,12 @@ int launch_sr_pass_tc_dbg(const mgsr_gen *g, const double *c, const double *c_sh
     if (mp == 0) {
         cfg.gridDim = dim3(2 * (nsm / 2));
         int ncl = 0;
-        cudaError_t e = f16 ? cudaOccupancyMaxActiveClusters(&ncl, k_gen_tc<true>, &cfg)
-                            : cudaOccupancyMaxActiveClusters(&ncl, k_gen_tc<false>, &cfg);
+        cudaError_t e = cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg);
         mp = (e == cudaSuccess && ncl > 0) ? ncl : nsm / 2;
     }
     const int pairs = ngp < mp ? ngp : mp;
     cfg.gridDim = dim3(2 * pairs);
-    if (f16) MGSR_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_gen_tc<true>, P));
-    else MGSR_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_gen_tc<false>, P));
+    MGSR_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, P));
     if (f16) k_tail_edge<true><<<edge_count(P.npos), 256, 0, st>>>(P);
     else k_tail_edge<false><<<edge_count(P.npos), 256, 0, st>>>(P);
     MGSR_LAUNCH_CHECK();
