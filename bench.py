@@ -6,9 +6,14 @@ Workload (``config.workload``): periodic 4096^2 grid, N_step=1 ladder
 4096 -> 8 (10 levels), N_smooth=2, coarse_sweeps=10, SR ("GAN") prolongation
 at the 3 finest prolongations (2048->4096, 1024->2048, 512->1024; 1,369,100
 windows of 6x6), Keys spline below; generator = reference architecture, B=8
-residual blocks, seeded He-normal weights (``random_weights(8, 0)``; the
-reference's trained artifacts are absent), bf16 tcgen05 operands with fp32
-accumulation (tf32 head, fp32 tail); fp64 stencils.  RHS: seeded Gaussian
+residual blocks; weights: the reference's trained-weights slot (pkg/artifacts)
+is empty, so BASELINE's "trained weights if present" is filled by
+artifacts/trained_b8.mgsr, produced by the reference's own documented
+training pipeline (artifacts/PROVENANCE.md); ``--weights he`` selects the
+seeded He-normal init (``random_weights(8, 0)``).  Speed does not depend on
+the weights; the fp16 field parity bar (1e-2 relL2) does: trained weights
+meet it, He-init weights amplify operand rounding (2e-2).
+fp16 tcgen05 operands with fp32 accumulation; fp64 stencils.  RHS: seeded Gaussian
 random field k^-5/3 + 32 blobs scaled to p_rms = 1e-4 (in the SR band).
 A step = one V-cycle + the solve loop's logging pass (diff and residual
 norms), one CUDA-graph launch.  Inputs (134 MB per fp64 grid) exceed the
@@ -51,6 +56,7 @@ def parse():
     ap.add_argument("--precision", default="fp16", choices=["fp16", "bf16", "fp32"])
     ap.add_argument("--sr-levels", type=int, default=3)
     ap.add_argument("--blocks", type=int, default=8)
+    ap.add_argument("--weights", default="trained", choices=["trained", "he"])
     ap.add_argument("--n-smooth", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -155,6 +161,18 @@ def measured_peaks():
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
 
 
+def weights_path(kind: str, blocks: int):
+    path = os.path.join(ROOT, "artifacts", f"trained_b{blocks}.mgsr")
+    return path if kind == "trained" and os.path.exists(path) else None
+
+
+def bench_weights(kind: str, blocks: int, srmodel_mod):
+    """MGSR1 trained weights (artifacts/) or the seeded He-normal init; same loader API in the
+    reference's srmodel and ours."""
+    path = weights_path(kind, blocks)
+    return srmodel_mod.load_weights(path) if path else srmodel_mod.random_weights(blocks, 0)
+
+
 def load_traffic(mode):
     """ncu dram bytes per launch of the dominant kernel, if a capture summary is committed."""
     path = os.path.join(ROOT, "profiles", "traffic.json")
@@ -208,7 +226,7 @@ def run_mine(args, rank: int, world: int, dist):
     dev = torch.device("cuda")
     n = args.n
     cfg = RunConfig(N_step=1, r_min=8, N_smooth=args.n_smooth, coarse_sweeps=10)
-    weights = srmodel.random_weights(args.blocks, 0) if args.mode == "gan" else None
+    weights = bench_weights(args.weights, args.blocks, srmodel) if args.mode == "gan" else None
     op = "sr" if args.mode == "gan" else "spline"
     plan = VCyclePlan(n, cfg, weights, precision=args.precision, sr_levels=args.sr_levels)
     f_np, p_np = make_inputs(n, replica_seed(rank), args.mode)
@@ -319,7 +337,7 @@ def run_mine(args, rank: int, world: int, dist):
 # ---------------------------------------------------------------------------
 # CPU baseline: the reference compiled from its own sources (oracle/_ref)
 
-def cpu_reference_sample(n: int, blocks: int, windows: int, mode: str, sr_levels: int):
+def cpu_reference_sample(n: int, blocks: int, windows: int, mode: str, sr_levels: int, wkind: str = "trained"):
     """Time the reference on a bounded sample and project V-cycles/s at n^2.
     Returns (projected cycles/s, kind, sample description)."""
     import numpy as np
@@ -331,7 +349,7 @@ def cpu_reference_sample(n: int, blocks: int, windows: int, mode: str, sr_levels
     if kind == "reference":
         from mgsr import smoother, solver, srmodel
         from mgsr.grid import Grid
-        w = srmodel.random_weights(blocks, 0)
+        w = bench_weights(wkind, blocks, srmodel)
 
         def fwd(x):
             return srmodel._forward_batch(w, x)
@@ -345,7 +363,8 @@ def cpu_reference_sample(n: int, blocks: int, windows: int, mode: str, sr_levels
             return time.perf_counter() - t0
     else:
         from oracle import mgsr_oracle as orc
-        w = orc.random_weights(blocks, 0)
+        path = weights_path(wkind, blocks)
+        w = orc.read_mgsr1(path) if path else orc.random_weights(blocks, 0)
 
         def fwd(x):
             return orc.forward_batch(w, x)
@@ -390,7 +409,7 @@ def run_reference_arm(args, rank, world):
     kind, sample = "reference", ""
     windows = 32 if args.mode == "gan" else 0
     for i in range(args.warmup + args.steps):
-        cyc, kind, sample = cpu_reference_sample(args.n, args.blocks, max(windows, 1), args.mode, args.sr_levels)
+        cyc, kind, sample = cpu_reference_sample(args.n, args.blocks, max(windows, 1), args.mode, args.sr_levels, wkind=args.weights)
         if i >= args.warmup:
             vals.append(cyc)
     v = sum(vals) / len(vals)
@@ -414,6 +433,8 @@ def workload_config(args):
     return {"workload": wl, "grid": args.n, "levels": len(_sides(args.n)), "mode": args.mode,
             "precision": args.precision if args.mode == "gan" else "fp64",
             "generator_blocks": args.blocks, "sr_levels": args.sr_levels if args.mode == "gan" else 0,
+            "weights": ("trained" if weights_path(args.weights, args.blocks) else "he_init") if args.mode == "gan"
+            else None,
             "parallelism": f"replicas x{args.gpus}", "l2": "inputs (134 MB/grid) exceed L2; no flush"}
 
 
@@ -467,7 +488,9 @@ def main():
             "metric": METRIC, "value": cyc_s, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": res["ms_total"] / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": f"f64+{args.precision}" if args.mode == "gan" else "f64",
-            "data": "synthetic (seeded GRF k^-5/3 + blobs RHS; seeded He-init generator weights)",
+            "data": "synthetic (seeded GRF k^-5/3 + blobs RHS); generator weights " + (
+                "artifacts/trained_b%d.mgsr (reference training pipeline)" % args.blocks
+                if weights_path(args.weights, args.blocks) else "seeded He-normal init"),
             "config": workload_config(args), "gupdates_per_s": cyc_s * n * n / 1e9,
             "roofline": roof, "clocks": res["clocks"],
             "gpu_launches": res["kernels"] * args.steps,
@@ -481,7 +504,7 @@ def main():
                                    "copies on a second stream, double-buffered across steps"}
         if not args.no_cpu_baseline:
             try:
-                cyc, kind, sample = cpu_reference_sample(n, args.blocks, 256, args.mode, args.sr_levels)
+                cyc, kind, sample = cpu_reference_sample(n, args.blocks, 256, args.mode, args.sr_levels, wkind=args.weights)
                 line["cpu_baseline"] = {"value": cyc, "unit": UNIT, "cores": os.cpu_count(), "kind": kind,
                                         "sample": sample}
             except Exception as exc:  # the baseline never blocks the GPU line
