@@ -22,6 +22,13 @@ void set_error(const std::string &msg) { g_last_error = msg; }
 
 __device__ __forceinline__ int wrap(int i, int n) { return i < 0 ? i + n : (i >= n ? i - n : i); }
 
+// t -> (t / d, t % d) with a shift when d is a power of two (every N_step = 1 ladder)
+__device__ __forceinline__ void split_idx(int t, int d, int dsh, int &q, int &r) {
+    if (dsh >= 0) { q = t >> dsh; r = t & (d - 1); }
+    else { q = t / d; r = t - q * d; }
+}
+__device__ __forceinline__ int pow2_shift(int d) { return (d & (d - 1)) == 0 ? __ffs(d) - 1 : -1; }
+
 // Row-parallel 2-D loops: threads of a block cover consecutive columns (coalesced), blocks
 // stride over rows.  No per-element 64-bit division (which dominated the 1-D
 // grid-stride versions: k_finalize ran at 1.3 TB/s on a 4096^2 grid).
@@ -78,12 +85,13 @@ __global__ void __launch_bounds__(1024) k_gs_small(double *__restrict__ p, FSrc 
         sf[c] = fs.at(c, sh);
     }
     __syncthreads();
-    const int half = nn >> 1;
+    const int half = nn >> 1, hn = n >> 1, hsh = pow2_shift(hn);
     for (int s = 0; s < sweeps; ++s) {
         for (int color = 0; color < 2; ++color) {
             for (int t = tid; t < half; t += nt) {
-                int i = t / (n >> 1);
-                int j = 2 * (t % (n >> 1)) + ((i + color) & 1);
+                int i, k;
+                split_idx(t, hn, hsh, i, k);
+                int j = 2 * k + ((i + color) & 1);
                 int im1 = i > 0 ? i - 1 : n - 1, ip1 = i < n - 1 ? i + 1 : 0;
                 int jm1 = j > 0 ? j - 1 : n - 1, jp1 = j < n - 1 ? j + 1 : 0;
                 double nb = ((sp[im1 * n + j] + sp[ip1 * n + j]) + sp[i * n + jm1]) + sp[i * n + jp1];
@@ -120,6 +128,8 @@ __global__ void __launch_bounds__(1024) k_gs_small(double *__restrict__ p, FSrc 
 // prolongation of the level below (the k_prolong2_add arithmetic).  Replaces
 // ~4 launches per level on the latency-bound bottom of every V-cycle.
 constexpr int kSmallMaxLev = 8;
+constexpr int kSmallThreads = 256;   // fewer, busier threads: the bottom levels are latency- and issue-bound
+
 struct SmallLadder {
     int nlev;
     int side[kSmallMaxLev];
@@ -140,7 +150,7 @@ __device__ double block_sum_1024(double v, double *sred) {
     return sred[32];
 }
 
-__global__ void __launch_bounds__(1024) k_correction_small(const double *__restrict__ rc0, const double *rc0_mean,
+__global__ void __launch_bounds__(kSmallThreads) k_correction_small(const double *__restrict__ rc0, const double *rc0_mean,
                                                            double *__restrict__ d0, SmallLadder L, int n_smooth,
                                                            int coarse_sweeps) {
     extern __shared__ double sm[];
@@ -169,11 +179,13 @@ __global__ void __launch_bounds__(1024) k_correction_small(const double *__restr
         for (int c = tid; c < nn; c += nt) sp[c] = 0.0;
         __syncthreads();
         const int sweeps = j == L.nlev - 1 ? coarse_sweeps : n_smooth;
+        const int hn = n >> 1, hsh = pow2_shift(hn);
         for (int s = 0; s < sweeps; ++s) {
             for (int color = 0; color < 2; ++color) {
                 for (int t = tid; t < half; t += nt) {
-                    int i = t / (n >> 1);
-                    int jj = 2 * (t % (n >> 1)) + ((i + color) & 1);
+                    int i, k;
+                    split_idx(t, hn, hsh, i, k);
+                    int jj = 2 * k + ((i + color) & 1);
                     int im1 = i > 0 ? i - 1 : n - 1, ip1 = i < n - 1 ? i + 1 : 0;
                     int jm1 = jj > 0 ? jj - 1 : n - 1, jp1 = jj < n - 1 ? jj + 1 : 0;
                     double nb = ((sp[im1 * n + jj] + sp[ip1 * n + jj]) + sp[i * n + jm1]) + sp[i * n + jp1];
@@ -192,8 +204,10 @@ __global__ void __launch_bounds__(1024) k_correction_small(const double *__restr
             const double inv_h2 = 1.0 / h2;
             double *fr = F[j + 1];
             double acc = 0.0;
+            const int csh = pow2_shift(nc);
             for (int t = tid; t < ncc; t += nt) {
-                const int ic = t / nc, jc = t - ic * nc;
+                int ic, jc;
+                split_idx(t, nc, csh, ic, jc);
                 const int i = 2 * ic, jj = 2 * jc;
                 const int im1 = i > 0 ? i - 1 : n - 1, ip1 = i < n - 1 ? i + 1 : 0;
                 const int jm1 = jj > 0 ? jj - 1 : n - 1, jp1 = jj < n - 1 ? jj + 1 : 0;
@@ -214,8 +228,10 @@ __global__ void __launch_bounds__(1024) k_correction_small(const double *__restr
         const int nc = L.side[j + 1], n = 2 * nc;
         const double *c = D[j + 1];
         double *out = D[j];
+        const int csh = pow2_shift(nc);
         for (int t = tid; t < nc * nc; t += nt) {
-            const int bi = t / nc, bj = t - bi * nc;
+            int bi, bj;
+            split_idx(t, nc, csh, bi, bj);
             int ri[4];
 #pragma unroll
             for (int o = 0; o < 4; ++o) {
@@ -1196,7 +1212,7 @@ int launch_correction_small(const double *rc0, const double *rc0_mean, double *d
         smem += 2 * sizeof(double) * size_t(sides[j]) * sides[j];
     }
     cudaFuncSetAttribute(k_correction_small, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    k_correction_small<<<1, 1024, smem, st>>>(rc0, rc0_mean, d0, L, n_smooth, coarse_sweeps);
+    k_correction_small<<<1, kSmallThreads, smem, st>>>(rc0, rc0_mean, d0, L, n_smooth, coarse_sweeps);
     MGSR_LAUNCH_CHECK();
     return MGSR_OK;
 }
