@@ -786,6 +786,67 @@ __global__ void k_prolong_add(const double *__restrict__ c, int nc, int s, const
     if (do_mean) grid_reduce<1>(v, slot, mean_out, 1.0 / double(total));
 }
 
+// Ratios 4/8/16 (power of two, s <= 16): the same arithmetic as k_prolong_add with the Keys
+// weights of each phase tabulated once per block (the phase is I mod s), the column's weights,
+// indices and phase hoisted out of the row loop, and shifts instead of divisions.  Threads own
+// a column J and walk rows, so the coarse neighbourhood is shared through L1 by the s threads of
+// a coarse block.  Bitwise identical to k_prolong_add.
+__global__ void k_prolong_add_pow2(const double *__restrict__ c, int nc, int s, int ssh, int ps,
+                                   const double *__restrict__ base, const double *bshift, double *__restrict__ out,
+                                   RedSlot slot, double *mean_out, int do_mean) {
+    __shared__ double wtab[16][4];
+    const int n = nc * s;
+    const int64_t total = int64_t(n) * n;
+    const double bsh = (base && bshift) ? *bshift : 0.0;
+    const double inv_s = 1.0 / double(s);
+    if (int(threadIdx.x) < 4 * s) {
+        const int ph = threadIdx.x >> 2, o = threadIdx.x & 3;
+        wtab[ph][o] = keys_w(double(ph) * inv_s - double(o - 1));
+    }
+    __syncthreads();
+    double v[1] = {0.0};
+    MGSR_COLS(J, n) {
+        const int bj = J >> ssh, pj = J & (s - 1);
+        double wj[4];
+        int cj[4];
+#pragma unroll
+        for (int o = 0; o < 4; ++o) {
+            wj[o] = wtab[pj][o];
+            cj[o] = wrap(bj + o - 1, nc);
+        }
+        // item = (coarse row bi, a run of ps of its s fine rows): the 4 x 4 coarse neighbourhood stays in
+        // registers for those fine rows (ps < s only to spread small grids over more blocks)
+        const int nrun = s / ps;
+        MGSR_ROWS(item, nc * nrun) {
+            const int bi = item / nrun, p0 = (item - bi * nrun) * ps;
+            double cc[4][4];
+#pragma unroll
+            for (int a = 0; a < 4; ++a) {
+                const double *cr = c + int64_t(wrap(bi + a - 1, nc)) * nc;
+#pragma unroll
+                for (int b = 0; b < 4; ++b) cc[a][b] = __ldg(cr + cj[b]);
+            }
+#pragma unroll 4
+            for (int pi = p0; pi < p0 + ps; ++pi) {
+                const int I = (bi << ssh) + pi;
+                const int64_t t = int64_t(I) * n + J;
+                double acc = 0.0;
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    double row = 0.0;
+#pragma unroll
+                    for (int a = 0; a < 4; ++a) row += wtab[pi][a] * cc[a][b];
+                    acc += wj[b] * row;
+                }
+                const double val = base ? (__ldg(base + t) - bsh) + acc : acc;
+                out[t] = val;
+                v[0] += val;
+            }
+        }
+    }
+    if (do_mean) grid_reduce<1>(v, slot, mean_out, 1.0 / double(total));
+}
+
 // Ratio-2 specialisation: one thread per coarse cell (bi, bj) produces the 2x2
 // fine block (2bi + {0,1}, 2bj + {0,1}).  With s = 2, t is 0 or 1/2 and the
 // Keys weights are exact constants: t = 0 gives (0, 1, 0, 0), whose weighted
@@ -1152,6 +1213,17 @@ int launch_prolong_add(const double *c, int nc, int s, const double *base, const
     RedSlot sl = red_slot_at(red_slot);
     if (s == 2) {
         k_prolong2_add<<<grid_2d(nc, nc), 256, 0, st>>>(c, nc, base, bshift, out, sl, mean_out, mean_out != nullptr);
+        MGSR_LAUNCH_CHECK();
+        return MGSR_OK;
+    }
+    if (s <= 16 && (s & (s - 1)) == 0 && nc * s <= 8192) {
+        // enough row items for ~8 blocks per SM: split each coarse row's s fine rows into runs
+        const int cols = (nc * s + 255) / 256;
+        int ps = s;
+        while (ps > 1 && int64_t(nc) * (s / ps) * cols < 148 * 8) ps >>= 1;
+        k_prolong_add_pow2<<<grid_2d(nc * (s / ps), nc * s), 256, 0, st>>>(c, nc, s, __builtin_ctz(s), ps, base,
+                                                                           bshift, out, sl, mean_out,
+                                                                           mean_out != nullptr);
         MGSR_LAUNCH_CHECK();
         return MGSR_OK;
     }
