@@ -213,3 +213,21 @@ def test_device_initial_iterate_bitwise(cuda, n, seed, pmax):
     exp = solver.initial_iterate(n, cfg)
     got = solver.initial_iterate_device(n, cfg).cpu().numpy()
     assert np.array_equal(got, exp)
+
+
+def test_default_config_ladder_3072_vs_oracle(cuda, orc):
+    """The reference's default RunConfig (N_step=4, r_min=12, N_smooth=20) at 3072^2: ladder
+    [3072, 192, 12] with ratio-16 spline prolongations and 20-sweep smoothing (chunked K=4 register
+    tiles).  Two V-cycles against the CPU oracle."""
+    from paper_2403_07936_b200 import datagen, solver
+    from paper_2403_07936_b200.grid import Grid
+    from paper_2403_07936_b200.smoother import PoissonProblem
+    n = 3072
+    f = datagen.grf_blobs_rhs(n, seed=0, kmax=n / 8)
+    ocfg = orc.Config(N_step=4, r_min=12, N_smooth=20)
+    p = orc.initial_iterate(n, orc.Config())
+    exp = orc.v_cycle(orc.v_cycle(p, f, ocfg, "spline"), f, ocfg, "spline")
+    cfg = cfg_(N_step=4, r_min=12, N_smooth=20)
+    got = solver.v_cycle(solver.v_cycle(Grid(p), PoissonProblem(Grid(f)), cfg, "spline"),
+                         PoissonProblem(Grid(f)), cfg, "spline").data
+    assert rel(got, exp) < 1e-12
