@@ -1014,81 +1014,127 @@ __global__ void k_normalize(const double *__restrict__ c, const double *shift, i
 
 // Tail of the edge windows (kept band touching the grid edge), exact fp32 with
 // the reference's replicate clamping (srmodel.py:285-289) on the 12x12 field.
+// Register-blocked and persistent: the fp32 tail weights are staged once per CTA as [c][dy][o][dx (12)], each
+// edge window's up-conv output as a replicate-padded [c][20][20] fp32 image (so every 9 x 9 tap
+// reads in bounds and 4 consecutive pixels' taps are one 12-float row); thread = (2 channels,
+// a strip of 4 kept pixels) accumulates 4 px x 3 outputs, 108 FMAs per 21 16-byte loads; the
+// 32 channel groups are reduced through shared memory.
+constexpr int TE_THREADS = 256, TE_PAD = 20, TE_WROW = 12;
+constexpr int TE_W_FLOATS = 64 * 9 * 3 * TE_WROW;        // 20736
+constexpr int TE_U_FLOATS = 64 * TE_PAD * TE_PAD;        // 25600
+constexpr int TE_R_FLOATS = 32 * 8 * 12;                 // partial sums [group][strip slot][4 px x 3 o]
+constexpr size_t TE_SMEM = sizeof(float) * (TE_W_FLOATS + TE_U_FLOATS + TE_R_FLOATS);
+
 template <bool F16>
-__global__ void __launch_bounds__(256) k_tail_edge(Params P) {
-    __shared__ float U[64 * 144];       // [c][Y][X]
-    __shared__ float Wt[3 * 8 * 81];    // weights of one 8-channel chunk [o][c][tap]
-    __shared__ float part[144 * 3];     // per (pixel, o) results (<= 144 kept pixels: the npos = 1 window)
-    const int e = blockIdx.x;
-    // invert edge_index
-    int wi, wj;
-    const int n = P.npos;
-    if (n == 1) { wi = 0; wj = 0; }
-    else if (e < n) { wi = 0; wj = e; }
-    else if (e < 2 * n) { wi = n - 1; wj = e - n; }
-    else { wi = 1 + (e - 2 * n) / 2; wj = ((e - 2 * n) & 1) ? n - 1 : 0; }
-    const uint16_t *src = P.edge_u + size_t(e) * 36 * 256;
-    for (int i = threadIdx.x; i < 36 * 256; i += blockDim.x) {
-        const int pp = i >> 8, oc = i & 255, c = oc >> 2, ii = (oc >> 1) & 1, jj = oc & 1;
-        const int Y = 2 * (pp / 6) + ii, X = 2 * (pp % 6) + jj;
-        U[c * 144 + Y * 12 + X] = op_lo<F16>(uint32_t(src[i]));
-    }
+__global__ void __launch_bounds__(TE_THREADS) k_tail_edge(Params P, int nedge) {
+    extern __shared__ __align__(16) float te[];
+    float *Wt = te, *U = te + TE_W_FLOATS, *red = U + TE_U_FLOATS;
+    const int tid = threadIdx.x;
     const BlobLayout BL = blob_layout((P.nl - 1) / 2);
     const float *w = reinterpret_cast<const float *>(P.blob + BL.tail_f32);   // [3][64][81]
     const float *bias = reinterpret_cast<const float *>(P.blob + BL.consts) + 64 + 192 * P.nl + 64;
-    const int last = P.npos - 1;
-    const int lo_i = wi == 0 ? 0 : 2, hi_i = wi == last ? 6 : 4, lo_j = wj == 0 ? 0 : 2, hi_j = wj == last ? 6 : 4;
-    const int wk = 2 * (hi_j - lo_j), npix = 2 * (hi_i - lo_i) * wk;   // <= 144 kept pixels
-    // work item = (pixel, output o), up to two per thread; weights staged per 8-channel chunk, U reused
-    // from shared memory
-    int yo[2][9], xo[2][9], wo[2];
-    bool act[2];
-    float acc[2] = {0.f, 0.f};
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-        const int item = threadIdx.x + h * blockDim.x, idx = item / 3;
-        wo[h] = item - 3 * idx;
-        act[h] = idx < npix;
-        const int fy = act[h] ? 2 * lo_i + idx / wk : 0, fx = act[h] ? 2 * lo_j + idx % wk : 0;
-#pragma unroll
-        for (int d = 0; d < 9; ++d) {
-            yo[h][d] = min(max(fy + d - 4, 0), 11) * 12;
-            xo[h][d] = min(max(fx + d - 4, 0), 11);
-        }
+    for (int i = tid; i < TE_W_FLOATS; i += TE_THREADS) {
+        const int dx = i % TE_WROW, o = (i / TE_WROW) % 3, dy = (i / (3 * TE_WROW)) % 9, c = i / (27 * TE_WROW);
+        Wt[i] = dx < 9 ? __ldg(w + (o * 64 + c) * 81 + dy * 9 + dx) : 0.f;
     }
-    for (int ck = 0; ck < 8; ++ck) {
-        __syncthreads();   // U staged / previous chunk's weights consumed
-        for (int i = threadIdx.x; i < 3 * 8 * 81; i += blockDim.x) {
-            const int oo = i / (8 * 81), rem = i - oo * 8 * 81;
-            Wt[i] = __ldg(w + (oo * 64 + 8 * ck) * 81 + rem);
+    const int g = tid >> 3, slot = tid & 7;   // channels 2g, 2g + 1; strip slot
+    const int n = P.npos, last = n - 1;
+    for (int e = blockIdx.x; e < nedge; e += gridDim.x) {
+        int wi, wj;
+        if (n == 1) { wi = 0; wj = 0; }
+        else if (e < n) { wi = 0; wj = e; }
+        else if (e < 2 * n) { wi = n - 1; wj = e - n; }
+        else { wi = 1 + (e - 2 * n) / 2; wj = ((e - 2 * n) & 1) ? n - 1 : 0; }
+        __syncthreads();   // previous window's U / partials consumed (and the weights staged)
+        const uint16_t *src = P.edge_u + size_t(e) * 36 * 256;
+        for (int i = tid; i < 36 * 256; i += TE_THREADS) {
+            const int pp = i >> 8, oc = i & 255, c = oc >> 2, ii = (oc >> 1) & 1, jj = oc & 1;
+            const int Y = 2 * (pp / 6) + ii, X = 2 * (pp % 6) + jj;
+            U[(c * TE_PAD + Y + 4) * TE_PAD + X + 4] = op_lo<F16>(uint32_t(src[i]));
         }
         __syncthreads();
+        // replicate padding: rows first (interior columns), then whole columns
+        for (int i = tid; i < 64 * 8 * 12; i += TE_THREADS) {
+            const int c = i / 96, r = (i / 12) % 8, x = i % 12;
+            const int Y = r < 4 ? r : 16 + (r - 4), ys = r < 4 ? 4 : 15;
+            U[(c * TE_PAD + Y) * TE_PAD + x + 4] = U[(c * TE_PAD + ys) * TE_PAD + x + 4];
+        }
+        __syncthreads();
+        for (int i = tid; i < 64 * TE_PAD * 8; i += TE_THREADS) {
+            const int c = i / (TE_PAD * 8), Y = (i / 8) % TE_PAD, k = i % 8;
+            const int X = k < 4 ? k : 16 + (k - 4), xs = k < 4 ? 4 : 15;
+            U[(c * TE_PAD + Y) * TE_PAD + X] = U[(c * TE_PAD + Y) * TE_PAD + xs];
+        }
+        __syncthreads();
+        const int lo_i = wi == 0 ? 0 : 2, hi_i = wi == last ? 6 : 4, lo_j = wj == 0 ? 0 : 2, hi_j = wj == last ? 6 : 4;
+        const int wk = 2 * (hi_j - lo_j), nstrip = 2 * (hi_i - lo_i) * (wk / 4);   // <= 36 strips of 4 px
+        for (int s0 = 0; s0 < nstrip; s0 += 8) {
+            const int sidx = s0 + slot;
+            float acc[4][3];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            if (!act[h]) continue;
-            for (int c = 0; c < 8; ++c) {
-                const float *uc = U + (8 * ck + c) * 144;
-                const float *wc = Wt + (wo[h] * 8 + c) * 81;
+            for (int k = 0; k < 4; ++k)
 #pragma unroll
-                for (int dy = 0; dy < 9; ++dy)
+                for (int o = 0; o < 3; ++o) acc[k][o] = 0.f;
+            if (sidx < nstrip) {
+                const int fy = 2 * lo_i + sidx / (wk / 4), fx0 = 2 * lo_j + 4 * (sidx % (wk / 4));
+#pragma unroll 1
+                for (int cc = 0; cc < 2; ++cc) {
+                    const int c = 2 * g + cc;
+#pragma unroll 1
+                    for (int dy = 0; dy < 9; ++dy) {
+                        float u[12], wv[3][12];
+                        const float4 *ur = reinterpret_cast<const float4 *>(U + (c * TE_PAD + fy + dy) * TE_PAD + fx0);
 #pragma unroll
-                    for (int dx = 0; dx < 9; ++dx) acc[h] = fmaf(uc[yo[h][dy] + xo[h][dx]], wc[dy * 9 + dx], acc[h]);
+                        for (int q = 0; q < 3; ++q) {
+                            const float4 t4 = ur[q];
+                            u[4 * q] = t4.x; u[4 * q + 1] = t4.y; u[4 * q + 2] = t4.z; u[4 * q + 3] = t4.w;
+                        }
+                        const float4 *wr = reinterpret_cast<const float4 *>(Wt + ((c * 9 + dy) * 3) * TE_WROW);
+#pragma unroll
+                        for (int o = 0; o < 3; ++o)
+#pragma unroll
+                            for (int q = 0; q < 3; ++q) {
+                                const float4 t4 = wr[o * 3 + q];
+                                wv[o][4 * q] = t4.x; wv[o][4 * q + 1] = t4.y; wv[o][4 * q + 2] = t4.z; wv[o][4 * q + 3] = t4.w;
+                            }
+#pragma unroll
+                        for (int dx = 0; dx < 9; ++dx)
+#pragma unroll
+                            for (int k = 0; k < 4; ++k)
+#pragma unroll
+                                for (int o = 0; o < 3; ++o) acc[k][o] = fmaf(u[k + dx], wv[o][dx], acc[k][o]);
+                    }
+                }
             }
-        }
-    }
 #pragma unroll
-    for (int h = 0; h < 2; ++h)
-        if (act[h]) part[threadIdx.x + h * blockDim.x] = acc[h];
-    __syncthreads();
-    for (int i = threadIdx.x; i < npix; i += blockDim.x) {
-        const int gy = 2 * lo_i + i / wk, gx = 2 * lo_j + i % wk;
-        double m = 0.0;
-        for (int oo = 0; oo < 3; ++oo) {
-            const float pre = part[i * 3 + oo] + __ldg(bias + oo);
-            m += double(P.tanh_s * tanhf(pre / P.tanh_s));
+            for (int k = 0; k < 4; ++k)
+#pragma unroll
+                for (int o = 0; o < 3; ++o) red[(g * 8 + slot) * 12 + k * 3 + o] = acc[k][o];
+            __syncthreads();
+            if (tid < 8 * 12) {
+                const int sl = tid / 12, ko = tid % 12, sidx2 = s0 + sl;
+                float sum = 0.f;
+                for (int gg = 0; gg < 32; ++gg) sum += red[(gg * 8 + sl) * 12 + ko];
+                red[32 * 8 * 12 - 8 * 12 + tid] = sum;   // reuse the last group's row for the totals
+                (void)sidx2;
+            }
+            __syncthreads();
+            if (tid < 8 * 4) {
+                const int sl = tid >> 2, k = tid & 3, sidx2 = s0 + sl;
+                if (sidx2 < nstrip) {
+                    const int fy = 2 * lo_i + sidx2 / (wk / 4), fx = 2 * lo_j + 4 * (sidx2 % (wk / 4)) + k;
+                    double m = 0.0;
+#pragma unroll
+                    for (int o = 0; o < 3; ++o) {
+                        const float pre = red[32 * 8 * 12 - 8 * 12 + sl * 12 + k * 3 + o] + __ldg(bias + o);
+                        m += double(P.tanh_s * tanhf(pre / P.tanh_s));
+                    }
+                    m = m / 3.0;
+                    P.fine[(long long)(2 * (2 * wi) + fy) * P.nf + 2 * (2 * wj) + fx] = denormalize_q(m, P.log_lo, P.span);
+                }
+            }
+            __syncthreads();
         }
-        m = m / 3.0;
-        P.fine[(long long)(2 * (2 * wi) + gy) * P.nf + 2 * (2 * wj) + gx] = denormalize_q(m, P.log_lo, P.span);
     }
 }
 
@@ -1292,8 +1338,18 @@ int launch_sr_pass_tc_dbg(const mgsr_gen *g, const double *c, const double *c_sh
     const int pairs = ngp < mp ? ngp : mp;
     cfg.gridDim = dim3(2 * pairs);
     MGSR_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, P));
-    if (f16) k_tail_edge<true><<<edge_count(P.npos), 256, 0, st>>>(P);
-    else k_tail_edge<false><<<edge_count(P.npos), 256, 0, st>>>(P);
+    {
+        const int ne = edge_count(P.npos);
+        static bool te_attr = false;
+        if (!te_attr) {
+            MGSR_CUDA_TRY(cudaFuncSetAttribute(k_tail_edge<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(TE_SMEM)));
+            MGSR_CUDA_TRY(cudaFuncSetAttribute(k_tail_edge<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(TE_SMEM)));
+            te_attr = true;
+        }
+        const int nb = ne < nsm ? ne : nsm;
+        if (f16) k_tail_edge<true><<<nb, TE_THREADS, TE_SMEM, st>>>(P, ne);
+        else k_tail_edge<false><<<nb, TE_THREADS, TE_SMEM, st>>>(P, ne);
+    }
     MGSR_LAUNCH_CHECK();
     return MGSR_OK;
 }
