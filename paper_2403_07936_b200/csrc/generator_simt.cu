@@ -97,9 +97,131 @@ __global__ void __launch_bounds__(kConvThreads) k_conv_simt(const float *__restr
     }
 }
 
+// Register-tiled form: CTA = (NW windows, a block of OB <= 16 output channels); thread = one
+// pixel (or MAXP pixels when a window has more than 256) of one window, accumulating all OB
+// channels, so each staged input value feeds OB FMAs and the block's weights ([c][tap][oc] in
+// shared memory, read as float4 broadcasts) feed every pixel.  Per output the accumulation order
+// (c ascending, dy, dx, fmaf) is k_conv_simt's, so results are bitwise identical.
+constexpr int kConv2Threads = 256, kConv2OB = 16, kConv2CC = 16;
+
+template <int K, int MAXP, int OP>
+__global__ void __launch_bounds__(kConv2Threads) k_conv_rt(const float *__restrict__ in, int N, int C, int H,
+                                                          const float *__restrict__ w, int O,
+                                                          float *__restrict__ out, Epi ep, int nw) {
+    extern __shared__ __align__(16) float sm2[];
+    constexpr int P = K / 2, KK = K * K;
+    const int HW = H * H, HP = H + K - 1, HP2 = HP * HP;
+    const int n0 = blockIdx.x * nw, ob = blockIdx.y * kConv2OB;
+    const int OBn = min(kConv2OB, O - ob);
+    float *s_w = sm2;                                   // [cc][KK][16]
+    float *s_in = sm2 + kConv2CC * KK * kConv2OB;       // [nw][cc][HP][HP]
+    const int tid = threadIdx.x;
+    float acc[MAXP][kConv2OB];
+#pragma unroll
+    for (int k = 0; k < MAXP; ++k)
+#pragma unroll
+        for (int o = 0; o < kConv2OB; ++o) acc[k][o] = 0.f;
+    int wl[MAXP], py[MAXP], px[MAXP];
+    bool act[MAXP];
+#pragma unroll
+    for (int k = 0; k < MAXP; ++k) {
+        const int slot = tid + k * kConv2Threads;
+        wl[k] = slot / HW;
+        const int pix = slot - wl[k] * HW;
+        py[k] = pix / H;
+        px[k] = pix - py[k] * H;
+        act[k] = wl[k] < nw && n0 + wl[k] < N;
+    }
+    for (int c0 = 0; c0 < C; c0 += kConv2CC) {
+        const int cc = min(kConv2CC, C - c0);
+        __syncthreads();
+        for (int idx = tid; idx < nw * cc * HP2; idx += kConv2Threads) {
+            const int wi = idx / (cc * HP2), r0 = idx - wi * cc * HP2, c = r0 / HP2, r = r0 - c * HP2;
+            const int yy = min(max(r / HP - P, 0), H - 1), xx = min(max(r % HP - P, 0), H - 1);
+            const int n = n0 + wi;
+            s_in[idx] = n < N ? in[((int64_t(n) * C + c0 + c) * H + yy) * H + xx] : 0.f;
+        }
+        for (int idx = tid; idx < cc * KK * kConv2OB; idx += kConv2Threads) {
+            const int o = idx % kConv2OB, t = (idx / kConv2OB) % KK, c = idx / (kConv2OB * KK);
+            s_w[idx] = o < OBn ? __ldg(w + (int64_t(ob + o) * C + c0 + c) * KK + t) : 0.f;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < MAXP; ++k) {
+            if (!act[k]) continue;
+            for (int c = 0; c < cc; ++c) {
+                const float *si = s_in + ((wl[k] * cc + c) * HP + py[k]) * HP + px[k];
+                const float4 *wc = reinterpret_cast<const float4 *>(s_w + c * KK * kConv2OB);
+#pragma unroll
+                for (int dy = 0; dy < K; ++dy)
+#pragma unroll
+                    for (int dx = 0; dx < K; ++dx) {
+                        const float v = si[dy * HP + dx];
+                        const float4 *wt = wc + (dy * K + dx) * (kConv2OB / 4);
+#pragma unroll
+                        for (int q = 0; q < kConv2OB / 4; ++q) {
+                            const float4 w4 = wt[q];
+                            acc[k][4 * q] = fmaf(v, w4.x, acc[k][4 * q]);
+                            acc[k][4 * q + 1] = fmaf(v, w4.y, acc[k][4 * q + 1]);
+                            acc[k][4 * q + 2] = fmaf(v, w4.z, acc[k][4 * q + 2]);
+                            acc[k][4 * q + 3] = fmaf(v, w4.w, acc[k][4 * q + 3]);
+                        }
+                    }
+            }
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < MAXP; ++k) {
+        if (!act[k]) continue;
+        const int n = n0 + wl[k], pix = py[k] * H + px[k], y = py[k], x = px[k];
+#pragma unroll
+        for (int oo = 0; oo < kConv2OB; ++oo) {
+            if (oo >= OBn) break;
+            const int o = ob + oo;
+            float v = acc[k][oo];
+            if (OP == OP_PRELU) {
+                out[(int64_t(n) * O + o) * HW + pix] = v > 0.f ? v : ep.alpha[o] * v;
+            } else if (OP == OP_BN_PRELU) {
+                v = fmaf(v, ep.scale[o], ep.shift[o]);
+                out[(int64_t(n) * O + o) * HW + pix] = v > 0.f ? v : ep.alpha[o] * v;
+            } else if (OP == OP_BN_RES) {
+                const int64_t oi = (int64_t(n) * O + o) * HW + pix;
+                out[oi] = ep.res[oi] + fmaf(v, ep.scale[o], ep.shift[o]);
+            } else if (OP == OP_SHUF_PRELU) {
+                const int c = o >> 2, i = (o >> 1) & 1, j = o & 1, W2 = 2 * H;
+                v = v > 0.f ? v : ep.alpha[c] * v;
+                out[((int64_t(n) * (O >> 2) + c) * W2 + 2 * y + i) * W2 + 2 * x + j] = v;
+            } else {
+                const float sc = ep.tanh_s;
+                out[(int64_t(n) * O + o) * HW + pix] = sc * tanhf((v + ep.bias[o]) / sc);
+            }
+        }
+    }
+}
+
 template <int K, int OP>
 static int conv(const float *in, int N, int C, int H, const float *w, int O, float *out, const Epi &ep,
                 cudaStream_t st) {
+    {
+        const int HW = H * H, HP = H + K - 1;
+        const int nw = HW <= kConv2Threads ? kConv2Threads / HW : 1;
+        const int per = (HW + kConv2Threads - 1) / kConv2Threads;
+        const size_t smem = sizeof(float) * (size_t(kConv2CC) * K * K * kConv2OB + size_t(nw) * kConv2CC * HP * HP);
+        if (per <= 3 && smem <= 200 * 1024) {
+            dim3 grid((N + nw - 1) / nw, (O + kConv2OB - 1) / kConv2OB);
+            if (per == 1) {
+                auto kern = k_conv_rt<K, 1, OP>;
+                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+                kern<<<grid, kConv2Threads, smem, st>>>(in, N, C, H, w, O, out, ep, nw);
+            } else {
+                auto kern = k_conv_rt<K, 3, OP>;
+                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+                kern<<<grid, kConv2Threads, smem, st>>>(in, N, C, H, w, O, out, ep, nw);
+            }
+            MGSR_LAUNCH_CHECK();
+            return MGSR_OK;
+        }
+    }
     const int HP = H + K - 1;
     int cc = 12288 / (HP * HP);
     if (cc > C) cc = C;
