@@ -270,151 +270,12 @@ __global__ void __launch_bounds__(kSmallThreads) k_correction_small(const double
     }
 }
 
-// Temporally blocked K-sweep GS.  A TY x TX tile plus a halo of H cells is
-// staged in shared memory; 2K half-sweeps run there (the invalid outer ring
-// grows by one cell per half-sweep and never reaches the interior +- 1), the
-// interior is written back once.  HBM traffic: read p and f once, write p
-// once for K sweeps.  With RC the residual at the coarse (even, even) points
-// of the interior is computed from the final values and written raw
-// (half-injection input, solver.py:178-179).
-//
-// Shared-memory layout: colour planes.  The tile origin is even in both
-// coordinates, so a cell's colour is (ly + lx) & 1; plane c holds the cells of
-// colour c of each row compacted (index ly * WH + lx / 2).  All four neighbours
-// of a colour-c cell live in plane 1-c at the same or adjacent index, so a
-// warp's accesses are unit-stride and conflict-free (the interleaved layout
-// read every other double: two wavefronts per request).
-template <int K, bool RC>
-__global__ void __launch_bounds__(kTbThreads, 3) k_gs_tb(const double *__restrict__ pin, double *__restrict__ pout,
-                                                      FSrc fs, int n, double h2, int zero_init, double inv_h2,
-                                                      double *__restrict__ rc, RedSlot slot, double *mean_out,
-                                                      double *rc_mean_out) {
-    constexpr int H = 2 * K + (RC ? 1 : 0);
-    constexpr int W = kTbTX + 2 * H, HH = kTbTY + 2 * H;
-    // plane rows padded to an even stride so a pair of same-colour cells is one 16-byte access
-    constexpr int WH = W / 2, WP = (WH + 1) & ~1, PL = WP * HH, NPR = WP / 2;
-    static_assert(W % 2 == 0, "tile width must be even");
-    extern __shared__ double sm[];
-    double *const sp = sm;            // planes 0,1 of p
-    double *const sf = sm + 2 * PL;   // planes 0,1 of f
-    const int tid = threadIdx.x;
-    const double sh = fs.load_shift();
-    const int tiles_x = n / kTbTX, ntiles = tiles_x * (n / kTbTY);
-    constexpr int NE = W * HH, PER = (NE + kTbThreads - 1) / kTbThreads;
-    double v[2] = {0.0, 0.0};     // grid sum of the new iterate, of the coarse residual
-    // Persistent: the block walks tiles blockIdx.x, +gridDim.x, ... (row-major, so
-    // concurrently resident blocks share halos in L2) and reduces once at the end.
-#pragma unroll 1
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int by = tile / tiles_x, bx = tile - by * tiles_x;
-        const int gx0 = bx * kTbTX - H, gy0 = by * kTbTY - H;
-        const bool inner = gx0 >= 0 && gy0 >= 0 && gx0 + W <= n && gy0 + HH <= n;
-        // Stage tile + halo: all loads of a thread are issued before any shared
-        // store (the staging is latency-bound otherwise).
-        __syncthreads();   // previous tile's reads of shared memory are done
-        double rp[PER], rf[PER];
-        if (inner) {   // interior tile: no periodic wrap (the common case)
-            const int64_t org = int64_t(gy0) * n + gx0;
-#pragma unroll
-            for (int u = 0; u < PER; ++u) {
-                const int idx = tid + u * kTbThreads;
-                rp[u] = 0.0;
-                rf[u] = 0.0;
-                if (idx < NE) {
-                    const int ly = idx / W, lx = idx - ly * W;
-                    const int64_t g = org + int64_t(ly) * n + lx;
-                    if (!zero_init) rp[u] = __ldg(pin + g);
-                    rf[u] = fs.at(g, sh);
-                }
-            }
-        } else {
-#pragma unroll
-            for (int u = 0; u < PER; ++u) {
-                const int idx = tid + u * kTbThreads;
-                rp[u] = 0.0;
-                rf[u] = 0.0;
-                if (idx < NE) {
-                    const int ly = idx / W, lx = idx - ly * W;
-                    const int64_t g = int64_t(wrap(gy0 + ly, n)) * n + wrap(gx0 + lx, n);
-                    if (!zero_init) rp[u] = __ldg(pin + g);
-                    rf[u] = fs.at(g, sh);
-                }
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < PER; ++u) {
-            const int idx = tid + u * kTbThreads;
-            if (idx < NE) {
-                const int ly = idx / W, lx = idx - ly * W;
-                const int o = ((ly + lx) & 1) * PL + ly * WP + (lx >> 1);
-                sp[o] = rp[u];
-                sf[o] = rf[u];
-            }
-        }
-        __syncthreads();
-        // half-sweep hs updates colour hs & 1 (red = (i + j) even first) on rows
-        // [1 + hs, HH - 2 - hs]: only cells at distance >= hs + 1 from the tile
-        // edge can still be exact, and only those are needed later.
-#pragma unroll 1
-        for (int hs = 0; hs < 2 * K; ++hs) {
-            const int c = hs & 1;
-            double *const pc = sp + c * PL;
-            const double *const po = sp + (1 - c) * PL;
-            const double *const fc = sf + c * PL;
-            const int r0 = 1 + hs, nrows = HH - 2 - 2 * hs;
-            // pairs of same-colour cells k = 2m, 2m + 1 (lx = 2k + par); the pairs also update the tile's
-            // edge columns and the pad slot, which only feed cells that are invalid already
-            for (int idx = tid; idx < nrows * NPR; idx += kTbThreads) {
-                const int rr = idx / NPR;
-                const int ly = r0 + rr;
-                const int par = (c + ly) & 1;              // lx parity of colour-c cells in this row
-                const int o = ly * WP + 2 * (idx - rr * NPR);
-                const double2 up = *reinterpret_cast<const double2 *>(po + o - WP);
-                const double2 dn = *reinterpret_cast<const double2 *>(po + o + WP);
-                const double2 mid = *reinterpret_cast<const double2 *>(po + o);
-                const double2 ff = *reinterpret_cast<const double2 *>(fc + o);
-                double l0, r0v, l1, r1;
-                if (par) {
-                    const double e2 = po[o + 2];
-                    l0 = mid.x; r0v = mid.y; l1 = mid.y; r1 = e2;
-                } else {
-                    const double em = po[o - 1];
-                    l0 = em; r0v = mid.x; l1 = mid.x; r1 = mid.y;
-                }
-                const double nb0 = ((up.x + dn.x) + l0) + r0v;
-                const double nb1 = ((up.y + dn.y) + l1) + r1;
-                *reinterpret_cast<double2 *>(pc + o) = make_double2((nb0 - h2 * ff.x) * 0.25, (nb1 - h2 * ff.y) * 0.25);
-            }
-            __syncthreads();
-        }
-        for (int idx = tid; idx < kTbTX * kTbTY; idx += kTbThreads) {
-            const int iy = idx / kTbTX, ix = idx - iy * kTbTX;
-            const int gi = gy0 + H + iy, gj = gx0 + H + ix;
-            const int ly = iy + H, lx = ix + H;
-            const int c = (ly + lx) & 1;
-            const int o = ly * WP + (lx >> 1);
-            const double val = sp[c * PL + o];
-            pout[int64_t(gi) * n + gj] = val;
-            v[0] += val;
-            if (RC && !(gi & 1) && !(gj & 1)) {
-                // (even, even) cell: colour 0; its neighbours are in plane 1
-                const double *po = sp + PL;
-                const int par = lx & 1;
-                double nb = ((po[o - WP] + po[o + WP]) + po[o - 1 + par]) + po[o + par];
-                double res = sf[o] - ((nb - 4.0 * val) * inv_h2);
-                rc[int64_t(gi >> 1) * (n >> 1) + (gj >> 1)] = res;
-                v[1] += res;
-            }
-        }
-    }
-    double *const outs[2] = {mean_out, RC ? rc_mean_out : nullptr};
-    const double scales[2] = {1.0 / (double(n) * double(n)), 4.0 / (double(n) * double(n))};
-    grid_reduce_to<2>(v, slot, outs, scales);
-}
-
 // ---------------------------------------------------------------------------
-// Register-blocked, TMA-fed K-sweep GS (the large levels).  Same arithmetic and
-// outputs as k_gs_tb; different data movement:
+// Temporally blocked K-sweep GS on the large levels (side >= 128): 2K half-sweeps on a
+// window of the grid whose halo (HE >= 2K, +1 when the residual is fused) keeps the
+// interior exact; HBM traffic is read p, f and write p once per K sweeps.  With RC the
+// residual at the coarse (even, even) interior points is computed from the final values and
+// written raw (half-injection input, solver.py:178-179).  Data movement:
 //   * a 64 x 64 window (tile interior + an even halo HE >= 2K (+1 with RC)) of
 //     p and f lands in shared memory by per-row cp.async.bulk copies (rows and
 //     the column wrap of edge tiles split into <= 2 segments per row), tracked
@@ -431,7 +292,7 @@ __global__ void __launch_bounds__(kTbThreads, 3) k_gs_tb(const double *__restric
 //   * interior written with 16-byte stores; tiles of the last row/column are
 //     shifted inwards (x0 = n - TX) rather than masked: they recompute cells
 //     of their neighbour bit for bit and only count their own cells in the sums.
-constexpr int kRbW = 64, kRbRows = 8, kRbWarps = 8, kRbThreads = 32 * kRbWarps, kRbMinN = 128;
+constexpr int kRbW = 64, kRbRows = 8, kRbWarps = 8, kRbThreads = 32 * kRbWarps, kRbMinN = 128, kRbMaxK = 4;
 
 __device__ __forceinline__ void rb_mbar_wait(uint32_t bar, uint32_t parity) {
     asm volatile(
@@ -1124,28 +985,21 @@ int launch_gs(const double *p_in, double *p_out, double *tmp, FSrc fs, int n, do
         }
         return MGSR_OK;
     }
-    // register-blocked TMA kernel for the large levels (MGSR_GS_TB=1 selects the shared-memory tiles)
-    static const bool force_tb = std::getenv("MGSR_GS_TB") != nullptr;
-    const bool use_rb = n >= kRbMinN && n % 2 == 0 && !force_tb;
-    if ((use_rb || (n % kTbTX == 0 && n % kTbTY == 0)) && sweeps >= 1 && p_in != p_out) {
-        const int chunks = (sweeps + kTbMaxK - 1) / kTbMaxK;
+    if (n >= kRbMinN && sweeps >= 1 && p_in != p_out) {
+        const int chunks = (sweeps + kRbMaxK - 1) / kRbMaxK;
         if (chunks > 1 && !tmp) { set_error("gs: chunked sweeps need a scratch buffer"); return MGSR_E_BAD_ARG; }
         int done = 0;
         const double *src = p_in;
         for (int ci = 0; ci < chunks; ++ci) {
             int k = sweeps - done;
-            if (k > kTbMaxK) k = kTbMaxK;
+            if (k > kRbMaxK) k = kRbMaxK;
             const bool last = ci == chunks - 1;
             const bool rcl = last && rc;
             double *dst = ((chunks - 1 - ci) % 2 == 0) ? p_out : tmp;
             const int zi = (ci == 0) ? zero_init : 0;
-            const int ntiles = (n / kTbTX) * (n / kTbTY);
-            const int H = 2 * k + (rcl ? 1 : 0);
-            const int wp = (((kTbTX + 2 * H) / 2) + 1) & ~1;   // padded plane row (see k_gs_tb)
-            size_t smem = 4 * sizeof(double) * size_t(wp) * (kTbTY + 2 * H);
             double *mo = last ? mean_out : nullptr;
-#define MGSR_TB_LAUNCH(KK, RCV, RCP, RCM)                                                                  \
-    if (use_rb) {                                                                                          \
+#define MGSR_RB_LAUNCH(KK, RCV, RCP, RCM)                                                                  \
+    {                                                                                                      \
         auto kern = k_gs_rb<KK, RCV>;                                                                      \
         constexpr int HE = (2 * KK + (RCV ? 1 : 0) + 1) & ~1, TX = kRbW - 2 * HE;                          \
         const int tl = ((n + TX - 1) / TX) * ((n + TX - 1) / TX);                                          \
@@ -1158,28 +1012,20 @@ int launch_gs(const double *p_in, double *p_out, double *tmp, FSrc fs, int n, do
         CUtensorMap tmp_, tmf_;                                                                            \
         if (make_tmap_2d(&tmp_, src ? src : fs.f, n) || make_tmap_2d(&tmf_, fs.f, n)) return MGSR_E_CUDA; \
         kern<<<blocks, kRbThreads, rsm, st>>>(tmp_, tmf_, src, dst, fs, n, h2, zi, inv_h2, RCP, s0, mo, RCM); \
-    } else {                                                                                               \
-        auto kern = k_gs_tb<KK, RCV>;                                                                      \
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));                \
-        int occ = 0;                                                                                       \
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kTbThreads, smem);                       \
-        int blocks = num_sms() * (occ > 0 ? occ : 1);                                                      \
-        if (blocks > ntiles) blocks = ntiles;                                                              \
-        kern<<<blocks, kTbThreads, smem, st>>>(src, dst, fs, n, h2, zi, inv_h2, RCP, s0, mo, RCM);         \
     }
-#define MGSR_TB_CASE(KK)                                                                                   \
+#define MGSR_RB_CASE(KK)                                                                                   \
     case KK:                                                                                               \
-        if (rcl) MGSR_TB_LAUNCH(KK, true, rc, rc_mean)                                                     \
-        else MGSR_TB_LAUNCH(KK, false, nullptr, nullptr)                                                   \
+        if (rcl) MGSR_RB_LAUNCH(KK, true, rc, rc_mean)                                                     \
+        else MGSR_RB_LAUNCH(KK, false, nullptr, nullptr)                                                   \
         break;
             switch (k) {
-                MGSR_TB_CASE(1)
-                MGSR_TB_CASE(2)
-                MGSR_TB_CASE(3)
-                MGSR_TB_CASE(4)
+                MGSR_RB_CASE(1)
+                MGSR_RB_CASE(2)
+                MGSR_RB_CASE(3)
+                MGSR_RB_CASE(4)
             }
-#undef MGSR_TB_CASE
-#undef MGSR_TB_LAUNCH
+#undef MGSR_RB_CASE
+#undef MGSR_RB_LAUNCH
             MGSR_LAUNCH_CHECK();
             done += k;
             src = dst;

@@ -4,7 +4,6 @@
 
 namespace mgsr {
 
-constexpr int kTbTX = 64, kTbTY = 32, kTbThreads = 256, kTbMaxK = 4;
 constexpr int kSmallN = 64;
 
 int grid_for(int64_t work, int threads);
