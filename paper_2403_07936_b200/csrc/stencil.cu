@@ -758,6 +758,79 @@ __global__ void k_prolong2_add(const double *__restrict__ c, int nc, const doubl
     if (do_mean) grid_reduce<1>(v, slot, mean_out, 1.0 / (double(n) * double(n)));
 }
 
+// Row-marching form of k_prolong2_add (same per-output arithmetic, bitwise identical values):
+// thread = coarse column bj (fine columns 2bj, 2bj+1), a block = 256 columns x a strip of
+// coarse rows sized for one wave; the 4 x 4 coarse neighbourhood slides down one coarse row per
+// step (4 new L1 loads instead of 16), the next row's loads are issued before the current
+// 2 x 2 fine block is computed.
+__global__ void __launch_bounds__(256, 4) k_prolong2_rows(const double *__restrict__ c, int nc,
+                                                          const double *__restrict__ base, const double *bshift,
+                                                          double *__restrict__ out, RedSlot slot, double *mean_out,
+                                                          int do_mean, int rows) {
+    const int n = 2 * nc;
+    const double bsh = (base && bshift) ? *bshift : 0.0;
+    const double w0 = -0.0625, w1 = 0.5625;
+    double v[1] = {0.0};
+    const int bj = blockIdx.x * blockDim.x + threadIdx.x;
+    const int b0 = blockIdx.y * rows, b1 = min(b0 + rows, nc);
+    if (bj < nc && b0 < b1) {
+        int cb[4];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) cb[b] = wrap(bj + b - 1, nc);
+        auto crow = [&](int r, double (&dst)[4]) {
+            const double *cr = c + int64_t(wrap(r, nc)) * nc;
+#pragma unroll
+            for (int b = 0; b < 4; ++b) dst[b] = __ldg(cr + cb[b]);
+        };
+        double c0[4], c1[4], c2[4], c3[4];
+        crow(b0 - 1, c0);
+        crow(b0, c1);
+        crow(b0 + 1, c2);
+        crow(b0 + 2, c3);
+#pragma unroll 1
+        for (int bi = b0; bi < b1; ++bi) {
+            double nx[4] = {0.0, 0.0, 0.0, 0.0};
+            if (bi + 1 < b1) crow(bi + 3, nx);
+            const int64_t t0 = int64_t(2 * bi) * n + 2 * bj, t1 = t0 + n;
+            double2 b0v = make_double2(0.0, 0.0), b1v = make_double2(0.0, 0.0);
+            if (base) {
+                b0v = __ldg(reinterpret_cast<const double2 *>(base + t0));
+                b1v = __ldg(reinterpret_cast<const double2 *>(base + t1));
+            }
+            double R0[4], R1[4];
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                R0[b] = c1[b];
+                double row = 0.0;
+                row += w0 * c0[b];
+                row += w1 * c1[b];
+                row += w1 * c2[b];
+                row += w0 * c3[b];
+                R1[b] = row;
+            }
+            double a01 = 0.0, a11 = 0.0;
+            a01 += w0 * R0[0]; a01 += w1 * R0[1]; a01 += w1 * R0[2]; a01 += w0 * R0[3];
+            a11 += w0 * R1[0]; a11 += w1 * R1[1]; a11 += w1 * R1[2]; a11 += w0 * R1[3];
+            double2 y0 = make_double2(R0[1], a01), y1 = make_double2(R1[1], a11);
+            if (base) {
+                y0.x = (b0v.x - bsh) + y0.x; y0.y = (b0v.y - bsh) + y0.y;
+                y1.x = (b1v.x - bsh) + y1.x; y1.y = (b1v.y - bsh) + y1.y;
+            }
+            *reinterpret_cast<double2 *>(out + t0) = y0;
+            *reinterpret_cast<double2 *>(out + t1) = y1;
+            v[0] += ((y0.x + y0.y) + (y1.x + y1.y));
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                c0[b] = c1[b];
+                c1[b] = c2[b];
+                c2[b] = c3[b];
+                c3[b] = nx[b];
+            }
+        }
+    }
+    if (do_mean) grid_reduce<1>(v, slot, mean_out, 1.0 / (double(n) * double(n)));
+}
+
 // out = (base - *bshift) + (up - *ushift), optional grid mean of out (SR correction add,
 // solver.py:190 / 196 with srmodel.py:486's mean subtraction folded in).
 __global__ void k_add2(const double *__restrict__ base, const double *bshift, const double *__restrict__ up,
@@ -808,20 +881,19 @@ __global__ void k_finalize(const double *__restrict__ out, const double *mean_pt
 }
 
 // Row-marching form of k_finalize (same per-cell arithmetic): thread = two adjacent columns, a
-// block = 256 column pairs x kFinRows rows; the out rows above / at / below stay in registers
+// block = 256 column pairs x a strip of rows (sized for one wave); the out rows above / at / below stay in registers
 // (out is read once per cell), left / right neighbours come by shuffle (lanes 0 / 31 load theirs),
 // the next row's loads are issued before the current row is computed.  The last block also
 // writes stats (k_stats_sqrt folded in).  n % 64 == 0.
-constexpr int kFinRows = 32;
-__global__ void __launch_bounds__(256) k_finalize_rows(const double *__restrict__ out, const double *mean_ptr,
+__global__ void __launch_bounds__(256, 4) k_finalize_rows(const double *__restrict__ out, const double *mean_ptr,
                                                        double *__restrict__ p, FSrc fs, int n, double inv_h2,
-                                                       RedSlot slot, double *acc_out, double *stats) {
+                                                       RedSlot slot, double *acc_out, double *stats, int rows) {
     const int lane = threadIdx.x & 31;
     const int pj = blockIdx.x * blockDim.x + threadIdx.x;
     const bool active = 2 * pj < n;   // whole warps (n / 2 is a multiple of 32)
     const int c0 = 2 * pj;
     const int cl = c0 == 0 ? n - 1 : c0 - 1, cr = c0 + 2 >= n ? c0 + 2 - n : c0 + 2;
-    const int r0 = blockIdx.y * kFinRows, r1 = min(r0 + kFinRows, n);
+    const int r0 = blockIdx.y * rows, r1 = min(r0 + rows, n);
     const double m = *mean_ptr;
     const double sh = fs.load_shift();
     const bool shifted = fs.shift != nullptr;
@@ -1057,6 +1129,16 @@ int launch_gs(const double *p_in, double *p_out, double *tmp, FSrc fs, int n, do
 int launch_prolong_add(const double *c, int nc, int s, const double *base, const double *bshift, double *out,
                        double *mean_out, void *red_slot, cudaStream_t st) {
     RedSlot sl = red_slot_at(red_slot);
+    if (s == 2 && nc >= 512) {
+        const int gx = (nc + 255) / 256;
+        int strips = (4 * num_sms()) / gx;
+        strips = strips < 1 ? 1 : (strips > nc ? nc : strips);
+        const int rows = (nc + strips - 1) / strips;
+        const dim3 g(gx, (nc + rows - 1) / rows);
+        k_prolong2_rows<<<g, 256, 0, st>>>(c, nc, base, bshift, out, sl, mean_out, mean_out != nullptr, rows);
+        MGSR_LAUNCH_CHECK();
+        return MGSR_OK;
+    }
     if (s == 2) {
         k_prolong2_add<<<grid_2d(nc, nc), 256, 0, st>>>(c, nc, base, bshift, out, sl, mean_out, mean_out != nullptr);
         MGSR_LAUNCH_CHECK();
@@ -1102,9 +1184,14 @@ int launch_finalize(const double *out, const double *mean_ptr, double *p, FSrc f
                     double *stats2, void *red_slot, cudaStream_t st) {
     RedSlot sl = red_slot_at(red_slot);
     double h = 2.0 * M_PI / n;
-    const dim3 g((n / 2 + 255) / 256, (n + kFinRows - 1) / kFinRows);
+    // one wave: 4 CTAs per SM (the kernel's occupancy), the row strips sized to fill it
+    const int gx = (n / 2 + 255) / 256;
+    int strips = (4 * num_sms()) / gx;
+    strips = strips < 1 ? 1 : (strips > n ? n : strips);
+    const int rows = (n + strips - 1) / strips;
+    const dim3 g(gx, (n + rows - 1) / rows);
     if (n % 64 == 0 && int64_t(g.x) * g.y <= kRedMaxBlocks) {
-        k_finalize_rows<<<g, 256, 0, st>>>(out, mean_ptr, p, fs, n, 1.0 / (h * h), sl, acc3, stats2);
+        k_finalize_rows<<<g, 256, 0, st>>>(out, mean_ptr, p, fs, n, 1.0 / (h * h), sl, acc3, stats2, rows);
         MGSR_LAUNCH_CHECK();
         return MGSR_OK;
     }
