@@ -158,6 +158,19 @@ int record_vcycle(mgsr_plan *pl, double *p, const double *f, int use_sr, cudaStr
     FSrc fs{f, nullptr, 1.0};
     const bool mk = pl->capturing_markers;
     if (mk) MGSR_CUDA_TRY(cudaEventRecordWithFlags(pl->cap_ev[4], st, cudaEventRecordExternal));
+    const int L = int(pl->sides.size());
+    bool tiny = n <= kSmallN && L >= 2 && L <= 8 && !std::getenv("MGSR_NO_FUSED_SMALL");
+    for (int j = 0; tiny && j < L - 1; ++j) {
+        if (pl->sides[j] != 2 * pl->sides[j + 1]) tiny = false;
+        if (use_sr && ((pl->cfg.sr_level_mask >> j) & 1u)) tiny = false;
+    }
+    if (tiny) {   // the whole spline cycle + logging pass of a small grid in one CTA
+        int r = launch_vcycle_small(p, f, pl->sides.data(), L, pl->cfg.n_smooth, pl->cfg.coarse_sweeps,
+                                    sc(pl, SC_STATS), st);
+        if (r) return r;
+        if (mk) MGSR_CUDA_TRY(cudaEventRecordWithFlags(pl->cap_ev[5], st, cudaEventRecordExternal));
+        return MGSR_OK;
+    }
     if (mk) MGSR_CUDA_TRY(cudaEventRecordWithFlags(pl->cap_ev[2], st, cudaEventRecordExternal));
     int r = launch_gs(p, pl->S, pl->tmp, fs, n, h * h, pl->cfg.n_smooth, 0, s0 == 2 ? pl->rc[1] : nullptr,
                       s0 == 2 ? rc_mean(pl, 1) : nullptr, sc(pl, SC_S_MEAN), pl->red, st);

@@ -150,6 +150,116 @@ __device__ double block_sum_1024(double v, double *sred) {
     return sred[32];
 }
 
+// GS sweeps from the current contents of sp with the exact per-sweep mean subtraction
+// (_stencil.pyx:25-45), whole grid in one CTA's shared memory.
+__device__ void small_gs(double *sp, const double *sf, int n, int sweeps, double *sred) {
+    const int tid = threadIdx.x, nt = blockDim.x, nn = n * n, half = nn >> 1;
+    const double h = 2.0 * M_PI / n, h2 = h * h;
+    const int hn = n >> 1, hsh = pow2_shift(hn);
+    for (int s = 0; s < sweeps; ++s) {
+        for (int color = 0; color < 2; ++color) {
+            for (int t = tid; t < half; t += nt) {
+                int i, k;
+                split_idx(t, hn, hsh, i, k);
+                int jj = 2 * k + ((i + color) & 1);
+                int im1 = i > 0 ? i - 1 : n - 1, ip1 = i < n - 1 ? i + 1 : 0;
+                int jm1 = jj > 0 ? jj - 1 : n - 1, jp1 = jj < n - 1 ? jj + 1 : 0;
+                double nb = ((sp[im1 * n + jj] + sp[ip1 * n + jj]) + sp[i * n + jm1]) + sp[i * n + jp1];
+                sp[i * n + jj] = (nb - h2 * sf[i * n + jj]) * 0.25;
+            }
+            __syncthreads();
+        }
+        double acc = 0.0;
+        for (int c = tid; c < nn; c += nt) acc += sp[c];
+        const double mean = block_sum_1024(acc, sred) * (1.0 / double(nn));
+        for (int c = tid; c < nn; c += nt) sp[c] -= mean;
+        __syncthreads();
+    }
+}
+
+// Raw residual f - L p at the injected (even, even) points of an n-grid -> fr (n/2 x n/2); returns
+// the mean (block sum).  Arithmetic of k_res_restrict / the fused residual of k_gs_rb.
+__device__ double small_residual_inject(const double *sp, const double *sf, int n, double *fr, double *sred) {
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const double h = 2.0 * M_PI / n, inv_h2 = 1.0 / (h * h);
+    const int nc = n >> 1, ncc = nc * nc, csh = pow2_shift(nc);
+    double acc = 0.0;
+    for (int t = tid; t < ncc; t += nt) {
+        int ic, jc;
+        split_idx(t, nc, csh, ic, jc);
+        const int i = 2 * ic, jj = 2 * jc;
+        const int im1 = i > 0 ? i - 1 : n - 1, ip1 = i < n - 1 ? i + 1 : 0;
+        const int jm1 = jj > 0 ? jj - 1 : n - 1, jp1 = jj < n - 1 ? jj + 1 : 0;
+        const int c = i * n + jj;
+        double nb = ((sp[im1 * n + jj] + sp[ip1 * n + jj]) + sp[i * n + jm1]) + sp[i * n + jp1];
+        const double res = sf[c] - ((nb - 4.0 * sp[c]) * inv_h2);
+        fr[t] = res;
+        acc += res;
+    }
+    return block_sum_1024(acc, sred) * (1.0 / double(ncc));
+}
+
+// out (2nc x 2nc) += Keys ratio-2 prolongation of c (k_prolong2_add arithmetic, base shift 0)
+__device__ void small_prolong2_add(const double *c, int nc, double *out) {
+    const int tid = threadIdx.x, nt = blockDim.x, n = 2 * nc;
+    const double w0 = -0.0625, w1 = 0.5625;
+    const int csh = pow2_shift(nc);
+    for (int t = tid; t < nc * nc; t += nt) {
+        int bi, bj;
+        split_idx(t, nc, csh, bi, bj);
+        int ri[4];
+#pragma unroll
+        for (int o = 0; o < 4; ++o) {
+            const int r = bi + o - 1;
+            ri[o] = r < 0 ? r + nc : (r >= nc ? r - nc : r);
+        }
+        double R0[4], R1[4];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            int cb = bj + b - 1;
+            cb = cb < 0 ? cb + nc : (cb >= nc ? cb - nc : cb);
+            const double c0 = c[ri[0] * nc + cb], c1 = c[ri[1] * nc + cb];
+            const double c2 = c[ri[2] * nc + cb], c3 = c[ri[3] * nc + cb];
+            R0[b] = c1;
+            double row = 0.0;
+            row += w0 * c0;
+            row += w1 * c1;
+            row += w1 * c2;
+            row += w0 * c3;
+            R1[b] = row;
+        }
+        double a01 = 0.0, a11 = 0.0;
+        a01 += w0 * R0[0]; a01 += w1 * R0[1]; a01 += w1 * R0[2]; a01 += w0 * R0[3];
+        a11 += w0 * R1[0]; a11 += w1 * R1[1]; a11 += w1 * R1[2]; a11 += w0 * R1[3];
+        const int t0 = (2 * bi) * n + 2 * bj, t1 = t0 + n;
+        out[t0] = (out[t0] - 0.0) + R0[1];
+        out[t0 + 1] = (out[t0 + 1] - 0.0) + a01;
+        out[t1] = (out[t1] - 0.0) + R1[1];
+        out[t1 + 1] = (out[t1 + 1] - 0.0) + a11;
+    }
+    __syncthreads();
+}
+
+// correction(rhs, l) of solver.py:181-190 for a ratio-2 sub-ladder in shared memory: D[j], F[j]
+// per level, F[0] filled by the caller; leaves the correction of level 0 in D[0].
+__device__ void small_ladder(double *const *D, double *const *F, const SmallLadder &L, int n_smooth,
+                             int coarse_sweeps, double *sred) {
+    const int tid = threadIdx.x, nt = blockDim.x;
+    for (int j = 0; j < L.nlev; ++j) {
+        const int n = L.side[j], nn = n * n;
+        for (int c = tid; c < nn; c += nt) D[j][c] = 0.0;
+        __syncthreads();
+        small_gs(D[j], F[j], n, j == L.nlev - 1 ? coarse_sweeps : n_smooth, sred);
+        if (j < L.nlev - 1) {   // residual at the injected points -> next RHS 0.5 (r - mean(r))
+            const int ncc = (n >> 1) * (n >> 1);
+            const double mean = small_residual_inject(D[j], F[j], n, F[j + 1], sred);
+            for (int t = tid; t < ncc; t += nt) F[j + 1][t] = (F[j + 1][t] - mean) * 0.5;
+            __syncthreads();
+        }
+    }
+    for (int j = L.nlev - 2; j >= 0; --j) small_prolong2_add(D[j + 1], L.side[j + 1], D[j]);   // ascend
+}
+
 __global__ void __launch_bounds__(kSmallThreads) k_correction_small(const double *__restrict__ rc0, const double *rc0_mean,
                                                            double *__restrict__ d0, SmallLadder L, int n_smooth,
                                                            int coarse_sweeps) {
@@ -167,106 +277,82 @@ __global__ void __launch_bounds__(kSmallThreads) k_correction_small(const double
         }
     }
     {   // level 0 RHS: 0.5 * (rc0 - mean)
-        const int n = L.side[0], nn = n * n;
+        const int nn = L.side[0] * L.side[0];
         const double m = *rc0_mean;
         for (int c = tid; c < nn; c += nt) F[0][c] = (rc0[c] - m) * 0.5;
     }
-    for (int j = 0; j < L.nlev; ++j) {
-        const int n = L.side[j], nn = n * n, half = nn >> 1;
-        const double h = 2.0 * M_PI / n, h2 = h * h;
-        double *sp = D[j];
-        const double *sf = F[j];
-        for (int c = tid; c < nn; c += nt) sp[c] = 0.0;
-        __syncthreads();
-        const int sweeps = j == L.nlev - 1 ? coarse_sweeps : n_smooth;
-        const int hn = n >> 1, hsh = pow2_shift(hn);
-        for (int s = 0; s < sweeps; ++s) {
-            for (int color = 0; color < 2; ++color) {
-                for (int t = tid; t < half; t += nt) {
-                    int i, k;
-                    split_idx(t, hn, hsh, i, k);
-                    int jj = 2 * k + ((i + color) & 1);
-                    int im1 = i > 0 ? i - 1 : n - 1, ip1 = i < n - 1 ? i + 1 : 0;
-                    int jm1 = jj > 0 ? jj - 1 : n - 1, jp1 = jj < n - 1 ? jj + 1 : 0;
-                    double nb = ((sp[im1 * n + jj] + sp[ip1 * n + jj]) + sp[i * n + jm1]) + sp[i * n + jp1];
-                    sp[i * n + jj] = (nb - h2 * sf[i * n + jj]) * 0.25;
-                }
-                __syncthreads();
-            }
-            double acc = 0.0;
-            for (int c = tid; c < nn; c += nt) acc += sp[c];
-            const double mean = block_sum_1024(acc, sred) * (1.0 / double(nn));
-            for (int c = tid; c < nn; c += nt) sp[c] -= mean;
-            __syncthreads();
-        }
-        if (j < L.nlev - 1) {   // residual at the injected (even, even) points -> next RHS
-            const int nc = n >> 1, ncc = nc * nc;
-            const double inv_h2 = 1.0 / h2;
-            double *fr = F[j + 1];
-            double acc = 0.0;
-            const int csh = pow2_shift(nc);
-            for (int t = tid; t < ncc; t += nt) {
-                int ic, jc;
-                split_idx(t, nc, csh, ic, jc);
-                const int i = 2 * ic, jj = 2 * jc;
-                const int im1 = i > 0 ? i - 1 : n - 1, ip1 = i < n - 1 ? i + 1 : 0;
-                const int jm1 = jj > 0 ? jj - 1 : n - 1, jp1 = jj < n - 1 ? jj + 1 : 0;
-                const int c = i * n + jj;
-                double nb = ((sp[im1 * n + jj] + sp[ip1 * n + jj]) + sp[i * n + jm1]) + sp[i * n + jp1];
-                const double res = sf[c] - ((nb - 4.0 * sp[c]) * inv_h2);
-                fr[t] = res;
-                acc += res;
-            }
-            const double mean = block_sum_1024(acc, sred) * (1.0 / double(ncc));
-            for (int t = tid; t < ncc; t += nt) fr[t] = (fr[t] - mean) * 0.5;
-            __syncthreads();
-        }
-    }
-    // ascend: D[j] += P2(D[j + 1])
-    const double w0 = -0.0625, w1 = 0.5625;
-    for (int j = L.nlev - 2; j >= 0; --j) {
-        const int nc = L.side[j + 1], n = 2 * nc;
-        const double *c = D[j + 1];
-        double *out = D[j];
-        const int csh = pow2_shift(nc);
-        for (int t = tid; t < nc * nc; t += nt) {
-            int bi, bj;
-            split_idx(t, nc, csh, bi, bj);
-            int ri[4];
-#pragma unroll
-            for (int o = 0; o < 4; ++o) {
-                const int r = bi + o - 1;
-                ri[o] = r < 0 ? r + nc : (r >= nc ? r - nc : r);
-            }
-            double R0[4], R1[4];
-#pragma unroll
-            for (int b = 0; b < 4; ++b) {
-                int cb = bj + b - 1;
-                cb = cb < 0 ? cb + nc : (cb >= nc ? cb - nc : cb);
-                const double c0 = c[ri[0] * nc + cb], c1 = c[ri[1] * nc + cb];
-                const double c2 = c[ri[2] * nc + cb], c3 = c[ri[3] * nc + cb];
-                R0[b] = c1;
-                double row = 0.0;
-                row += w0 * c0;
-                row += w1 * c1;
-                row += w1 * c2;
-                row += w0 * c3;
-                R1[b] = row;
-            }
-            double a01 = 0.0, a11 = 0.0;
-            a01 += w0 * R0[0]; a01 += w1 * R0[1]; a01 += w1 * R0[2]; a01 += w0 * R0[3];
-            a11 += w0 * R1[0]; a11 += w1 * R1[1]; a11 += w1 * R1[2]; a11 += w0 * R1[3];
-            const int t0 = (2 * bi) * n + 2 * bj, t1 = t0 + n;
-            out[t0] = (out[t0] - 0.0) + R0[1];
-            out[t0 + 1] = (out[t0 + 1] - 0.0) + a01;
-            out[t1] = (out[t1] - 0.0) + R1[1];
-            out[t1 + 1] = (out[t1 + 1] - 0.0) + a11;
-        }
-        __syncthreads();
-    }
+    small_ladder(D, F, L, n_smooth, coarse_sweeps, sred);
+    const int nn = L.side[0] * L.side[0];
+    for (int c = tid; c < nn; c += nt) d0[c] = D[0][c];
+}
+
+// A whole spline V-cycle of a small grid (side <= kSmallN, ratio-2 ladder) plus the solve loop's
+// logging pass in ONE CTA (solver.py:158-197 + 311-313): N_smooth GS sweeps on p with the exact
+// per-sweep mean, the injected residual, the sub-ladder correction, the Keys prolongation added,
+// new p = out - mean(out), stats = (diff_norm, residual rms).  Same per-element arithmetic as the
+// multi-kernel cycle; the means are block sums.  Replaces ~5 launches per cycle on config 1.
+__global__ void __launch_bounds__(kSmallThreads) k_vcycle_small(double *__restrict__ p, const double *__restrict__ f,
+                                                       SmallLadder L, int n_smooth, int coarse_sweeps,
+                                                       double *stats) {
+    extern __shared__ double sm[];
+    __shared__ double sred[33];
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int n = L.side[0], nn = n * n;
+    double *P = sm, *S = sm + nn, *Fp = sm + 2 * nn;
+    double *D[kSmallMaxLev], *F[kSmallMaxLev];
+    SmallLadder Lc{};
+    Lc.nlev = L.nlev - 1;
     {
-        const int nn = L.side[0] * L.side[0];
-        for (int c = tid; c < nn; c += nt) d0[c] = D[0][c];
+        int off = 3 * nn;
+        for (int j = 0; j < Lc.nlev; ++j) {
+            Lc.side[j] = L.side[j + 1];
+            const int m = Lc.side[j] * Lc.side[j];
+            D[j] = sm + off;
+            F[j] = sm + off + m;
+            off += 2 * m;
+        }
+    }
+    for (int c = tid; c < nn; c += nt) {
+        P[c] = p[c];
+        S[c] = P[c];
+        Fp[c] = f[c];
+    }
+    __syncthreads();
+    small_gs(S, Fp, n, n_smooth, sred);                                  // S: gauge-fixed smoothed iterate
+    {
+        const double rm = small_residual_inject(S, Fp, n, F[0], sred);   // level-1 RHS 0.5 (r - mean(r))
+        const int ncc = (n >> 1) * (n >> 1);
+        for (int t = tid; t < ncc; t += nt) F[0][t] = (F[0][t] - rm) * 0.5;
+        __syncthreads();
+    }
+    small_ladder(D, F, Lc, n_smooth, coarse_sweeps, sred);
+    small_prolong2_add(D[0], Lc.side[0], S);                             // out = (S - 0) + P(d1)
+    double acc = 0.0;
+    for (int c = tid; c < nn; c += nt) acc += S[c];
+    const double m = block_sum_1024(acc, sred) * (1.0 / double(nn));
+    const double h = 2.0 * M_PI / n, inv_h2 = 1.0 / (h * h);
+    double v0 = 0.0, v1 = 0.0, v2 = 0.0;
+    for (int c = tid; c < nn; c += nt) {
+        const int i = c / n, j = c - i * n;
+        const int im1 = i > 0 ? i - 1 : n - 1, ip1 = i < n - 1 ? i + 1 : 0;
+        const int jm1 = j > 0 ? j - 1 : n - 1, jp1 = j < n - 1 ? j + 1 : 0;
+        const double o = S[c];
+        const double nb = ((S[im1 * n + j] + S[ip1 * n + j]) + S[i * n + jm1]) + S[i * n + jp1];
+        const double np_ = o - m;
+        const double d = np_ - P[c];
+        const double r = Fp[c] - ((nb - 4.0 * o) * inv_h2);
+        p[c] = np_;
+        v0 += d * d;
+        v1 += r;
+        v2 += r * r;
+    }
+    v0 = block_sum_1024(v0, sred) * (1.0 / double(nn));
+    v1 = block_sum_1024(v1, sred) * (1.0 / double(nn));
+    v2 = block_sum_1024(v2, sred) * (1.0 / double(nn));
+    if (tid == 0) {
+        stats[0] = sqrt(v0);
+        const double var = v2 - v1 * v1;
+        stats[1] = sqrt(var > 0.0 ? var : 0.0);
     }
 }
 
@@ -1218,6 +1304,23 @@ int launch_correction_small(const double *rc0, const double *rc0_mean, double *d
     }
     cudaFuncSetAttribute(k_correction_small, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     k_correction_small<<<1, kSmallThreads, smem, st>>>(rc0, rc0_mean, d0, L, n_smooth, coarse_sweeps);
+    MGSR_LAUNCH_CHECK();
+    return MGSR_OK;
+}
+
+int launch_vcycle_small(double *p, const double *f, const int *sides, int nlev, int n_smooth, int coarse_sweeps,
+                        double *stats, cudaStream_t st) {
+    if (nlev < 2 || nlev > kSmallMaxLev || sides[0] > kSmallN) { set_error("vcycle_small: bad ladder"); return MGSR_E_BAD_ARG; }
+    SmallLadder L{};
+    L.nlev = nlev;
+    size_t smem = 3 * sizeof(double) * size_t(sides[0]) * sides[0];
+    for (int j = 0; j < nlev; ++j) {
+        L.side[j] = sides[j];
+        if (j > 0 && sides[j] * 2 != sides[j - 1]) { set_error("vcycle_small: ratio-2 ladder only"); return MGSR_E_BAD_ARG; }
+        if (j > 0) smem += 2 * sizeof(double) * size_t(sides[j]) * sides[j];
+    }
+    cudaFuncSetAttribute(k_vcycle_small, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    k_vcycle_small<<<1, kSmallThreads, smem, st>>>(p, f, L, n_smooth, coarse_sweeps, stats);
     MGSR_LAUNCH_CHECK();
     return MGSR_OK;
 }

@@ -19,6 +19,9 @@ int launch_finalize(const double *out, const double *mean_ptr, double *p, FSrc f
                     double *stats2, void *red_slot, cudaStream_t st);
 int launch_affine(const double *a, double *out, int64_t count, const double *shift, double scale, cudaStream_t st);
 // correction of a whole ratio-2 sub-ladder with sides[0] <= kSmallN in one CTA (spline prolongation)
+// a whole spline V-cycle + logging pass of a ratio-2 ladder with sides[0] <= kSmallN in one CTA
+int launch_vcycle_small(double *p, const double *f, const int *sides, int nlev, int n_smooth, int coarse_sweeps,
+                        double *stats, cudaStream_t st);
 int launch_correction_small(const double *rc0, const double *rc0_mean, double *d0, const int *sides, int nlev,
                             int n_smooth, int coarse_sweeps, cudaStream_t st);
 
