@@ -70,54 +70,6 @@ __global__ void k_mean(const double *__restrict__ a, int64_t count, RedSlot slot
     grid_reduce<1>(v, slot, result, 1.0 / double(count));
 }
 
-// Whole small grid in one CTA: all sweeps with the reference's per-sweep mean
-// subtraction done exactly in order (block reduction), optional fused coarse
-// residual.  n <= kSmallN.
-__global__ void __launch_bounds__(1024) k_gs_small(double *__restrict__ p, FSrc fs, int n, double h2,
-                                                   int sweeps, int zero_init, double *mean_out) {
-    extern __shared__ double sm[];
-    double *sp = sm, *sf = sm + n * n;
-    __shared__ double sred[32];
-    const int tid = threadIdx.x, nt = blockDim.x, nn = n * n;
-    const double sh = fs.load_shift();
-    for (int c = tid; c < nn; c += nt) {
-        sp[c] = zero_init ? 0.0 : p[c];
-        sf[c] = fs.at(c, sh);
-    }
-    __syncthreads();
-    const int half = nn >> 1, hn = n >> 1, hsh = pow2_shift(hn);
-    for (int s = 0; s < sweeps; ++s) {
-        for (int color = 0; color < 2; ++color) {
-            for (int t = tid; t < half; t += nt) {
-                int i, k;
-                split_idx(t, hn, hsh, i, k);
-                int j = 2 * k + ((i + color) & 1);
-                int im1 = i > 0 ? i - 1 : n - 1, ip1 = i < n - 1 ? i + 1 : 0;
-                int jm1 = j > 0 ? j - 1 : n - 1, jp1 = j < n - 1 ? j + 1 : 0;
-                double nb = ((sp[im1 * n + j] + sp[ip1 * n + j]) + sp[i * n + jm1]) + sp[i * n + jp1];
-                sp[i * n + j] = (nb - h2 * sf[i * n + j]) * 0.25;
-            }
-            __syncthreads();
-        }
-        double acc = 0.0;
-        for (int c = tid; c < nn; c += nt) acc += sp[c];
-        acc = warp_sum(acc);
-        if ((tid & 31) == 0) sred[tid >> 5] = acc;
-        __syncthreads();
-        if (tid < 32) {
-            double w = tid < (nt >> 5) ? sred[tid] : 0.0;
-            w = warp_sum(w);
-            if (tid == 0) sred[0] = w;
-        }
-        __syncthreads();
-        const double mean = sred[0] * (1.0 / double(nn));
-        for (int c = tid; c < nn; c += nt) sp[c] -= mean;
-        __syncthreads();
-    }
-    for (int c = tid; c < nn; c += nt) p[c] = sp[c];
-    if (tid == 0 && mean_out) *mean_out = 0.0;   // already gauge-fixed
-}
-
 // ---------------------------------------------------------------------------
 // Whole coarse sub-ladder in ONE CTA: correction(rhs, l) of solver.py:181-190 for
 // a level with side <= kSmallN and every level below it (ratio-2 ladder, spline
@@ -152,9 +104,8 @@ __device__ double block_sum_1024(double v, double *sred) {
 
 // GS sweeps from the current contents of sp with the exact per-sweep mean subtraction
 // (_stencil.pyx:25-45), whole grid in one CTA's shared memory.
-__device__ void small_gs(double *sp, const double *sf, int n, int sweeps, double *sred) {
+__device__ void small_gs(double *sp, const double *sf, int n, double h2, int sweeps, double *sred) {
     const int tid = threadIdx.x, nt = blockDim.x, nn = n * n, half = nn >> 1;
-    const double h = 2.0 * M_PI / n, h2 = h * h;
     const int hn = n >> 1, hsh = pow2_shift(hn);
     for (int s = 0; s < sweeps; ++s) {
         for (int color = 0; color < 2; ++color) {
@@ -249,7 +200,8 @@ __device__ void small_ladder(double *const *D, double *const *F, const SmallLadd
         const int n = L.side[j], nn = n * n;
         for (int c = tid; c < nn; c += nt) D[j][c] = 0.0;
         __syncthreads();
-        small_gs(D[j], F[j], n, j == L.nlev - 1 ? coarse_sweeps : n_smooth, sred);
+        const double h = 2.0 * M_PI / n;
+        small_gs(D[j], F[j], n, h * h, j == L.nlev - 1 ? coarse_sweeps : n_smooth, sred);
         if (j < L.nlev - 1) {   // residual at the injected points -> next RHS 0.5 (r - mean(r))
             const int ncc = (n >> 1) * (n >> 1);
             const double mean = small_residual_inject(D[j], F[j], n, F[j + 1], sred);
@@ -258,6 +210,25 @@ __device__ void small_ladder(double *const *D, double *const *F, const SmallLadd
         }
     }
     for (int j = L.nlev - 2; j >= 0; --j) small_prolong2_add(D[j + 1], L.side[j + 1], D[j]);   // ascend
+}
+
+// Whole small grid in one CTA: all sweeps with the reference's per-sweep mean subtraction done
+// exactly in order (block reduction).  n <= kSmallN.
+__global__ void __launch_bounds__(kSmallThreads) k_gs_small(double *__restrict__ p, FSrc fs, int n, double h2,
+                                                           int sweeps, int zero_init, double *mean_out) {
+    extern __shared__ double sm[];
+    double *sp = sm, *sf = sm + n * n;
+    __shared__ double sred[33];
+    const int tid = threadIdx.x, nt = blockDim.x, nn = n * n;
+    const double sh = fs.load_shift();
+    for (int c = tid; c < nn; c += nt) {
+        sp[c] = zero_init ? 0.0 : p[c];
+        sf[c] = fs.at(c, sh);
+    }
+    __syncthreads();
+    small_gs(sp, sf, n, h2, sweeps, sred);
+    for (int c = tid; c < nn; c += nt) p[c] = sp[c];
+    if (tid == 0 && mean_out) *mean_out = 0.0;   // already gauge-fixed
 }
 
 __global__ void __launch_bounds__(kSmallThreads) k_correction_small(const double *__restrict__ rc0, const double *rc0_mean,
@@ -318,7 +289,10 @@ __global__ void __launch_bounds__(kSmallThreads) k_vcycle_small(double *__restri
         Fp[c] = f[c];
     }
     __syncthreads();
-    small_gs(S, Fp, n, n_smooth, sred);                                  // S: gauge-fixed smoothed iterate
+    {
+        const double h = 2.0 * M_PI / n;
+        small_gs(S, Fp, n, h * h, n_smooth, sred);                       // S: gauge-fixed smoothed iterate
+    }
     {
         const double rm = small_residual_inject(S, Fp, n, F[0], sred);   // level-1 RHS 0.5 (r - mean(r))
         const int ncc = (n >> 1) * (n >> 1);
@@ -1134,7 +1108,7 @@ int launch_gs(const double *p_in, double *p_out, double *tmp, FSrc fs, int n, do
             MGSR_CUDA_TRY(cudaMemcpyAsync(p_out, p_in, bytes, cudaMemcpyDeviceToDevice, st));
         size_t smem = 2 * sizeof(double) * n * n;
         cudaFuncSetAttribute(k_gs_small, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        k_gs_small<<<1, 1024, smem, st>>>(p_out, fs, n, h2, sweeps, zero_init, mean_out);
+        k_gs_small<<<1, kSmallThreads, smem, st>>>(p_out, fs, n, h2, sweeps, zero_init, mean_out);
         MGSR_LAUNCH_CHECK();
         if (rc) {
             k_res_restrict<<<grid_2d(n / 2, n / 2), 256, 0, st>>>(p_out, fs, n, 2, inv_h2, rc,
