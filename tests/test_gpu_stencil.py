@@ -132,3 +132,32 @@ def test_diff_norm(cuda):
     rng = np.random.default_rng(0)
     a, b = rng.standard_normal((300, 300)), rng.standard_normal((300, 300))
     assert abs(diff_norm(Grid(a), Grid(b)) - np.sqrt(np.mean((a - b) ** 2))) < 1e-14
+
+
+@pytest.mark.parametrize("n,sweeps", [(2, 3), (4, 1), (6, 2), (10, 5), (32, 7), (66, 2)])
+def test_gs_tiny_and_odd_multiple_sides_vs_oracle(cuda, orc, n, sweeps):
+    """Smallest sides (single-CTA kernel, n <= 64, every sweep's exact mean) and a side just above it
+    (66: the generic half-sweep path) against the C oracle."""
+    from paper_2403_07936_b200 import kernels
+    p, f, h2 = random_problem(n, 40 + n)
+    exp = p.copy(); orc.gs_sweeps(exp, f, h2, sweeps)
+    got = p.copy(); kernels.gs_sweeps(got, f, h2, sweeps)
+    assert rel(got, exp) < 1e-12
+
+
+@pytest.mark.parametrize("nc,s", [(2, 2), (3, 4), (5, 8), (2, 16), (6, 2)])
+def test_spline_tiny_coarse_grids_vs_oracle(cuda, orc, nc, s):
+    """Coarse sides below the 4-tap stencil width: the periodic wrap folds taps onto the same cells."""
+    from paper_2403_07936_b200 import transfer
+    from paper_2403_07936_b200.grid import Grid
+    c = np.random.default_rng(nc * 31 + s).standard_normal((nc, nc))
+    assert rel(transfer.spline_prolong(Grid(c), s).data, orc.spline_prolong(c, s)) < 1e-12
+
+
+@pytest.mark.parametrize("n,s", [(4, 2), (32, 16), (48, 4)])
+def test_restrict_edge_sizes_vs_oracle(cuda, orc, n, s):
+    from paper_2403_07936_b200 import transfer
+    from paper_2403_07936_b200.grid import Grid
+    x = np.random.default_rng(n + s).standard_normal((n, n))
+    assert rel(transfer.restrict(Grid(x), s).data, orc.restrict(x, s)) < 1e-13
+    assert np.array_equal(transfer.restrict(Grid(x), s, subtract_mean=False).data, orc.restrict(x, s, False))
