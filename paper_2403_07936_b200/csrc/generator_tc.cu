@@ -1340,12 +1340,9 @@ int launch_sr_pass_tc_dbg(const mgsr_gen *g, const double *c, const double *c_sh
     MGSR_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, P));
     {
         const int ne = edge_count(P.npos);
-        static bool te_attr = false;
-        if (!te_attr) {
-            MGSR_CUDA_TRY(cudaFuncSetAttribute(k_tail_edge<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(TE_SMEM)));
-            MGSR_CUDA_TRY(cudaFuncSetAttribute(k_tail_edge<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(TE_SMEM)));
-            te_attr = true;
-        }
+        // per current device (function attributes are per device), like k_gen_tc's above
+        MGSR_CUDA_TRY(cudaFuncSetAttribute(f16 ? k_tail_edge<true> : k_tail_edge<false>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, int(TE_SMEM)));
         const int nb = ne < nsm ? ne : nsm;
         if (f16) k_tail_edge<true><<<nb, TE_THREADS, TE_SMEM, st>>>(P, ne);
         else k_tail_edge<false><<<nb, TE_THREADS, TE_SMEM, st>>>(P, ne);
