@@ -104,23 +104,23 @@ __global__ void __launch_bounds__(kConvThreads) k_conv_simt(const float *__restr
 // (c ascending, dy, dx, fmaf) is k_conv_simt's, so results are bitwise identical.
 constexpr int kConv2Threads = 256, kConv2OB = 16, kConv2CC = 16;
 
-template <int K, int MAXP, int OP>
+template <int K, int MAXP, int OP, int OB>
 __global__ void __launch_bounds__(kConv2Threads) k_conv_rt(const float *__restrict__ in, int N, int C, int H,
                                                           const float *__restrict__ w, int O,
                                                           float *__restrict__ out, Epi ep, int nw) {
     extern __shared__ __align__(16) float sm2[];
     constexpr int P = K / 2, KK = K * K;
     const int HW = H * H, HP = H + K - 1, HP2 = HP * HP;
-    const int n0 = blockIdx.x * nw, ob = blockIdx.y * kConv2OB;
-    const int OBn = min(kConv2OB, O - ob);
+    const int n0 = blockIdx.x * nw, ob = blockIdx.y * OB;
+    const int OBn = min(OB, O - ob);
     float *s_w = sm2;                                   // [cc][KK][16]
-    float *s_in = sm2 + kConv2CC * KK * kConv2OB;       // [nw][cc][HP][HP]
+    float *s_in = sm2 + kConv2CC * KK * OB;       // [nw][cc][HP][HP]
     const int tid = threadIdx.x;
-    float acc[MAXP][kConv2OB];
+    float acc[MAXP][OB];
 #pragma unroll
     for (int k = 0; k < MAXP; ++k)
 #pragma unroll
-        for (int o = 0; o < kConv2OB; ++o) acc[k][o] = 0.f;
+        for (int o = 0; o < OB; ++o) acc[k][o] = 0.f;
     int wl[MAXP], py[MAXP], px[MAXP];
     bool act[MAXP];
 #pragma unroll
@@ -141,8 +141,8 @@ __global__ void __launch_bounds__(kConv2Threads) k_conv_rt(const float *__restri
             const int n = n0 + wi;
             s_in[idx] = n < N ? in[((int64_t(n) * C + c0 + c) * H + yy) * H + xx] : 0.f;
         }
-        for (int idx = tid; idx < cc * KK * kConv2OB; idx += kConv2Threads) {
-            const int o = idx % kConv2OB, t = (idx / kConv2OB) % KK, c = idx / (kConv2OB * KK);
+        for (int idx = tid; idx < cc * KK * OB; idx += kConv2Threads) {
+            const int o = idx % OB, t = (idx / OB) % KK, c = idx / (OB * KK);
             s_w[idx] = o < OBn ? __ldg(w + (int64_t(ob + o) * C + c0 + c) * KK + t) : 0.f;
         }
         __syncthreads();
@@ -151,15 +151,15 @@ __global__ void __launch_bounds__(kConv2Threads) k_conv_rt(const float *__restri
             if (!act[k]) continue;
             for (int c = 0; c < cc; ++c) {
                 const float *si = s_in + ((wl[k] * cc + c) * HP + py[k]) * HP + px[k];
-                const float4 *wc = reinterpret_cast<const float4 *>(s_w + c * KK * kConv2OB);
+                const float4 *wc = reinterpret_cast<const float4 *>(s_w + c * KK * OB);
 #pragma unroll
                 for (int dy = 0; dy < K; ++dy)
 #pragma unroll
                     for (int dx = 0; dx < K; ++dx) {
                         const float v = si[dy * HP + dx];
-                        const float4 *wt = wc + (dy * K + dx) * (kConv2OB / 4);
+                        const float4 *wt = wc + (dy * K + dx) * (OB / 4);
 #pragma unroll
-                        for (int q = 0; q < kConv2OB / 4; ++q) {
+                        for (int q = 0; q < OB / 4; ++q) {
                             const float4 w4 = wt[q];
                             acc[k][4 * q] = fmaf(v, w4.x, acc[k][4 * q]);
                             acc[k][4 * q + 1] = fmaf(v, w4.y, acc[k][4 * q + 1]);
@@ -175,7 +175,7 @@ __global__ void __launch_bounds__(kConv2Threads) k_conv_rt(const float *__restri
         if (!act[k]) continue;
         const int n = n0 + wl[k], pix = py[k] * H + px[k], y = py[k], x = px[k];
 #pragma unroll
-        for (int oo = 0; oo < kConv2OB; ++oo) {
+        for (int oo = 0; oo < OB; ++oo) {
             if (oo >= OBn) break;
             const int o = ob + oo;
             float v = acc[k][oo];
@@ -206,17 +206,21 @@ static int conv(const float *in, int N, int C, int H, const float *w, int O, flo
         const int HW = H * H, HP = H + K - 1;
         const int nw = HW <= kConv2Threads ? kConv2Threads / HW : 1;
         const int per = (HW + kConv2Threads - 1) / kConv2Threads;
-        const size_t smem = sizeof(float) * (size_t(kConv2CC) * K * K * kConv2OB + size_t(nw) * kConv2CC * HP * HP);
+        // output-channel block: 16, or 4 for the 3-channel tail (no FMAs on padding channels)
+        const int ob = O >= 16 ? kConv2OB : 4;
+        const size_t smem = sizeof(float) * (size_t(kConv2CC) * K * K * ob + size_t(nw) * kConv2CC * HP * HP);
         if (per <= 3 && smem <= 200 * 1024) {
-            dim3 grid((N + nw - 1) / nw, (O + kConv2OB - 1) / kConv2OB);
-            if (per == 1) {
-                auto kern = k_conv_rt<K, 1, OP>;
+            dim3 grid((N + nw - 1) / nw, (O + ob - 1) / ob);
+            auto go = [&](auto kern) {
                 cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
                 kern<<<grid, kConv2Threads, smem, st>>>(in, N, C, H, w, O, out, ep, nw);
+            };
+            if (ob == kConv2OB) {
+                if (per == 1) go(k_conv_rt<K, 1, OP, kConv2OB>);
+                else go(k_conv_rt<K, 3, OP, kConv2OB>);
             } else {
-                auto kern = k_conv_rt<K, 3, OP>;
-                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-                kern<<<grid, kConv2Threads, smem, st>>>(in, N, C, H, w, O, out, ep, nw);
+                if (per == 1) go(k_conv_rt<K, 1, OP, 4>);
+                else go(k_conv_rt<K, 3, OP, 4>);
             }
             MGSR_LAUNCH_CHECK();
             return MGSR_OK;
