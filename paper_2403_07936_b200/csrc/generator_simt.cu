@@ -556,6 +556,7 @@ extern "C" int mgsr_generator_forward(const mgsr_gen *g, const double *x, int64_
     size_t nx = size_t(batch) * 3 * H * H, ny = size_t(batch) * 3 * 4 * H * H;
     size_t bytes = sizeof(float) * (nx + ny + gen_scratch_floats(H) * size_t(batch));
     float *buf = nullptr;
+    keep_async_pool();
     MGSR_CUDA_TRY(cudaMallocAsync(&buf, bytes, st));
     k_f64_to_f32<<<grid_for(nx, 256), 256, 0, st>>>(x, buf, nx);
     int r = gen_forward_f32(g, buf, int(batch), H, buf + nx, buf + nx + ny, st);

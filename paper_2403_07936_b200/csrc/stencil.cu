@@ -1041,6 +1041,21 @@ __global__ void k_sqdiff(const double *__restrict__ a, const double *__restrict_
 // ---------------------------------------------------------------------------
 // launch helpers (shared with plan.cu)
 
+// Stream-ordered scratch for the API entry points (cudaMallocAsync): keep freed blocks in the device's
+// default pool instead of returning them at every synchronisation (release threshold 0), which made a
+// 4096^2 mgsr_gs_sweeps remap 268 MB per call.
+void keep_async_pool() {
+    static bool done[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64 || done[dev]) return;
+    cudaMemPool_t mp;
+    if (cudaDeviceGetDefaultMemPool(&mp, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done[dev] = true;
+}
+
 int num_sms() {
     static int cached = 0;
     if (!cached) {
@@ -1343,6 +1358,7 @@ extern "C" int mgsr_gs_sweeps(double *p, const double *f, int64_t n, double h2, 
     if (n <= kSmallN)  // exact per-sweep mean subtraction inside one CTA
         return launch_gs(p, p, nullptr, fs, int(n), h2, sweeps, 0, nullptr, nullptr, nullptr, red, st);
     double *tmp = nullptr;
+    keep_async_pool();
     MGSR_CUDA_TRY(cudaMallocAsync(&tmp, 2 * sizeof(double) * n * n, st));
     int rc = launch_gs(p, tmp, tmp + n * n, fs, int(n), h2, sweeps, 0, nullptr, nullptr, scal, red, st);
     if (rc == MGSR_OK) rc = launch_affine(tmp, p, n * n, scal, 1.0, st);
