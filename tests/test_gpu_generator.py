@@ -225,3 +225,19 @@ def test_tc_bench_size_pass_vs_oracle_sampled_windows(cuda, orc, weights):
     # north-star bar for trained weights; seeded He-init networks amplify operand rounding (measured
     # 2.1e-2 here, precision matrix in DESIGN.md) and are held to the documented 3e-2
     assert rel_l2(got[m], exp) < (1e-2 if weights == "trained" else 3e-2)
+
+
+def test_tc_generator_depths(cuda):
+    """Residual-block counts other than 4/8: B=1 runs on the tensor cores within the bar; a generator
+    whose constants no longer fit the kernel's shared memory (B=16) is refused loudly, never run
+    on a fallback."""
+    from paper_2403_07936_b200 import srmodel
+    from paper_2403_07936_b200.grid import Grid, NormBounds
+    c = _fields(32)["smooth"]
+    w1 = srmodel.random_weights(1, 3)
+    ref = srmodel.sr_prolong(Grid(c), w1, NormBounds(), 2, precision="fp32").data
+    got = srmodel.sr_prolong(Grid(c), w1, NormBounds(), 2, precision="fp16").data
+    assert rel_l2(got, ref) < 1e-2
+    w16 = srmodel.random_weights(16, 0)
+    with pytest.raises(ValueError, match="too deep"):
+        srmodel.sr_prolong(Grid(c), w16, NormBounds(), 2, precision="fp16")

@@ -231,3 +231,19 @@ def test_default_config_ladder_3072_vs_oracle(cuda, orc):
     got = solver.v_cycle(solver.v_cycle(Grid(p), PoissonProblem(Grid(f)), cfg, "spline"),
                          PoissonProblem(Grid(f)), cfg, "spline").data
     assert rel(got, exp) < 1e-12
+
+
+def test_solve_non_power_of_two_side_uses_host_start(cuda, orc):
+    """Sides whose n*n is not a power of two keep the host draw of the seeded start (the device
+    draw needs numpy's perfect pairwise tree); the history still matches the oracle."""
+    from paper_2403_07936_b200 import solver
+    from paper_2403_07936_b200.grid import Grid
+    from paper_2403_07936_b200.smoother import PoissonProblem
+    assert not solver._device_start_ok(96)
+    f = orc.sine_modes_rhs(96, 4)
+    p_ref, log_ref = orc.solve(f, orc.Config(N_step=1, r_min=12, N_smooth=2))
+    p, log = solver.solve(PoissonProblem(Grid(f)), cfg_(r_min=12))
+    assert log.iterations == log_ref.iterations
+    a = np.array([[r.diff_norm, r.residual_norm] for r in log.records])
+    b = np.array([[r.diff_norm, r.residual_norm] for r in log_ref.records])
+    assert (np.abs(a - b) / b).max() < 1e-6

@@ -81,3 +81,13 @@ def test_single_mode_and_errors(cuda, sg):
         spectral.turbulent_source(32, 4, 0, p_rms=-1.0)
     with pytest.raises(ValueError, match="n >= 4"):
         spectral.power_spectrum(Grid(np.zeros((2, 2))))
+
+
+def test_power_spectrum_zero_field_and_peak_normalize(cuda):
+    from paper_2403_07936_b200 import spectral
+    from paper_2403_07936_b200.grid import Grid
+    z = spectral.power_spectrum(Grid(np.zeros((16, 16))), peak_normalize=True)
+    assert np.array_equal(z.power, np.zeros(9))   # a zero field stays all-zero (grid.py:165-169)
+    x = np.random.default_rng(5).standard_normal((32, 32))
+    s = spectral.power_spectrum(Grid(x), peak_normalize=True).power
+    assert s.max() == 1.0
