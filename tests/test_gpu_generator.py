@@ -192,7 +192,7 @@ def test_tc_rejects_multi_pass_ratio(cuda):
 def test_tc_bench_size_pass_vs_oracle_sampled_windows(cuda, orc, weights):
     """The bench's finest pass at full size (n_c = 2048, 1,044,484 windows): the fp16 tensor-core
     field (before the per-pass mean subtraction, via mgsr_debug_tc_pass) against the fp64 CPU
-    oracle on seeded sampled windows -- corners, edge windows and interior windows -- within the
+    oracle on 256 seeded sampled windows -- corners, edge windows and interior windows -- within the
     north-star 1e-2 relL2 bar.  Weights: trained B=8, and the seeded He-init B=8 the bench uses."""
     import ctypes
     from paper_2403_07936_b200 import _lib, datagen, srmodel
@@ -213,7 +213,7 @@ def test_tc_bench_size_pass_vs_oracle_sampled_windows(cuda, orc, weights):
     npos = nc // 2 - 2
     rng = np.random.default_rng(11)
     picks = {(0, 0), (0, npos - 1), (npos - 1, 0), (npos - 1, npos - 1), (0, 517), (npos - 1, 3), (700, 0)}
-    while len(picks) < 32:
+    while len(picks) < 256:
         picks.add(tuple(int(x) for x in rng.integers(1, npos - 1, size=2)))
     sample = [i * npos + j for i, j in sorted(picks)]
     ow = orc.Weights({k: v for k, v in w.tensors.items()}, w.num_residual_blocks, w.tanh_scale)
@@ -221,7 +221,7 @@ def test_tc_bench_size_pass_vs_oracle_sampled_windows(cuda, orc, weights):
     qf = orc.sr_pass(orc.normalize(c, b), ow, 1, sample=sample)
     m = ~np.isnan(qf)
     exp = orc.denormalize(qf[m], np.sign(qf[m]), b)
-    assert m.sum() >= 32 * 16
+    assert m.sum() >= 256 * 16
     # north-star bar for trained weights; seeded He-init networks amplify operand rounding (measured
     # 2.1e-2 here, precision matrix in DESIGN.md) and are held to the documented 3e-2
     assert rel_l2(got[m], exp) < (1e-2 if weights == "trained" else 3e-2)
