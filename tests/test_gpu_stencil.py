@@ -161,3 +161,32 @@ def test_restrict_edge_sizes_vs_oracle(cuda, orc, n, s):
     x = np.random.default_rng(n + s).standard_normal((n, n))
     assert rel(transfer.restrict(Grid(x), s).data, orc.restrict(x, s)) < 1e-13
     assert np.array_equal(transfer.restrict(Grid(x), s, subtract_mean=False).data, orc.restrict(x, s, False))
+
+
+def test_c_abi_binding_as_documented(cuda, orc):
+    """The reference-side ctypes stub of INTEGRATION.md §3, verbatim in shape: raw device pointers,
+    the workspace size from mgsr_workspace_bytes, ValueError from mgsr_last_error -- no torch ops."""
+    import ctypes
+    from paper_2403_07936_b200 import _lib
+    lib = ctypes.CDLL(_lib.LIB_PATH)
+    lib.mgsr_last_error.restype = ctypes.c_char_p
+    lib.mgsr_workspace_bytes.restype = ctypes.c_size_t
+    lib.mgsr_workspace_bytes.argtypes = [ctypes.c_int64]
+    lib.mgsr_gs_sweeps.restype = ctypes.c_int
+    lib.mgsr_gs_sweeps.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_double,
+                                   ctypes.c_int32, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]
+
+    def check(rc):
+        if rc != 0:
+            raise ValueError(lib.mgsr_last_error().decode())
+
+    n, sweeps = 256, 3
+    p, f, h2 = random_problem(n, 77)
+    dp, df = cuda.from_numpy(p.copy()).cuda(), cuda.from_numpy(f).cuda()
+    nb = lib.mgsr_workspace_bytes(n)
+    ws = cuda.empty(nb, dtype=cuda.uint8, device="cuda")
+    check(lib.mgsr_gs_sweeps(dp.data_ptr(), df.data_ptr(), n, h2, sweeps, ws.data_ptr(), nb, None))
+    exp = p.copy(); orc.gs_sweeps(exp, f, h2, sweeps)
+    assert rel(dp.cpu().numpy(), exp) < 1e-12
+    with pytest.raises(ValueError, match="even side"):
+        check(lib.mgsr_gs_sweeps(dp.data_ptr(), df.data_ptr(), 255, h2, 1, ws.data_ptr(), nb, None))
