@@ -5,6 +5,8 @@ finest prolongations (per-level GAN mask).  Reports V-cycles to diff < 1e-10 per
 and wall time per solve.  Not collected by pytest.
 
     python tests/config5_timing.py [out.json] [batch] [n]
+    python -m torch.distributed.run --nproc-per-node 8 --master-addr 127.0.0.1 tests/config5_timing.py ...
+        (RHS sharded round-robin over the ranks, one GPU each: solver.solve_batch_distributed)
 """
 import json
 import os
@@ -24,6 +26,14 @@ from paper_2403_07936_b200.smoother import PoissonProblem  # noqa: E402
 
 def main():
     out = sys.argv[1] if len(sys.argv) > 1 else None
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        dist.init_process_group("nccl")
+    run = (lambda ps, cfg, w, **kw: solver.solve_batch_distributed(ps, cfg, w, **kw)) if world > 1 else \
+        (lambda ps, cfg, w, **kw: solver.solve_batch(ps, cfg, w, **kw))
     batch = int(sys.argv[2]) if len(sys.argv) > 2 else 16
     n = int(sys.argv[3]) if len(sys.argv) > 3 else 2048
     w = srmodel.load_weights(os.path.join(ROOT, "artifacts", "trained_b8.mgsr"))
@@ -34,11 +44,11 @@ def main():
         for gl in (1, 2, 3):
             cfg = solver.RunConfig(N_step=1, r_min=8, N_smooth=nu, mode="hybrid", N_GAN=1.0, S_thres=5e-4,
                                    N_iter=100)
-            solver.solve_batch(probs, cfg, w, precision="fp16", sr_levels=gl)   # plans, graphs (not timed)
+            run(probs, cfg, w, precision="fp16", sr_levels=gl)   # plans, graphs (not timed)
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            res = solver.solve_batch(probs, cfg, w, precision="fp16", sr_levels=gl)
-            wall = time.perf_counter() - t0
+            res = run(probs, cfg, w, precision="fp16", sr_levels=gl)
+            wall = time.perf_counter() - t0   # includes the gather: every rank holds all results
             its = [log.iterations for _, log in res]
             conv = [log.converged(1e-10) for _, log in res]
             sr_cycles = [sum(r.operator == "sr" for r in log.records) for _, log in res]
@@ -47,9 +57,11 @@ def main():
                    "iterations_max": int(max(its)), "all_converged": bool(all(conv)),
                    "sr_cycles_mean": float(np.mean(sr_cycles)),
                    "wall_s_batch": wall, "wall_ms_per_solve": 1e3 * wall / batch}
+            row["ranks"] = world
             rows.append(row)
-            print(json.dumps(row), flush=True)
-    if out:
+            if rank == 0:
+                print(json.dumps(row), flush=True)
+    if out and rank == 0:
         json.dump({"note": "fp16 tensor-core generator (trained B=8 fixture), latched hybrid N_GAN=1, S_thres=5e-4, "
                            "tol 1e-10; wall clock of the whole batch incl. host->device RHS copies and result "
                            "readback; solves run concurrently (one plan + stream each, one graph launch per solve)",

@@ -268,3 +268,32 @@ def test_pairwise_leaf_tree_equals_numpy_mean(n):
     while s.size > 1:
         s = s[0::2] + s[1::2]
     assert (0.0 + s[0]) / (n * n) == a.mean()
+
+
+def test_solve_batch_distributed_gloo_world2(tmp_path):
+    """Config 5 across ranks (replicas only): round-robin shards, results gathered in input order on
+    every rank, each RHS solved exactly once."""
+    import json
+    import socket
+    import subprocess
+    import sys
+    from paper_2403_07936_b200 import solver
+    assert solver.shard_indices(5, 0, 2) == [0, 2, 4] and solver.shard_indices(5, 1, 2) == [1, 3]
+    with pytest.raises(ValueError):
+        solver.shard_indices(4, 2, 2)
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    procs = []
+    for r in range(2):
+        env = dict(os.environ, RANK=str(r), WORLD_SIZE="2", LOCAL_RANK=str(r), MASTER_ADDR="127.0.0.1",
+                   MASTER_PORT=str(port), PYTHONPATH=ROOT)
+        procs.append(subprocess.Popen([sys.executable, os.path.join(ROOT, "tests", "_shard_worker.py"),
+                                       str(tmp_path)], env=env))
+    for pr in procs:
+        assert pr.wait(timeout=240) == 0
+    res = [json.load(open(tmp_path / f"shard{r}.json")) for r in range(2)]
+    assert sorted(res[0]["seen"] + res[1]["seen"]) == [0, 1, 2, 3, 4]
+    for r in res:
+        assert r["order"] == [0.0, 1.0, 2.0, 3.0, 4.0]
+        assert r["solved_by"] == [0.0, 1.0, 0.0, 1.0, 0.0]
