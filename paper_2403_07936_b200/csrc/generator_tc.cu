@@ -1,43 +1,46 @@
 // Tensor-core (tcgen05/TMEM) generator megakernel for ratio-2 SR passes.
 //
 // Reference semantics: srmodel.py:285-344 (generator), 414-463 (windowed
-// pass), grid.py:103-114 (log normalisation).  One persistent CTA per SM
-// walks groups of 6 windows; every layer of a window group stays on chip:
+// pass), grid.py:103-114 (log normalisation).  Persistent CTA pairs (clusters
+// of 2, one CTA per SM) walk groups of 8 windows per CTA; every layer of a
+// window group stays on chip:
 //
-//   * activations: bf16 in shared memory, each 6x6 window stored as an 8x8
-//     replicate-padded tile (64 rows) so that every 3x3 tap of a same-size
-//     replicate-padded correlation is the SAME matrix shifted by a constant
-//     row offset: the UMMA A-descriptor start address moves by 16 B per row
-//     (K-major, no swizzle) -- no im2col.  Two windows = one 128-row M tile,
-//     three tiles per group.
+//   * activations: fp16 (or bf16) in shared memory, each 6x6 window stored as
+//     an 8x8 replicate-padded image; the group's 8 images are interleaved by
+//     image row, so every 3x3 tap of a same-size replicate-padded correlation
+//     is the SAME matrix shifted by a constant row offset (dy * 64 + dx rows):
+//     the UMMA A-descriptor start address moves by 16 B per row (K-major, no
+//     swizzle) -- no im2col.  Tile t (M = 128 rows) holds padded rows
+//     py = 2t+1, 2t+2 of all 8 windows; three tiles per group; two buffers
+//     (layer L reads buffer L % 2).
+//   * cta_group::2: the leader issues M = 256 MMAs (128 rows from each CTA);
+//     the weights of a tap are split along N, 32 output channels per CTA.
 //   * TMEM (512 columns): per tile a 64-column fp32 accumulator, the fp32
-//     residual stream (64 columns) and the global-skip tensor (bf16 pairs,
-//     32 columns); the tail accumulators reuse the dead residual columns.
-//   * weights: bf16, pre-packed in the UMMA core-matrix layout, one 8 KB slot
-//     per 3x3 tap: the 9-slot ring holds a whole layer, so the MMA issuer
-//     runs tile-major and each tile's epilogue overlaps the next tile's MMAs.
-//     Slots refill with the next layer's taps (cp.async.bulk + mbarrier
-//     complete_tx) as soon as the last tile has consumed them.
+//     residual stream (64 columns) and the packed global skip (32 columns);
+//     the up-conv quarters double-buffer over the accumulator and residual
+//     columns, the tail accumulators (Z) reuse the skip columns.
+//   * weights: pre-packed in the UMMA core-matrix layout (BN scale folded),
+//     streamed through a 16-slot ring of 4 KB half-taps (cp.async.bulk +
+//     mbarrier complete_tx), read from L2 once per group.
 //   * head 9x9 conv: fp16 MMA (K = 81 taps padded to 96, the 3 identical input
-//     channels folded) on an im2col built per tile (two buffers); PReLU in the epilogue.
-//   * body: 2B+1 3x3 convs (bf16 x bf16 -> fp32, N = 64), BN folded into a
-//     per-channel affine; PReLU / residual add / global skip fused into the
-//     TMEM -> register -> smem epilogue.
-//   * up conv 64->256 as four N = 64 quarters; PReLU fused; the output is
-//     kept UNSHUFFLED: quarter u holds shuffled channels 16u..16u+15 in their
-//     four sub-pixel phases.
-//   * tail 9x9 conv (64 -> 3) on the x2 field = a 5x5 conv on the coarse grid
-//     over (channel, phase) inputs producing 3 outputs x 4 phases (sub-pixel
-//     decomposition), run on the same pipeline: 25 shifted taps, N = 16,
-//     accumulated over the four quarters in TMEM.  For interior windows the
-//     stitched (kept) pixels read only in-window cells, so no padding is
-//     involved; windows touching the grid edge (0.4% at n_c = 2048) spill
-//     their up-conv output to global memory and an exact fp32 kernel
-//     evaluates their tail with the reference's replicate clamping.
+//     channels folded) on an im2col built per tile (two buffers), built for
+//     the next group before the current group's stitched-pixel epilogue.
+//   * body: 2B+1 3x3 convs (N = 64, fp32 accumulate); PReLU / residual add /
+//     global skip fused into the TMEM -> register -> smem epilogue.
+//   * up conv 64->256 as four N = 64 quarters; PReLU fused; each quarter is
+//     drained pixel-shuffled into U (shared memory), the tail's A operand.
+//   * tail 9x9 conv (64 -> 3), pruned to the stitched (kept) fine rows of
+//     interior windows: the kept rows are M, the vertical tap dy is an A-row
+//     shift of U, the horizontal tap dx and the 3 outputs go along N (27 of
+//     32), reduced over dx by warp shuffles; windows touching the grid edge
+//     (0.4% at n_c = 2048) spill their up-conv output to global memory and an
+//     exact fp32 kernel (k_tail_edge) evaluates their tail with the
+//     reference's replicate clamping.
 //   * bias + s*tanh(x/s) + channel mean + sign-preserving 10^ map in the final
 //     epilogue, written straight into the fine fp64 grid.
 //
-// Warp roles: warp 0 = weight producer, warp 1 = MMA issuer + TMEM allocator,
+// Warp roles: warp 0 = weight producer, warp 1 = MMA issuer + TMEM allocator
+// (the peer CTA's warp 1 forwards its "slot landed" signals to the leader),
 // warps 2..17 = epilogue (512 threads; warp w reads TMEM lane quadrant w%4,
 // channel quarter (w-2)/4).
 #include <cuda_bf16.h>
