@@ -1,7 +1,8 @@
 // fp64 stencil kernels of the V-cycle: red-black Gauss-Seidel (temporally
-// blocked in shared memory), fused residual -> half-injection restriction,
-// separable Keys spline prolongation fused with the correction add, and the
-// solve-loop logging pass.  Compiled with --fmad=false so every product and
+// blocked: TMA-fed windows relaxed in registers on the large levels, whole
+// grids in one CTA's shared memory at the bottom of the ladder), fused
+// residual -> half-injection restriction, Keys spline prolongation fused with
+// the correction add, and the solve-loop logging pass.  Compiled with --fmad=false so every product and
 // sum rounds exactly as the reference's -ffp-contract=off C loops
 // (pkg/setup.py:37-39).
 #include <cuda.h>
