@@ -43,7 +43,8 @@ const char *mgsr_version(void);
 
 /* ---- stencil kernels: the MGSR_BACKEND plugin point (kernels/__init__.py:35-49) ---- */
 
-/* Bytes of device workspace mgsr_gs_sweeps / mgsr_residual / mgsr_restrict need for side n. */
+/* Bytes of device workspace mgsr_gs_sweeps / mgsr_residual / mgsr_restrict need for side n.
+ * Any contents: each call resets the reduction tickets it uses (stream-ordered). */
 size_t mgsr_workspace_bytes(int64_t n);
 
 /* In-place red-black Gauss-Seidel, red=(i+j) even first, mean subtracted

@@ -580,6 +580,7 @@ extern "C" int mgsr_sr_prolong(const mgsr_gen *g, const double *c, int64_t nc, i
     char *w = static_cast<char *>(ws);
     double *mean = reinterpret_cast<double *>(w);
     void *red = w + 256;
+    MGSR_CUDA_TRY(cudaMemsetAsync(red, 0, sizeof(unsigned), st));   // the slot's ticket starts at zero
     w += 256 + kRedSlotBytes;
     int r = launch_sr_prolong(g, c, nullptr, int(nc), s, p_min, p_max, precision, out, mean, w,
                               ws_bytes - 256 - kRedSlotBytes, red, st);

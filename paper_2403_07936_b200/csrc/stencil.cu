@@ -419,7 +419,7 @@ __global__ void __launch_bounds__(kRbThreads, 2)
     extern __shared__ __align__(128) double sm[];
     double *const sp = sm;                        // [64][64] p window
     double *const sf = sm + kRbW * kRbW;          // [64][64] f window
-    double2 *const xb = reinterpret_cast<double2 *>(sm + 2 * kRbW * kRbW);   // [2][warps][2][32] published rows
+    double *const xb = sm + 2 * kRbW * kRbW;      // [2][warps][2][32] published boundary cells
     __shared__ __align__(8) uint64_t bar_storage;
     const uint32_t bar = uint32_t(__cvta_generic_to_shared(&bar_storage));
     const uint32_t sp_a = uint32_t(__cvta_generic_to_shared(sp)), sf_a = uint32_t(__cvta_generic_to_shared(sf));
@@ -523,20 +523,15 @@ __global__ void __launch_bounds__(kRbThreads, 2)
                 p[r][e] = (nb - h2 * f[r][e]) * 0.25;
             }
             if (hs < 2 * K - 1 || RC) {   // publish the boundary rows for the next half-sweep (or the residual)
-                double2 *xo = xb + (hs & 1) * (kRbWarps * 64);
-                xo[(w * 2 + 0) * 32 + lane] = make_double2(p[0][0], p[0][1]);
-                xo[(w * 2 + 1) * 32 + lane] = make_double2(p[R - 1][0], p[R - 1][1]);
+                // only the cells this half-sweep updated change: row 0's element c and row R-1's element
+                // (c + R - 1) & 1 = 1 - c (R even) -- exactly the neighbours the next half-sweep (colour
+                // 1 - c) reads across the warp boundaries (and the residual's up neighbours)
+                double *xo = xb + (hs & 1) * (kRbWarps * 64);
+                xo[(w * 2 + 0) * 32 + lane] = p[0][c];
+                xo[(w * 2 + 1) * 32 + lane] = p[R - 1][1 - c];
                 __syncthreads();
-                if (w > 0) {
-                    const double2 t = xo[((w - 1) * 2 + 1) * 32 + lane];
-                    hu[0] = t.x;
-                    hu[1] = t.y;
-                }
-                if (w < kRbWarps - 1) {
-                    const double2 t = xo[((w + 1) * 2 + 0) * 32 + lane];
-                    hd[0] = t.x;
-                    hd[1] = t.y;
-                }
+                if (w > 0) hu[1 - c] = xo[((w - 1) * 2 + 1) * 32 + lane];
+                if (w < kRbWarps - 1) hd[c] = xo[((w + 1) * 2 + 0) * 32 + lane];
             }
         }
         // interior: window rows [HE, HE + TY), columns [HE, HE + TX)
@@ -1151,7 +1146,7 @@ int launch_gs(const double *p_in, double *p_out, double *tmp, FSrc fs, int n, do
         auto kern = k_gs_rb<KK, RCV>;                                                                      \
         constexpr int HE = (2 * KK + (RCV ? 1 : 0) + 1) & ~1, TX = kRbW - 2 * HE;                          \
         const int tl = ((n + TX - 1) / TX) * ((n + TX - 1) / TX);                                          \
-        const size_t rsm = sizeof(double) * (2 * kRbW * kRbW + 2 * 2 * kRbWarps * 64);                     \
+        const size_t rsm = sizeof(double) * (2 * kRbW * kRbW + 2 * kRbWarps * 64);                         \
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(rsm));                 \
         int occ = 0;                                                                                       \
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kRbThreads, rsm);                        \
@@ -1338,11 +1333,15 @@ extern "C" size_t mgsr_workspace_bytes(int64_t n) {
     return 256 + 4 * kRedSlotBytes;
 }
 
-static int check_ws(void *ws, size_t bytes) {
+// Validate a caller's workspace and reset its reduction-slot tickets (the grid reductions need them at
+// zero and return them to zero; a recycled or fresh uninitialised buffer may hold anything).
+static int check_ws(void *ws, size_t bytes, cudaStream_t st) {
     if (!ws || bytes < mgsr_workspace_bytes(0)) {
         set_error("workspace too small");
         return MGSR_E_WORKSPACE;
     }
+    for (int k = 0; k < 3; ++k)
+        MGSR_CUDA_TRY(cudaMemsetAsync(static_cast<char *>(ws) + 256 + k * kRedSlotBytes, 0, sizeof(unsigned), st));
     return MGSR_OK;
 }
 
@@ -1350,9 +1349,9 @@ extern "C" int mgsr_gs_sweeps(double *p, const double *f, int64_t n, double h2, 
                               size_t ws_bytes, void *stream) {
     if (n < 2 || !p || !f || sweeps < 0) { set_error("sweep count must be >= 0"); return MGSR_E_BAD_ARG; }
     if (n % 2) { set_error("red-black coloring needs an even side, got " + std::to_string(n)); return MGSR_E_ODD_SIDE; }
-    if (int r = check_ws(ws, ws_bytes)) return r;
-    if (sweeps == 0) return MGSR_OK;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (int r = check_ws(ws, ws_bytes, st)) return r;
+    if (sweeps == 0) return MGSR_OK;
     double *scal = static_cast<double *>(ws);
     void *red = static_cast<char *>(ws) + 256;
     FSrc fs{f, nullptr, 1.0};
@@ -1378,8 +1377,8 @@ extern "C" int mgsr_laplacian(const double *p, double *out, int64_t n, double in
 extern "C" int mgsr_residual(const double *p, const double *f, double *r, int64_t n, void *ws, size_t ws_bytes,
                              void *stream) {
     if (n < 2 || !p || !f || !r) { set_error("bad argument"); return MGSR_E_BAD_ARG; }
-    if (int e = check_ws(ws, ws_bytes)) return e;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (int e = check_ws(ws, ws_bytes, st)) return e;
     double *scal = static_cast<double *>(ws);
     RedSlot sl = red_slot_at(static_cast<char *>(ws) + 256);
     double h = 2.0 * M_PI / double(n);
@@ -1392,8 +1391,8 @@ extern "C" int mgsr_restrict(const double *fine, double *coarse, int64_t n, int3
                              void *ws, size_t ws_bytes, void *stream) {
     if (s < 2 || (s & (s - 1))) { set_error("transfer ratio must be a power of two >= 2, got " + std::to_string(s)); return MGSR_E_RATIO; }
     if (n % s) { set_error("fine side " + std::to_string(n) + " is not divisible by ratio " + std::to_string(s)); return MGSR_E_NOT_DIVISIBLE; }
-    if (int e = check_ws(ws, ws_bytes)) return e;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (int e = check_ws(ws, ws_bytes, st)) return e;
     double *scal = static_cast<double *>(ws);
     RedSlot sl = red_slot_at(static_cast<char *>(ws) + 256);
     int64_t nc = n / s;
@@ -1412,8 +1411,8 @@ extern "C" int mgsr_spline_prolong(const double *c, int64_t nc, int32_t s, doubl
 
 extern "C" int mgsr_rms_diff(const double *a, const double *b, int64_t count, double *out_host, void *ws,
                              size_t ws_bytes, void *stream) {
-    if (int e = check_ws(ws, ws_bytes)) return e;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (int e = check_ws(ws, ws_bytes, st)) return e;
     double *scal = static_cast<double *>(ws);
     RedSlot sl = red_slot_at(static_cast<char *>(ws) + 256);
     k_sqdiff<<<grid_for(count, 256), 256, 0, st>>>(a, b, count, sl, scal);
