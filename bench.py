@@ -273,9 +273,9 @@ def run_mine(args, rank: int, world: int, dist):
         raise RuntimeError(f"non-finite cycle statistics {stats}")
 
     # ---- end to end through the C ABI with pinned host buffers ----
-    # Every step copies its inputs host -> device and reads its result back; the copies run on a
-    # second stream and are double-buffered, so step i + 1's upload and step i's readback overlap
-    # the V-cycles (the timed region still contains every copy).
+    # Every step copies its inputs host -> device and reads its result back; uploads and readbacks run
+    # on two copy streams (the PCIe directions overlap) and are double-buffered, so step i + 1's
+    # upload and step i's readback overlap the V-cycles (the timed region still contains every copy).
     e2e = None
     if not args.no_e2e:
         hp = torch.from_numpy(p_np).pin_memory()
@@ -291,20 +291,23 @@ def run_mine(args, rank: int, world: int, dist):
             dfs[b].copy_(f)
             ops.vcycle_(dps[b], dfs[b], plan.handle, use_sr, dst[b])
         torch.cuda.synchronize()
-        cs = torch.cuda.Stream()
+        cs = torch.cuda.Stream()      # uploads
+        cs_dn = torch.cuda.Stream()   # readbacks: a separate stream, so the two PCIe directions overlap
         ev_in = [torch.cuda.Event() for _ in range(2)]
         ev_done = [torch.cuda.Event() for _ in range(2)]
+        ev_read = [torch.cuda.Event() for _ in range(2)]
         k2 = max(1, min(args.steps, 5))
         if dist is not None:
             dist.barrier()
         e0.record(st)
         cs.wait_stream(st)
+        cs_dn.wait_stream(st)
 
         def upload(i):
             b = i & 1
             with torch.cuda.stream(cs):
                 if i >= 2:
-                    cs.wait_event(ev_done[b])   # the cycle that last used buffer b has finished
+                    cs.wait_event(ev_read[b])   # the cycle that last used buffer b and its readback finished
                 dps[b].copy_(hp, non_blocking=True)
                 dfs[b].copy_(hf, non_blocking=True)
                 ev_in[b].record(cs)
@@ -317,11 +320,13 @@ def run_mine(args, rank: int, world: int, dist):
             ev_done[b].record(st)
             if i + 1 < k2:
                 upload(i + 1)
-            with torch.cuda.stream(cs):
-                cs.wait_event(ev_done[b])
+            with torch.cuda.stream(cs_dn):
+                cs_dn.wait_event(ev_done[b])
                 houts[b].copy_(dps[b], non_blocking=True)
                 hstats[b].copy_(dst[b], non_blocking=True)
+                ev_read[b].record(cs_dn)
         st.wait_stream(cs)
+        st.wait_stream(cs_dn)
         e1.record(st)
         torch.cuda.synchronize()
         e2e_ms = e0.elapsed_time(e1)
@@ -501,7 +506,7 @@ def main():
             line["e2e"] = {"value": replica_value(k2, ms, world), "unit": UNIT, "h2d_bytes_per_step": bi,
                            "d2h_bytes_per_step": bo,
                            "path": "pinned host p,f -> torch.ops.mgsr.vcycle_ (C ABI mgsr_plan_vcycle) -> host p; "
-                                   "copies on a second stream, double-buffered across steps"}
+                                   "uploads and readbacks on two copy streams, double-buffered across steps"}
         if not args.no_cpu_baseline:
             try:
                 cyc, kind, sample = cpu_reference_sample(n, args.blocks, 256, args.mode, args.sr_levels, wkind=args.weights)
