@@ -74,11 +74,16 @@ constexpr int PLANE_ROWS = GUARD + IMG_ROWS + GUARD;  // 528
 constexpr int ACT_PLANE = PLANE_ROWS * 16;            // bytes per 8-channel plane
 constexpr int ACT_BYTES = 8 * ACT_PLANE;              // 67584 per buffer
 // CTA pair (cta_group::2): the leader CTA issues M = 256 MMAs whose A rows come 128 from each CTA's
-// activations and whose B (N = 64 output channels) is split along N, 32 channels in each CTA's ring.
-constexpr int NSLOT = 16;                             // ring slots (> 9: next layer's first taps prefetch)
-constexpr int TAP_BYTES = 8192;                       // one 3x3 tap in the blob: [half][32 oc][64 ic] bf16
-constexpr int SLOT_BYTES = 4096;                      // this CTA's half of a tap
-constexpr int RING_BYTES = NSLOT * SLOT_BYTES;        // 65536
+// activations.  The three taps of a kernel row dy (dx = 0, 1, 2) are ONE MMA with N = 3 x 64 = 192: A is the
+// plane shifted by dy rows only and the accumulator holds y_dx[r] = sum_dy W(dy, dx) a[r + 64 (dy - 1)];
+// the epilogue forms out[r] = y_0[r - 1] + y_1[r] + y_2[r + 1] with lane shuffles (a row's px -+ 1
+// neighbours are the adjacent lanes), so A is read from shared memory 3 times per layer instead of 9.
+// B is split along N: each CTA's ring unit holds its 32 output channels for the 3 dx taps (N = 96).
+constexpr int NUNIT = 5;                              // ring units (> 3: the next layer's first rows prefetch)
+constexpr int TAP_BYTES = 8192;                       // one 3x3 tap in the blob (both 32-oc halves)
+constexpr int UNIT_BYTES = 3 * 4096;                  // this CTA's half of a kernel row: [dx 3][ng 4][kc 8][8 oc][8]
+constexpr int ROW_BYTES = 2 * UNIT_BYTES;             // a kernel row in the blob (both halves)
+constexpr int RING_BYTES = NUNIT * UNIT_BYTES;        // 61440
 constexpr int MISC_BYTES = 8192;                      // q tables (8 x 36 floats) + head im2col index table
 constexpr int BAR_BYTES = 1024;
 // head phase, in activation buffer 1 (free until layer 0's epilogue): im2col, two buffers
@@ -86,7 +91,7 @@ constexpr int HK = 96;                                   // head K (81 taps padd
 constexpr int HPLANES = HK / 8;                          // 12 planes of 8 fp16
 constexpr int I2C_BYTES = HPLANES * ROWS * 16;           // 24576 per im2col buffer (two buffers)
 constexpr int HB_BYTES = HPLANES * 64 * 16;              // 12288: two halves of 32 oc
-constexpr int HB_HALF = HB_BYTES / 2;                    // 6144, streamed through the ring (2 slots)
+constexpr int HB_HALF = HB_BYTES / 2;                    // 6144, streamed through the ring (one unit)
 constexpr int IDX_OFF = 2048;                            // in misc: uint8 [64 padded pixels][96 k] -> q index
 static_assert(2 * I2C_BYTES <= ACT_BYTES, "im2col");
 static_assert(WPG * 36 * 4 <= IDX_OFF && IDX_OFF + 64 * HK <= MISC_BYTES, "misc");
@@ -111,8 +116,9 @@ constexpr int OFF_RING = OFF_ACT + 2 * ACT_BYTES;
 constexpr int OFF_MISC = OFF_RING + RING_BYTES;
 constexpr int OFF_BAR = OFF_MISC + MISC_BYTES;
 constexpr int OFF_CONST = OFF_BAR + BAR_BYTES;
-// TMEM columns
-constexpr int COL_ACC = 0, COL_RES = 192, COL_SKIP = 384;
+// TMEM columns: two 192-column accumulator buffers (accumulator units alternate between them: head tiles,
+// body / post tiles, up-quarter tiles), then the packed global skip
+constexpr int COL_ACC = 0, ACC_COLS = 192, COL_SKIP = 384;
 constexpr int COL_Z = COL_SKIP;   // tail accumulators (32 per Z tile, 4 tiles) reuse the skip columns + the spare 32
 
 constexpr int NEPI = 16;                       // epilogue warps
@@ -135,8 +141,8 @@ __host__ __device__ inline BlobLayout blob_layout(int blocks) {
     L.nl = 2 * blocks + 1;
     L.head_b = 0;
     L.body = L.head_b + HB_BYTES;
-    L.up = L.body + size_t(L.nl) * 9 * TAP_BYTES;
-    L.tail = L.up + size_t(UP_QUARTERS) * 9 * TAP_BYTES;
+    L.up = L.body + size_t(L.nl) * 3 * ROW_BYTES;
+    L.tail = L.up + size_t(UP_QUARTERS) * 3 * ROW_BYTES;
     L.tail_f32 = L.tail + size_t(UP_QUARTERS) * TW_QBYTES;   // then [3][64][81] fp32 (edge kernel)
     L.consts = L.tail_f32 + sizeof(float) * 3 * 64 * 81;
     // fp16 operand set (body, up, tail) follows at +fmt_stride from the bf16 set
@@ -395,24 +401,23 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
     uint8_t *ubuf = act;              // up phase: U + tail weights in buffer 0
     // Barriers marked (leader) are waited on by the leader's MMA warp only and collect the arrivals of
     // both CTAs; (both) are signalled in both CTAs by the leader's multicast commits; the rest are local.
-    const uint32_t b_full = smem_u32(bars + 0);                     // [NSLOT] this CTA's ring slot landed
-    const uint32_t b_empty = smem_u32(bars + NSLOT);                // [NSLOT] (both) slot consumed
-    const uint32_t b_peerfull = smem_u32(bars + 2 * NSLOT);         // [NSLOT] (leader) peer's slot landed
-    constexpr int BB = 3 * NSLOT;
-    const uint32_t b_acc_full = smem_u32(bars + BB + 0);    // [T] (both) MMA -> epilogue: accumulator ready
-    const uint32_t b_act_ready = smem_u32(bars + BB + 3);   // [T] (leader) epilogues -> MMA: tile's rows written
-    const uint32_t b_acc_full2 = smem_u32(bars + BB + 6);   // [T] (both) MMA -> drain: up accumulator buffer 1 ready
-    const uint32_t b_drained = smem_u32(bars + BB + 9);     // [2][T] (leader) drain warps -> MMA: up buffer free
-    const uint32_t b_i2c_full = smem_u32(bars + BB + 15);   // [2] (leader) im2col buffer built (both CTAs)
-    const uint32_t b_i2c_empty = smem_u32(bars + BB + 17);  // [2] (both) im2col buffer consumed
-    const uint32_t b_ubuf_full = smem_u32(bars + BB + 19);  // (leader) drains -> MMA: the quarter's U written
-    const uint32_t b_ubuf_free = smem_u32(bars + BB + 20);  // (both) tail MMAs -> drains: U consumed
-    const uint32_t b_zfull = smem_u32(bars + BB + 21);      // [ZT] (both) last tail MMAs -> epilogue: Z ready
-    const uint32_t b_tw_full = smem_u32(bars + BB + 25);    // [4] this CTA's quarter tail weights landed
-    const uint32_t b_tw_peerfull = smem_u32(bars + BB + 29);   // [4] (leader) the peer's landed
-    const uint32_t b_tw_empty = smem_u32(bars + BB + 33);   // [4] (both) tail MMAs of the quarter done
-    const uint32_t b_post_done = smem_u32(bars + BB + 37);  // (both) post layer's MMAs done: buffer 0 free
-    static_assert((BB + 38) * 8 <= BAR_BYTES - 8, "barriers");
+    const uint32_t b_full = smem_u32(bars + 0);                     // [NUNIT] this CTA's ring unit landed
+    const uint32_t b_empty = smem_u32(bars + NUNIT);                // [NUNIT] (both) unit consumed
+    const uint32_t b_peerfull = smem_u32(bars + 2 * NUNIT);         // [NUNIT] (leader) peer's unit landed
+    constexpr int BB = 3 * NUNIT;
+    const uint32_t b_acc_full = smem_u32(bars + BB + 0);    // [2] (both) MMA -> epilogue: accumulator buffer ready
+    const uint32_t b_drained = smem_u32(bars + BB + 2);     // [2] (leader) epilogues -> MMA: accumulator buffer read
+    const uint32_t b_act_ready = smem_u32(bars + BB + 4);   // [T] (leader) epilogues -> MMA: tile's rows written
+    const uint32_t b_i2c_full = smem_u32(bars + BB + 7);    // [2] (leader) im2col buffer built (both CTAs)
+    const uint32_t b_i2c_empty = smem_u32(bars + BB + 9);   // [2] (both) im2col buffer consumed
+    const uint32_t b_ubuf_full = smem_u32(bars + BB + 11);  // (leader) drains -> MMA: the quarter's U written
+    const uint32_t b_ubuf_free = smem_u32(bars + BB + 12);  // (both) tail MMAs -> drains: U consumed
+    const uint32_t b_zfull = smem_u32(bars + BB + 13);      // [ZT] (both) last tail MMAs -> epilogue: Z ready
+    const uint32_t b_tw_full = smem_u32(bars + BB + 17);    // [4] this CTA's quarter tail weights landed
+    const uint32_t b_tw_peerfull = smem_u32(bars + BB + 21);   // [4] (leader) the peer's landed
+    const uint32_t b_tw_empty = smem_u32(bars + BB + 25);   // [4] (both) tail MMAs of the quarter done
+    const uint32_t b_post_done = smem_u32(bars + BB + 29);  // (both) post layer's MMAs done: buffer 0 free
+    static_assert((BB + 30) * 8 <= BAR_BYTES - 8, "barriers");
     const uint32_t rank = cluster_rank();
     const bool leader = rank == 0;
     const int pair = int(blockIdx.x >> 1), npairs = int(gridDim.x >> 1);
@@ -429,7 +434,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
         for (int i = threadIdx.x; i < const_floats(NL) / 4; i += NTHREADS) dst[i] = src[i];
     }
     if (threadIdx.x == 0) {
-        for (int s = 0; s < NSLOT; ++s) {
+        for (int s = 0; s < NUNIT; ++s) {
             mbar_init(b_full + 8 * s, 1);
             mbar_init(b_empty + 8 * s, 1);
             mbar_init(b_peerfull + 8 * s, 1);
@@ -438,13 +443,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
             mbar_init(b_i2c_full + 8 * b2, 2);
             mbar_init(b_i2c_empty + 8 * b2, 1);
         }
-        for (int t = 0; t < T; ++t) {
-            mbar_init(b_acc_full + 8 * t, 1);
-            mbar_init(b_act_ready + 8 * t, 2 * NEPI);
-            mbar_init(b_drained + 8 * t, 2 * NEPI);
-            mbar_init(b_acc_full2 + 8 * t, 1);
-            mbar_init(b_drained + 8 * (T + t), 2 * NEPI);
+        for (int b2 = 0; b2 < 2; ++b2) {
+            mbar_init(b_acc_full + 8 * b2, 1);
+            mbar_init(b_drained + 8 * b2, 2 * NEPI);
         }
+        for (int t = 0; t < T; ++t) mbar_init(b_act_ready + 8 * t, 2 * NEPI);
         mbar_init(b_ubuf_full, 2 * NEPI);
         mbar_init(b_ubuf_free, 1);
         mbar_init(b_post_done, 1);
@@ -468,29 +471,28 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
 
     if (warp == 0) {
         // ================= weight producer =================
-        uint32_t ph = 0;   // bit s = fill parity of slot s
-        int slot = 0;      // taps stream through the ring in order: slot = global tap index mod NSLOT
+        uint32_t ph = 0;   // bit s = fill parity of unit s
+        int slot = 0;      // kernel rows stream through the ring in order: unit = global row index mod NUNIT
         uint32_t tw_ph[UP_QUARTERS_C] = {0, 0, 0, 0};
         uint32_t grp_ph = 0;
-        auto fill = [&](const uint8_t *src, uint32_t bytes = SLOT_BYTES) {
+        auto fill = [&](const uint8_t *src, uint32_t bytes = UNIT_BYTES) {
             mbar_wait(b_empty + 8 * slot, ((ph >> slot) & 1u) ^ 1u);
             if (elect_one()) {
                 mbar_expect_tx(b_full + 8 * slot, bytes);
-                bulk_g2s(smem_u32(ring + slot * SLOT_BYTES), src, bytes, b_full + 8 * slot);
+                bulk_g2s(smem_u32(ring + slot * UNIT_BYTES), src, bytes, b_full + 8 * slot);
             }
             __syncwarp();
             ph ^= 1u << slot;
-            slot = slot == NSLOT - 1 ? 0 : slot + 1;
+            slot = slot == NUNIT - 1 ? 0 : slot + 1;
         };
         for (int gp = pair; gp < ngp; gp += npairs) {
-            for (int h = 0; h < 2; ++h)   // this CTA's half of the head weights: planes 0-7, 8-11
-                fill(wblob + BL.head_b + rank * HB_HALF + h * SLOT_BYTES, h < 1 ? SLOT_BYTES : HB_HALF - SLOT_BYTES);
+            fill(wblob + BL.head_b + rank * HB_HALF, HB_HALF);   // this CTA's half of the head weights
             for (int L = 0; L < NLAYERS; ++L)
-                for (int tap = 0; tap < 9; ++tap)
-                    fill(wblob + P.wfmt + BL.body + (size_t(L) * 9 + tap) * TAP_BYTES + rank * SLOT_BYTES);
+                for (int dy = 0; dy < 3; ++dy)
+                    fill(wblob + P.wfmt + BL.body + (size_t(L) * 3 + dy) * ROW_BYTES + rank * UNIT_BYTES);
             for (int u = 0; u < UP_QUARTERS; ++u) {
-                for (int tap = 0; tap < 9; ++tap)
-                    fill(wblob + P.wfmt + BL.up + (size_t(u) * 9 + tap) * TAP_BYTES + rank * SLOT_BYTES);
+                for (int dy = 0; dy < 3; ++dy)
+                    fill(wblob + P.wfmt + BL.up + (size_t(u) * 3 + dy) * ROW_BYTES + rank * UNIT_BYTES);
                 // this CTA's half of the quarter's tail weights -> buffer 0, once the post layer's MMAs
                 // released it and the last group's tail MMAs of quarter u completed
                 if (u == 0) mbar_wait(b_post_done, grp_ph);
@@ -515,13 +517,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
                 if (elect_one()) mbar_arrive_leader(b_peerfull + 8 * slot);
                 __syncwarp();
                 ph ^= 1u << slot;
-                slot = slot == NSLOT - 1 ? 0 : slot + 1;
+                slot = slot == NUNIT - 1 ? 0 : slot + 1;
             }
         };
         for (int gp = pair; gp < ngp; gp += npairs) {   // same order as the producer's fills
-            fwd(2 + NLAYERS * 9);
+            fwd(1 + NLAYERS * 3);
             for (int u = 0; u < UP_QUARTERS; ++u) {
-                fwd(9);
+                fwd(3);
                 mbar_wait(b_tw_full + 8 * u, twp);
                 if (elect_one()) mbar_arrive_leader(b_tw_peerfull + 8 * u);
                 __syncwarp();
@@ -531,75 +533,74 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
     } else if (warp == 1) {
         // ================= MMA issuer (leader; warp-uniform control, one elected lane issues) =================
         uint32_t ph = 0, i2c_ph = 0;   // i2c_ph bit b: parity of the next completion of b_i2c_full[b]
-        int slot0 = 0;   // ring slot of tap 0 of the current layer
+        int slot0 = 0;   // ring unit of kernel row 0 of the current layer
         uint32_t ar_ph = 0;   // bit t: parity of the next completion of b_act_ready[t]
-        uint32_t dr_ph = 0;   // bit t: parity of the next completion of b_drained[0][t]
+        uint32_t dr_ph = 0;   // bit b: parity of the next completion of b_drained[b]
+        int vb = 0;           // accumulator buffer of the next accumulator unit (units alternate buffers)
         const uint32_t act_base = smem_u32(act), ring_base = smem_u32(ring);
         const uint32_t i2c_base = smem_u32(i2c), u_base = smem_u32(ubuf);
-        const uint32_t id64 = F16 ? idesc_f16(64) : idesc_bf16(64);
-        const uint64_t b_desc0 = make_desc(ring_base, 512, 128);         // half tap: 32-row planes
+        const uint32_t id192 = F16 ? idesc_f16(192) : idesc_bf16(192);
         Tracer<INSTR> tr{nullptr, 0};
         auto wait_ar = [&](int t) {
             mbar_wait(b_act_ready + 8 * t, (ar_ph >> t) & 1u);
             ar_ph ^= 1u << t;
         };
-        // one N = 64 3x3 layer over the three tiles (body, post, up quarter), reading buffer `buf`
-        // wait: 0 = act_ready (the rows this tile's taps read are written: tiles t - 1..t + 1), 1 = none,
-        // 2/3 = up accumulator buffer 0/1 of this tile drained
-        auto conv_layer = [&](int lid, int buf, int wait, uint32_t dcol, auto &&after_t0) {
+        // the accumulator buffer of the next unit was read by the epilogue of the unit two before
+        auto acquire_acc = [&] {
+            mbar_wait(b_drained + 8 * vb, (dr_ph >> vb) & 1u);
+            dr_ph ^= 1u << vb;
+        };
+        // one 3x3 64 -> 64 layer over the three tiles (body, post, up quarter), reading buffer `buf`: per tile
+        // three N = 192 MMAs chains (kernel rows dy) of K = 64; wait_act: the rows this tile's taps read
+        // (tiles t - 1..t + 1) are written
+        auto conv_layer = [&](int lid, int buf, bool wait_act, auto &&after_t0) {
             const uint64_t a_desc0 = make_desc(act_base + buf * ACT_BYTES, ACT_PLANE, 128);
 #pragma unroll
             for (int t = 0; t < T; ++t) {
-                if (wait == 0) {
+                if (wait_act) {
                     if (t == 0) { wait_ar(0); wait_ar(1); }
                     else if (t == 1) wait_ar(2);
-                } else if (wait == 2) {   // buffer 0: waited at every completion (u = 2 here, head next group)
-                    mbar_wait(b_drained + 8 * t, (dr_ph >> t) & 1u);
-                    dr_ph ^= 1u << t;
-                } else if (wait == 3) {   // buffer 1 completes twice per group (u = 1, 3 drained); only the
-                    mbar_wait(b_drained + 8 * (T + t), 0u);   // first is waited: always an even completion
                 }
+                acquire_acc();
                 if (lane == 0) tr(2, lid, t);
                 tc_fence_after();
                 const uint64_t a_t = a_desc0 + uint64_t(GUARD + (2 * t + 1) * 64);
-                const uint32_t d = tmem + dcol + 64 * t;
+                const uint32_t d = tmem + COL_ACC + ACC_COLS * vb;
                 if (elect_one()) {
 #pragma unroll
-                    for (int tap = 0; tap < 9; ++tap) {
-                        int s = slot0 + tap;
-                        s = s >= NSLOT ? s - NSLOT : s;
+                    for (int dy = 0; dy < 3; ++dy) {
+                        int s = slot0 + dy;
+                        s = s >= NUNIT ? s - NUNIT : s;
                         if (t == 0) {
                             mbar_wait(b_full + 8 * s, (ph >> s) & 1u);
                             mbar_wait(b_peerfull + 8 * s, (ph >> s) & 1u);
-                            if (tap == 0) tr(4, lid, 0);
+                            if (dy == 0) tr(4, lid, 0);
                             tc_fence_after();
                         }
-                        const int shift = (tap / 3 - 1) * 64 + (tap % 3 - 1);
-                        const uint64_t a = a_t + uint64_t(int64_t(shift));
-                        const uint64_t b = b_desc0 + uint64_t(s * (SLOT_BYTES / 16));
+                        const uint64_t a = a_t + uint64_t(int64_t((dy - 1) * 64));
+                        const uint64_t b = make_desc(ring_base + s * UNIT_BYTES, 128, 1024);   // 12 n-groups of 8
 #pragma unroll
                         for (int ks = 0; ks < 4; ++ks)
-                            mma_bf16(d, a + uint64_t(ks * (2 * ACT_PLANE / 16)), b + uint64_t(ks * (2 * 512 / 16)),
-                                     id64, (tap | ks) > 0);
+                            mma_bf16(d, a + uint64_t(ks * (2 * ACT_PLANE / 16)), b + uint64_t(ks * (256 / 16)), id192,
+                                     (dy | ks) > 0);
                         if (t == T - 1) umma_commit(b_empty + 8 * s);
                     }
-                    // separate completion barriers per up buffer: a tile's two buffers may complete
-                    // back to back, which a single barrier could not tell apart
-                    umma_commit((dcol == COL_RES ? b_acc_full2 : b_acc_full) + 8 * t);
+                    umma_commit(b_acc_full + 8 * vb);
                     if (lid == NLAYERS && t == T - 1) umma_commit(b_post_done);   // buffer 0 no longer read
                 }
                 __syncwarp();
+                vb ^= 1;
                 if (lane == 0) tr(3, lid, t);
                 if (t == 0) after_t0();
             }
 #pragma unroll
-            for (int tap = 0; tap < 9; ++tap) {
-                int s = slot0 + tap;
-                s = s >= NSLOT ? s - NSLOT : s;
+            for (int dy = 0; dy < 3; ++dy) {
+                int s = slot0 + dy;
+                s = s >= NUNIT ? s - NUNIT : s;
                 ph ^= 1u << s;
             }
-            slot0 += 9;
-            slot0 = slot0 >= NSLOT ? slot0 - NSLOT : slot0;
+            slot0 += 3;
+            slot0 = slot0 >= NUNIT ? slot0 - NUNIT : slot0;
         };
         // pruned 9x9 tail, quarter u: Z[j] (M = 256 pixels of kept fine row 4 + j, N = 32 = 3 dx + o) +=
         // sum over dy of U shifted by j + dy fine rows x TW[u][dy]; 36 MMAs
@@ -633,56 +634,45 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
             // head: D[t] = im2col(q) (128 x 96, fp16) x Wh^T (96 x 64); im2col buffer t & 1
             for (int t = 0; t < T; ++t) {
                 const int ib = t & 1;
-                // the head accumulates into up buffer 0 of this tile (cols COL_ACC + 64 t)
-                mbar_wait(b_drained + 8 * t, (dr_ph >> t) & 1u);
-                dr_ph ^= 1u << t;
+                acquire_acc();
                 if (lane == 0) tr(2, 0, t);
                 mbar_wait(b_i2c_full + 8 * ib, (i2c_ph >> ib) & 1u);
                 if (lane == 0) tr(5, 0, t);
                 i2c_ph ^= 1u << ib;
                 tc_fence_after();
-                const uint32_t d = tmem + COL_ACC + 64 * t;
+                const uint32_t d = tmem + COL_ACC + ACC_COLS * vb;
                 if (elect_one()) {
+                    if (t == 0) {
+                        mbar_wait(b_full + 8 * slot0, (ph >> slot0) & 1u);
+                        mbar_wait(b_peerfull + 8 * slot0, (ph >> slot0) & 1u);
+                        tc_fence_after();
+                    }
 #pragma unroll
                     for (int ks = 0; ks < HK / 16; ++ks) {
-                        int sl = slot0 + (ks >> 2);
-                        sl = sl >= NSLOT ? sl - NSLOT : sl;
-                        if (t == 0 && (ks & 3) == 0) {
-                            mbar_wait(b_full + 8 * sl, (ph >> sl) & 1u);
-                            mbar_wait(b_peerfull + 8 * sl, (ph >> sl) & 1u);
-                            tc_fence_after();
-                        }
                         uint64_t a = make_desc(i2c_base + ib * I2C_BYTES + 2 * ks * (ROWS * 16), ROWS * 16, 128);
-                        uint64_t b = make_desc(ring_base + sl * SLOT_BYTES + (ks & 3) * 1024, 32 * 16, 128);
+                        uint64_t b = make_desc(ring_base + slot0 * UNIT_BYTES + ks * 1024, 32 * 16, 128);
                         mma_bf16(d, a, b, idesc_f16(64), ks > 0);
-                        if (t == T - 1 && ((ks & 3) == 3 || ks == HK / 16 - 1)) umma_commit(b_empty + 8 * sl);
                     }
-                    umma_commit(b_acc_full + 8 * t);
+                    if (t == T - 1) umma_commit(b_empty + 8 * slot0);
+                    umma_commit(b_acc_full + 8 * vb);
                     umma_commit(b_i2c_empty + 8 * ib);
                 }
                 __syncwarp();
+                vb ^= 1;
                 if (lane == 0) tr(3, 0, t);
             }
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                int sl = slot0 + h;
-                sl = sl >= NSLOT ? sl - NSLOT : sl;
-                ph ^= 1u << sl;
-            }
-            slot0 += 2;
-            slot0 = slot0 >= NSLOT ? slot0 - NSLOT : slot0;
+            ph ^= 1u << slot0;
+            slot0 = slot0 == NUNIT - 1 ? 0 : slot0 + 1;
             auto none = [] {};
 #pragma unroll 1
-            for (int L = 0; L < NLAYERS; ++L) conv_layer(L + 1, L & 1, 0, COL_ACC, none);
-            // up quarters (reading buffer NL & 1 = 1), accumulators double-buffered over cols [0, 192) and
-            // [192, 384) (the residual stream and skip are dead after the post layer): quarter u + 1 runs
-            // while u drains; the tail of quarter u issues after tile 0 of up quarter u + 1 (u is drained
-            // into U by then), so it completes before that quarter's tiles 1, 2 and the drain of u + 1
-            // (which rewrites U) overlaps their MMAs
-            conv_layer(40, 1, 0, COL_ACC, none);
-            conv_layer(41, 1, 1, COL_RES, [&] { tail_mma(0); });
-            conv_layer(42, 1, 2, COL_ACC, [&] { tail_mma(1); });
-            conv_layer(43, 1, 3, COL_RES, [&] { tail_mma(2); });
+            for (int L = 0; L < NLAYERS; ++L) conv_layer(L + 1, L & 1, true, none);
+            // up quarters (reading buffer NL & 1 = 1); the tail of quarter u issues after tile 0 of up
+            // quarter u + 1 (u is drained into U by then), so it completes before that quarter's tiles 1, 2
+            // and the drain of u + 1 (which rewrites U) overlaps their MMAs
+            conv_layer(40, 1, true, none);
+            conv_layer(41, 1, false, [&] { tail_mma(0); });
+            conv_layer(42, 1, false, [&] { tail_mma(1); });
+            conv_layer(43, 1, false, [&] { tail_mma(2); });
             tail_mma(3);
             grp_ph ^= 1u;
         }
@@ -696,13 +686,43 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
         const int row = 32 * q + lane;         // row within a tile
         const int pyl = row >> 6, wrow = (row >> 3) & 7, px = row & 7;   // tile row = (py - 2 t - 1, window, px)
         const bool interior = px >= 1 && px <= 6;
-        // lane holding the interior pixel this pad column replicates (itself when interior): same warp
-        const int pad_src = lane + (px == 0 ? 1 : (px == 7 ? -1 : 0));
         const uint32_t lane_addr = uint32_t(32 * q) << 16;
-        uint32_t af_ph[T] = {0, 0, 0};
+        uint32_t af_ph = 0;   // bit b: parity of the next completion of b_acc_full[b]
+        int vb = 0;           // accumulator buffer of the next unit (the MMA warp's order)
         int i2c_uses[2] = {0, 0};   // builds into im2col buffer b so far
         if (lane == 0)
-            for (int t = 0; t < T; ++t) mbar_arrive_leader(b_drained + 8 * t);   // up buffer 0 (= head accumulator) starts free
+            for (int b2 = 0; b2 < 2; ++b2) mbar_arrive_leader(b_drained + 8 * b2);   // both buffers start free
+        // wait for the next accumulator unit; returns this lane's TMEM address of its buffer
+        auto acc_wait = [&]() -> uint32_t {
+            mbar_wait(b_acc_full + 8 * vb, (af_ph >> vb) & 1u);
+            af_ph ^= 1u << vb;
+            tc_fence_after();
+            return tmem + lane_addr + COL_ACC + ACC_COLS * vb;
+        };
+        auto acc_release = [&] {   // this warp has read the unit's accumulator
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_leader(b_drained + 8 * vb);
+            vb ^= 1;
+        };
+        // a 3x3 unit: columns n = 96 h + 32 dx + oc' (h = output-channel half); out[r] = y_0[r - 1] + y_1[r]
+        // + y_2[r + 1], the row's px -+ 1 neighbours being lanes -+ 1.  Replicate padding: the pad column
+        // px = 0 equals px = 1, so the y_0 px = 1 needs is its own (and px = 6 takes its own y_2): the pad rows'
+        // results are never used and their activations are dead data.  One indexed shuffle per partial.
+        const int src_l = px == 1 ? lane : lane - 1, src_r = px == 6 ? lane : lane + 1;
+        auto load_dx3 = [&](float (&y)[16]) {
+            const uint32_t c = acc_wait() + (cq >> 1) * 96 + (cq & 1) * 16;
+            uint32_t v0[16], v1[16], v2[16];
+            TMEM_LD16(c, v0);
+            TMEM_LD16(c + 32, v1);
+            TMEM_LD16(c + 64, v2);
+            tmem_wait_ld();
+            acc_release();
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+                y[j] = (__uint_as_float(v1[j]) + __shfl_sync(0xffffffffu, __uint_as_float(v0[j]), src_l)) +
+                       __shfl_sync(0xffffffffu, __uint_as_float(v2[j]), src_r);
+        };
         const float *head_a = cs;
         uint8_t *idx_tab = reinterpret_cast<uint8_t *>(smem + OFF_MISC + IDX_OFF);
         for (int i = et; i < 64 * HK; i += 32 * NEPI) {   // im2col index table (replicate-clamped 9x9 taps)
@@ -718,7 +738,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
         const float *up_a = cs + 64 + 192 * NL;
         const float *tail_b = up_a + 64;
         Tracer<INSTR> tr{nullptr, 0};
-        uint32_t af2_ph = 0;   // bit t = parity of the next completion of b_acc_full2[t]
         uint32_t z_ph = 0;     // parity of the next completion of b_zfull (one per group)
         // q tables of a group's 8 windows (fp64 normalise -> fp32) -> misc
         auto load_q = [&](int gq) {
@@ -780,15 +799,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
             for (int L = -1; L < NL; ++L) {
                 uint8_t *obuf = act + ((L + 1) & 1) * ACT_BYTES;
                 for (int t = 0; t < T; ++t) {
-                    mbar_wait(b_acc_full + 8 * t, af_ph[t]);
                     tr(6, L + 1, t);
-                    af_ph[t] ^= 1;
-                    tc_fence_after();
-                    uint32_t v[16];
-                    TMEM_LD16(tmem + lane_addr + COL_ACC + 64 * t + cb, v);
-                    tmem_wait_ld();
+                    // this thread's row of the output buffer (for a residual block's second conv it holds the
+                    // block input x_k: the fp16 residual stream, updated in place)
+                    uint8_t *dst = obuf + (2 * cq) * ACT_PLANE + (GUARD + (2 * t + 1) * 64 + row) * 16;
                     float y[16];
                     if (L < 0) {
+                        uint32_t v[16];
+                        TMEM_LD16(acc_wait() + cb, v);
+                        tmem_wait_ld();
+                        acc_release();
                         float al[16];
                         lds16(head_a + cb, al);
 #pragma unroll
@@ -796,12 +816,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
                             float x = __uint_as_float(v[j]);
                             y[j] = x > 0.f ? x : al[j] * x;
                         }
-                        uint32_t st[16], sk[8];
-#pragma unroll
-                        for (int j = 0; j < 16; ++j) st[j] = __float_as_uint(y[j]);
+                        uint32_t sk[8];
 #pragma unroll
                         for (int j = 0; j < 8; ++j) sk[j] = pack_op<F16>(y[2 * j], y[2 * j + 1]);
-                        TMEM_ST16(tmem + lane_addr + COL_RES + 64 * t + cb, st);
                         TMEM_ST8(tmem + lane_addr + COL_SKIP + 32 * t + 8 * cq, sk);
                         tmem_wait_st();
                     } else {
@@ -810,47 +827,43 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
                         const bool post = L == NL - 1;
                         float kb[16];   // BN scale is folded into the packed weights; shift remains
                         lds16(sc + 64 + cb, kb);
+                        float a[16];
+                        load_dx3(a);
                         if (conv1) {
                             float al[16];
                             lds16(sc + 128 + cb, al);
 #pragma unroll
                             for (int j = 0; j < 16; ++j) {
-                                float x = __uint_as_float(v[j]) + kb[j];
+                                float x = a[j] + kb[j];
                                 y[j] = x > 0.f ? x : al[j] * x;
                             }
                         } else if (!post) {
-                            uint32_t rv[16];
-                            TMEM_LD16(tmem + lane_addr + COL_RES + 64 * t + cb, rv);
-                            tmem_wait_ld();
+                            const uint4 r0 = *reinterpret_cast<const uint4 *>(dst);
+                            const uint4 r1 = *reinterpret_cast<const uint4 *>(dst + ACT_PLANE);
+                            const uint32_t rv[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
 #pragma unroll
-                            for (int j = 0; j < 16; ++j)
-                                y[j] = __uint_as_float(rv[j]) + (__uint_as_float(v[j]) + kb[j]);
-                            uint32_t st[16];
-#pragma unroll
-                            for (int j = 0; j < 16; ++j) st[j] = __float_as_uint(y[j]);
-                            TMEM_ST16(tmem + lane_addr + COL_RES + 64 * t + cb, st);
-                            tmem_wait_st();
+                            for (int e = 0; e < 8; ++e) {
+                                y[2 * e] = op_lo<F16>(rv[e]) + (a[2 * e] + kb[2 * e]);
+                                y[2 * e + 1] = op_hi<F16>(rv[e]) + (a[2 * e + 1] + kb[2 * e + 1]);
+                            }
                         } else {
                             uint32_t sk[8];
                             TMEM_LD8(tmem + lane_addr + COL_SKIP + 32 * t + 8 * cq, sk);
                             tmem_wait_ld();
 #pragma unroll
                             for (int e = 0; e < 8; ++e) {
-                                y[2 * e] = (__uint_as_float(v[2 * e]) + kb[2 * e]) + op_lo<F16>(sk[e]);
-                                y[2 * e + 1] = (__uint_as_float(v[2 * e + 1]) + kb[2 * e + 1]) + op_hi<F16>(sk[e]);
+                                y[2 * e] = (a[2 * e] + kb[2 * e]) + op_lo<F16>(sk[e]);
+                                y[2 * e + 1] = (a[2 * e + 1] + kb[2 * e + 1]) + op_hi<F16>(sk[e]);
                             }
                         }
                     }
                     uint32_t pk[8];
 #pragma unroll
                     for (int j = 0; j < 8; ++j) pk[j] = pack_op<F16>(y[2 * j], y[2 * j + 1]);
-                    {   // replicate padding without partial stores: a pad column takes the packed values of its
-                        // interior neighbour (lane +-1) by shuffle, then every lane writes its own row; the first
-                        // and last image rows (tiles 0 and 2) also write the pad rows py = 0 and 7
-                        uint32_t sv[8];
-#pragma unroll
-                        for (int j = 0; j < 8; ++j) sv[j] = __shfl_sync(0xffffffffu, pk[j], pad_src);
-                        uint8_t *dst = obuf + (2 * cq) * ACT_PLANE + (GUARD + (2 * t + 1) * 64 + row) * 16;
+                    {   // every lane writes its own row (the pad columns px = 0, 7 are dead data, see load_dx3); the
+                        // first and last image rows (tiles 0 and 2) also write the pad rows py = 0 and 7 (the kernel
+                        // rows dy = 0, 2 read them)
+                        const uint32_t *sv = pk;
                         const uint4 v0 = make_uint4(sv[0], sv[1], sv[2], sv[3]), v1 = make_uint4(sv[4], sv[5], sv[6], sv[7]);
                         *reinterpret_cast<uint4 *>(dst) = v0;
                         *reinterpret_cast<uint4 *>(dst + ACT_PLANE) = v1;
@@ -885,21 +898,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
                 for (int m = 0; m < 4; ++m) ua[m] = up_a[UQ * u + 4 * cq + m];
 #pragma unroll
                 for (int t = 0; t < T; ++t) {
-                    if (u & 1) {
-                        mbar_wait(b_acc_full2 + 8 * t, (af2_ph >> t) & 1u);
-                        af2_ph ^= 1u << t;
-                    } else {
-                        mbar_wait(b_acc_full + 8 * t, af_ph[t]);
-                        af_ph[t] ^= 1;
-                    }
                     tr(8, u, t);
-                    tc_fence_after();
-                    uint32_t v[16];
-                    TMEM_LD16(tmem + lane_addr + (u & 1 ? COL_RES : COL_ACC) + 64 * t + cb, v);
-                    tmem_wait_ld();
-                    tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive_leader(b_drained + 8 * ((u & 1) * T + t));
+                    float a[16];
+                    load_dx3(a);
                     if (u > 0 && t == 0) mbar_wait(b_ubuf_free, uint32_t(u - 1) & 1u);
                     tr(9, u, t);
                     if (interior) {
@@ -908,7 +909,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
                         float y[16];
 #pragma unroll
                         for (int j = 0; j < 16; ++j) {
-                            const float x = __uint_as_float(v[j]);
+                            const float x = a[j];
                             y[j] = x > 0.f ? x : ua[j >> 2] * x;
                         }
                         uint8_t *Ub = ubuf + (cq >> 1) * U_PLANE + 8 * (cq & 1);
@@ -1191,20 +1192,22 @@ int tc_pack_weights(mgsr_gen *g, const float *const *t) {
     // BN(conv(x)) = conv(x; W * k) + (beta - mean * k), k = gamma / sqrt(var + 1e-5): the scale is
     // folded into the packed weights (per output channel), the shift stays in the epilogue.
     auto bn_scale = [&](int gi, int oc) { return double(t[gi][oc]) / std::sqrt(double(t[gi + 3][oc]) + 1e-5); };
-    auto pack_tap = [&](uint16_t *dst, const float *w, int oc0, int tap, int bn_gi) {
-        int dy = tap / 3, dx = tap % 3;
+    // kernel row dy of a 3x3 64 -> 64 conv (output channels oc0..oc0 + 63): [half][dx 3][ng 4][kc 8][8 oc][8 ic],
+    // so a CTA's unit is one K-major B operand of N = 96 rows (n = 32 dx + oc') with 8-row groups 1 KB apart
+    auto pack_row = [&](uint16_t *dst, const float *w, int oc0, int dy, int bn_gi) {
         uint16_t *dst16 = reinterpret_cast<uint16_t *>(reinterpret_cast<uint8_t *>(dst) + BL.fmt_stride);
-        for (int kc = 0; kc < 8; ++kc)
-            for (int oc = 0; oc < 64; ++oc) {
-                const double k = bn_gi >= 0 ? bn_scale(bn_gi, oc0 + oc) : 1.0;
-                for (int e = 0; e < 8; ++e) {
-                    int ic = 8 * kc + e;
-                    const float v = float(double(w[(((oc0 + oc) * 64 + ic) * 3 + dy) * 3 + dx]) * k);
-                    const int o = (((oc >> 5) * 8 + kc) * 32 + (oc & 31)) * 8 + e;   // [half][kc][32 oc][8]
-                    dst[o] = f2bf(v);
-                    dst16[o] = f2h(v);
+        for (int dx = 0; dx < 3; ++dx)
+            for (int kc = 0; kc < 8; ++kc)
+                for (int oc = 0; oc < 64; ++oc) {
+                    const double k = bn_gi >= 0 ? bn_scale(bn_gi, oc0 + oc) : 1.0;
+                    for (int e = 0; e < 8; ++e) {
+                        int ic = 8 * kc + e;
+                        const float v = float(double(w[(((oc0 + oc) * 64 + ic) * 3 + dy) * 3 + dx]) * k);
+                        const int o = (((((oc >> 5) * 3 + dx) * 4 + ((oc & 31) >> 3)) * 8 + kc) * 8 + (oc & 7)) * 8 + e;
+                        dst[o] = f2bf(v);
+                        dst16[o] = f2h(v);
+                    }
                 }
-            }
     };
     const int ip = 2 + 11 * B;   // post conv index
     auto bn_index = [&](int L) -> int {   // tensor index of body layer L's BN gamma
@@ -1212,13 +1215,13 @@ int tc_pack_weights(mgsr_gen *g, const float *const *t) {
         return 2 + 11 * (L / 2) + ((L & 1) ? 7 : 1);
     };
     for (int L = 0; L < BL.nl; ++L)
-        for (int tap = 0; tap < 9; ++tap)
-            pack_tap(reinterpret_cast<uint16_t *>(blob.data() + BL.body + (size_t(L) * 9 + tap) * TAP_BYTES),
-                     t[conv_index(L)], 0, tap, bn_index(L));
+        for (int dy = 0; dy < 3; ++dy)
+            pack_row(reinterpret_cast<uint16_t *>(blob.data() + BL.body + (size_t(L) * 3 + dy) * ROW_BYTES),
+                     t[conv_index(L)], 0, dy, bn_index(L));
     for (int u = 0; u < UP_QUARTERS; ++u)
-        for (int tap = 0; tap < 9; ++tap)
-            pack_tap(reinterpret_cast<uint16_t *>(blob.data() + BL.up + (size_t(u) * 9 + tap) * TAP_BYTES),
-                     t[ip + 5], 64 * u, tap, -1);
+        for (int dy = 0; dy < 3; ++dy)
+            pack_row(reinterpret_cast<uint16_t *>(blob.data() + BL.up + (size_t(u) * 3 + dy) * ROW_BYTES),
+                     t[ip + 5], 64 * u, dy, -1);
     {
         // tail B operand: per quarter u and CTA half h, [dy 9][k 2][16 n][8] with n = 16 h + n' = 3 dx + o
         // (27 of 32 used) and k = shuffled channel 16 u + 8 k + e
