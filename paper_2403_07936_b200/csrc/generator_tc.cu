@@ -541,26 +541,21 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
         const uint32_t i2c_base = smem_u32(i2c), u_base = smem_u32(ubuf);
         const uint32_t id192 = F16 ? idesc_f16(192) : idesc_bf16(192);
         Tracer<INSTR> tr{nullptr, 0};
-        auto wait_ar = [&](int t) {
-            mbar_wait(b_act_ready + 8 * t, (ar_ph >> t) & 1u);
-            ar_ph ^= 1u << t;
-        };
         // the accumulator buffer of the next unit was read by the epilogue of the unit two before
         auto acquire_acc = [&] {
             mbar_wait(b_drained + 8 * vb, (dr_ph >> vb) & 1u);
             dr_ph ^= 1u << vb;
         };
         // one 3x3 64 -> 64 layer over the three tiles (body, post, up quarter), reading buffer `buf`: per tile
-        // three N = 192 MMAs chains (kernel rows dy) of K = 64; wait_act: the rows this tile's taps read
-        // (tiles t - 1..t + 1) are written
+        // three N = 192 MMA chains (kernel rows dy) of K = 64.  wait_act: the rows each kernel row reads are
+        // written -- tile t's rows dy = 0, 1 read padded rows 2t .. 2t + 2 (tiles <= t), only dy = 2 reaches
+        // row 2t + 3 of tile t + 1, so the previous layer's tile t + 1 epilogue is waited for just before it
+        // (two thirds of a tile's MMAs of extra slack for the epilogue)
         auto conv_layer = [&](int lid, int buf, bool wait_act, auto &&after_t0) {
             const uint64_t a_desc0 = make_desc(act_base + buf * ACT_BYTES, ACT_PLANE, 128);
 #pragma unroll
             for (int t = 0; t < T; ++t) {
-                if (wait_act) {
-                    if (t == 0) { wait_ar(0); wait_ar(1); }
-                    else if (t == 1) wait_ar(2);
-                }
+                const uint32_t arp = ar_ph;
                 acquire_acc();
                 if (lane == 0) tr(2, lid, t);
                 tc_fence_after();
@@ -571,6 +566,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
                     for (int dy = 0; dy < 3; ++dy) {
                         int s = slot0 + dy;
                         s = s >= NUNIT ? s - NUNIT : s;
+                        if (wait_act && ((t == 0 && dy == 0) || (t < T - 1 && dy == 2))) {
+                            const int ta = dy == 0 ? 0 : t + 1;
+                            mbar_wait(b_act_ready + 8 * ta, (arp >> ta) & 1u);
+                            tc_fence_after();
+                        }
                         if (t == 0) {
                             mbar_wait(b_full + 8 * s, (ph >> s) & 1u);
                             mbar_wait(b_peerfull + 8 * s, (ph >> s) & 1u);
@@ -589,6 +589,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
                     if (lid == NLAYERS && t == T - 1) umma_commit(b_post_done);   // buffer 0 no longer read
                 }
                 __syncwarp();
+                if (wait_act) ar_ph ^= t == 0 ? 3u : (t == 1 ? 4u : 0u);
                 vb ^= 1;
                 if (lane == 0) tr(3, lid, t);
                 if (t == 0) after_t0();
