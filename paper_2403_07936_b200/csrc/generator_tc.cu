@@ -6,28 +6,31 @@
 // window group stays on chip:
 //
 //   * activations: fp16 (or bf16) in shared memory, each 6x6 window stored as
-//     an 8x8 replicate-padded image; the group's 8 images are interleaved by
-//     image row, so every 3x3 tap of a same-size replicate-padded correlation
-//     is the SAME matrix shifted by a constant row offset (dy * 64 + dx rows):
-//     the UMMA A-descriptor start address moves by 16 B per row (K-major, no
-//     swizzle) -- no im2col.  Tile t (M = 128 rows) holds padded rows
-//     py = 2t+1, 2t+2 of all 8 windows; three tiles per group; two buffers
-//     (layer L reads buffer L % 2).
+//     an 8x8 image (pad rows py = 0, 7 written; the pad columns are dead data);
+//     the group's 8 images are interleaved by image row.  Tile t (M = 128 rows)
+//     holds padded rows py = 2t+1, 2t+2 of all 8 windows; three tiles per
+//     group; two buffers (layer L reads buffer L % 2).
+//   * a 3x3 conv is three MMA chains per tile, one per kernel row dy: A is the
+//     plane shifted by dy * 64 rows (the UMMA A-descriptor start address moves,
+//     K-major, no swizzle -- no im2col) and B stacks the row's three dx taps
+//     (N = 192); the epilogue sums y_0[r - 1] + y_1[r] + y_2[r + 1] with lane
+//     shuffles (px -+ 1 are the adjacent lanes; replicate padding = a lane's own
+//     partial at px = 1, 6).
 //   * cta_group::2: the leader issues M = 256 MMAs (128 rows from each CTA);
-//     the weights of a tap are split along N, 32 output channels per CTA.
-//   * TMEM (512 columns): per tile a 64-column fp32 accumulator, the fp32
-//     residual stream (64 columns) and the packed global skip (32 columns);
-//     the up-conv quarters double-buffer over the accumulator and residual
-//     columns, the tail accumulators (Z) reuse the skip columns.
+//     B is split along N, 32 output channels (x 3 dx) per CTA.
+//   * TMEM (512 columns): two 192-column fp32 accumulator buffers (units
+//     alternate) and the packed global skip (96 columns); the tail
+//     accumulators (Z) reuse the skip columns.  The residual stream is the
+//     fp16 activation plane itself.
 //   * weights: pre-packed in the UMMA core-matrix layout (BN scale folded),
-//     streamed through a 16-slot ring of 4 KB half-taps (cp.async.bulk +
+//     streamed through a 5-unit ring of 12 KB kernel rows (cp.async.bulk +
 //     mbarrier complete_tx), read from L2 once per group.
 //   * head 9x9 conv: fp16 MMA (K = 81 taps padded to 96, the 3 identical input
 //     channels folded) on an im2col built per tile (two buffers), built for
 //     the next group before the current group's stitched-pixel epilogue.
-//   * body: 2B+1 3x3 convs (N = 64, fp32 accumulate); PReLU / residual add /
-//     global skip fused into the TMEM -> register -> smem epilogue.
-//   * up conv 64->256 as four N = 64 quarters; PReLU fused; each quarter is
+//   * body: 2B+1 3x3 convs (fp32 accumulate); PReLU / residual add / global
+//     skip fused into the TMEM -> register -> smem epilogue.
+//   * up conv 64->256 as four quarters of 64 outputs; PReLU fused; each quarter is
 //     drained pixel-shuffled into U (shared memory), the tail's A operand.
 //   * tail 9x9 conv (64 -> 3), pruned to the stitched (kept) fine rows of
 //     interior windows: the kept rows are M, the vertical tap dy is an A-row
@@ -84,6 +87,7 @@ constexpr int TAP_BYTES = 8192;                       // one 3x3 tap in the blob
 constexpr int UNIT_BYTES = 3 * 4096;                  // this CTA's half of a kernel row: [dx 3][ng 4][kc 8][8 oc][8]
 constexpr int ROW_BYTES = 2 * UNIT_BYTES;             // a kernel row in the blob (both halves)
 constexpr int RING_BYTES = NUNIT * UNIT_BYTES;        // 61440
+static_assert(3 * ROW_BYTES == 9 * TAP_BYTES, "a layer is 9 taps");
 constexpr int MISC_BYTES = 8192;                      // q tables (8 x 36 floats) + head im2col index table
 constexpr int BAR_BYTES = 1024;
 // head phase, in activation buffer 1 (free until layer 0's epilogue): im2col, two buffers
