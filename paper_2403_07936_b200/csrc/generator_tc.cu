@@ -244,6 +244,16 @@ __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 512;" ::: 
         ::"r"(taddr), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), \
         "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])          \
         : "memory")
+#define TMEM_LD32(taddr, v)                                                                                   \
+    asm volatile(                                                                                             \
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"       \
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                            \
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),     \
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), \
+          "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]),          \
+          "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),          \
+          "=r"(v[30]), "=r"(v[31])                                                                           \
+        : "r"(taddr))
 #define TMEM_LD8(taddr, v)                                                                                    \
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"                     \
                  : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),       \
@@ -710,22 +720,22 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
             if (lane == 0) mbar_arrive_leader(b_drained + 8 * vb);
             vb ^= 1;
         };
-        // a 3x3 unit: columns n = 96 h + 32 dx + oc' (h = output-channel half); out[r] = y_0[r - 1] + y_1[r]
+        // a 3x3 unit: columns n = 96 h + 48 (oc' / 16) + 16 dx + oc' % 16 (h = output-channel half, so a
+        // thread's 48 columns are contiguous: one x32 and one x16 load); out[r] = y_0[r - 1] + y_1[r]
         // + y_2[r + 1], the row's px -+ 1 neighbours being lanes -+ 1.  Replicate padding: the pad column
         // px = 0 equals px = 1, so the y_0 px = 1 needs is its own (and px = 6 takes its own y_2): the pad rows'
         // results are never used and their activations are dead data.  One indexed shuffle per partial.
         const int src_l = px == 1 ? lane : lane - 1, src_r = px == 6 ? lane : lane + 1;
         auto load_dx3 = [&](float (&y)[16]) {
-            const uint32_t c = acc_wait() + (cq >> 1) * 96 + (cq & 1) * 16;
-            uint32_t v0[16], v1[16], v2[16];
-            TMEM_LD16(c, v0);
-            TMEM_LD16(c + 32, v1);
-            TMEM_LD16(c + 64, v2);
+            const uint32_t c = acc_wait() + (cq >> 1) * 96 + (cq & 1) * 48;
+            uint32_t v01[32], v2[16];
+            TMEM_LD32(c, v01);
+            TMEM_LD16(c + 32, v2);
             tmem_wait_ld();
             acc_release();
 #pragma unroll
             for (int j = 0; j < 16; ++j)
-                y[j] = (__uint_as_float(v1[j]) + __shfl_sync(0xffffffffu, __uint_as_float(v0[j]), src_l)) +
+                y[j] = (__uint_as_float(v01[16 + j]) + __shfl_sync(0xffffffffu, __uint_as_float(v01[j]), src_l)) +
                        __shfl_sync(0xffffffffu, __uint_as_float(v2[j]), src_r);
         };
         const float *head_a = cs;
@@ -1197,8 +1207,9 @@ int tc_pack_weights(mgsr_gen *g, const float *const *t) {
     // BN(conv(x)) = conv(x; W * k) + (beta - mean * k), k = gamma / sqrt(var + 1e-5): the scale is
     // folded into the packed weights (per output channel), the shift stays in the epilogue.
     auto bn_scale = [&](int gi, int oc) { return double(t[gi][oc]) / std::sqrt(double(t[gi + 3][oc]) + 1e-5); };
-    // kernel row dy of a 3x3 64 -> 64 conv (output channels oc0..oc0 + 63): [half][dx 3][ng 4][kc 8][8 oc][8 ic],
-    // so a CTA's unit is one K-major B operand of N = 96 rows (n = 32 dx + oc') with 8-row groups 1 KB apart
+    // kernel row dy of a 3x3 64 -> 64 conv (output channels oc0..oc0 + 63): [half][ng 12][kc 8][8 rows][8 ic], so
+    // a CTA's unit is one K-major B operand of N = 96 rows with 8-row groups 1 KB apart; row n' = 48 (oc' / 16)
+    // + 16 dx + oc' % 16 (oc' = oc % 32), so an epilogue thread's 16 channels x 3 dx are adjacent columns
     auto pack_row = [&](uint16_t *dst, const float *w, int oc0, int dy, int bn_gi) {
         uint16_t *dst16 = reinterpret_cast<uint16_t *>(reinterpret_cast<uint8_t *>(dst) + BL.fmt_stride);
         for (int dx = 0; dx < 3; ++dx)
@@ -1208,7 +1219,8 @@ int tc_pack_weights(mgsr_gen *g, const float *const *t) {
                     for (int e = 0; e < 8; ++e) {
                         int ic = 8 * kc + e;
                         const float v = float(double(w[(((oc0 + oc) * 64 + ic) * 3 + dy) * 3 + dx]) * k);
-                        const int o = (((((oc >> 5) * 3 + dx) * 4 + ((oc & 31) >> 3)) * 8 + kc) * 8 + (oc & 7)) * 8 + e;
+                        const int nr = 48 * ((oc & 31) >> 4) + 16 * dx + (oc & 15);
+                        const int o = ((((oc >> 5) * 12 + (nr >> 3)) * 8 + kc) * 8 + (nr & 7)) * 8 + e;
                         dst[o] = f2bf(v);
                         dst16[o] = f2h(v);
                     }
