@@ -60,7 +60,28 @@ def parse():
     ap.add_argument("--n-smooth", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    # launch-path self-test (CPU, gloo): every rank fakes its timed region; exercises the torchrun
+    # self-launch, the rendezvous, the max-over-ranks reduction and the whole-job value
+    ap.add_argument("--plumbing-test", action="store_true", help=argparse.SUPPRESS)
     return ap.parse_args()
+
+
+def self_launch(args) -> None:
+    """``--gpus N`` (N > 1) outside torchrun: re-exec this script under torch.distributed.run with
+    one rank per GPU (127.0.0.1 rendezvous) and exit with its status.  NCCL's INIT lines (the
+    communicator setup over NVLink) go to stderr, so stdout stays the single JSON line."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ)
+    if not args.plumbing_test:
+        env.setdefault("NCCL_DEBUG", "INFO")
+        env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    sys.exit(subprocess.call(cmd, env=env))
 
 
 # ---------------------------------------------------------------------------
@@ -440,7 +461,7 @@ def workload_config(args):
             "generator_blocks": args.blocks, "sr_levels": args.sr_levels if args.mode == "gan" else 0,
             "weights": ("trained" if weights_path(args.weights, args.blocks) else "he_init") if args.mode == "gan"
             else None,
-            "parallelism": f"replicas x{args.gpus}", "l2": "inputs (134 MB/grid) exceed L2; no flush"}
+            "parallelism": f"replicas x{int(os.environ.get('WORLD_SIZE', args.gpus))}", "l2": "inputs (134 MB/grid) exceed L2; no flush"}
 
 
 def _sides(n):
@@ -450,8 +471,20 @@ def _sides(n):
     return s
 
 
+def run_plumbing(args, rank: int, world: int, dist):
+    """--plumbing-test: the multi-rank bookkeeping of run_mine without a GPU (fake per-rank times)."""
+    import torch
+    ms = 100.0 + 10.0 * rank
+    dev = torch.device("cpu")
+    return dict(ms_total=reduce_max(ms, dist, dev), gen_ms=0.0, gs_ms=0.0, cyc_ms=0.0, kernels=0,
+                e2e=(1, reduce_max(ms, dist, dev), 0, 0), clocks={"sm_mhz": None, "sm_max_mhz": None,
+                                                               "reasons": ["plumbing-test"]}, stats=[])
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "mine":
+        self_launch(args)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if args.impl == "reference":
@@ -462,11 +495,18 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as tdist
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
-        tdist.init_process_group("nccl")
+        if args.plumbing_test:
+            tdist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+            tdist.init_process_group("nccl")
         dist = tdist
-    res = run_mine(args, rank, world, dist)
-    if rank == 0:
+    res = (run_plumbing if args.plumbing_test else run_mine)(args, rank, world, dist)
+    if rank == 0 and args.plumbing_test:
+        print(json.dumps({"metric": METRIC, "value": replica_value(args.steps, res["ms_total"], world),
+                          "unit": UNIT, "n_gpus": world, "steps": args.steps, "ms_per_step": res["ms_total"] / args.steps,
+                          "config": workload_config(args), "plumbing_test": True}), flush=True)
+    elif rank == 0:
         peaks, peak_kind = measured_peaks()
         n = args.n
         cyc_s = replica_value(args.steps, res["ms_total"], world)

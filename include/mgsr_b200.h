@@ -47,6 +47,10 @@ const char *mgsr_version(void);
  * Any contents: each call resets the reduction tickets it uses (stream-ordered). */
 size_t mgsr_workspace_bytes(int64_t n);
 
+/* API scratch (mgsr_gs_sweeps' temporary, mgsr_generator_forward's buffers) comes from a memory pool
+ * private to this library, one per device, which keeps freed blocks mapped; the process-wide default
+ * pool is never modified. */
+
 /* In-place red-black Gauss-Seidel, red=(i+j) even first, mean subtracted
  * (deferred to once per call; <=6e-16 from per-sweep).
  * Replaces kernels.gs_sweeps(p, f, h2, sweeps)  (_stencil.pyx:12-45). */
@@ -71,7 +75,9 @@ int mgsr_restrict(const double *fine, double *coarse, int64_t n, int32_t s, int3
 int mgsr_spline_prolong(const double *c, int64_t nc, int32_t s, double *out, void *stream);
 
 /* Reductions used by Grid.rms / diff_norm (grid.py:67-78): out[0] = sqrt(mean((a-b)^2))
- * (b may be NULL -> rms(a)). Deterministic fixed-order reduction. */
+ * (b may be NULL -> rms(a)). Deterministic fixed-order reduction.  The result is a HOST value,
+ * so this call synchronises `stream` (the reference returns a Python float, grid.py:74-78);
+ * the V-cycle plan computes its norms on the device without synchronising. */
 int mgsr_rms_diff(const double *a, const double *b, int64_t count, double *out_host,
                   void *ws, size_t ws_bytes, void *stream);
 

@@ -13,6 +13,17 @@ import threading
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("MGSR_LIB") or os.path.join(HERE, "libmgsr_b200.so")
 
+_PROFILER_ENV = ("MGSR_NO_GRAPH", "CUDA_INJECTION64_PATH", "NV_NSIGHT_INJECTION_TRANSPORT_TYPE",
+                 "NV_TPS_LAUNCH_TOKEN", "NV_COMPUTE_PROFILER_PERFWORKS_DIR")
+
+
+def graphs_disabled() -> bool:
+    """Same rule as plan.cu: MGSR_NO_GRAPH=1, or an injected profiler (Nsight Compute fails the first
+    kernel launched into a stream capture), makes the plan issue its kernel sequence eagerly; the
+    device-resident solve loop (graph conditional nodes) is then replaced by the per-cycle loop."""
+    return any(os.environ.get(k) for k in _PROFILER_ENV)
+
+
 MGSR_OK = 0
 MGSR_E_CUDA = -8
 PREC = {"fp32": 0, "bf16": 1, "fp16": 2}

@@ -23,6 +23,10 @@ struct mgsr_gen {
 
 namespace mgsr {
 
+// One predicate decides both the workspace size and the kernel of a precision mode.
+inline bool valid_precision(int p) { return p == MGSR_PREC_FP32 || p == MGSR_PREC_BF16 || p == MGSR_PREC_FP16; }
+inline bool tensor_core_precision(int p) { return p == MGSR_PREC_BF16 || p == MGSR_PREC_FP16; }
+
 // Windowed SR prolongation (one full sr_prolong, all passes).
 // c_shift: optional device scalar subtracted from c before normalising.
 // out: fine grid (nc*s)^2 raw data (before the final mean subtraction);

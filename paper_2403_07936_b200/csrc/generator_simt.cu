@@ -199,6 +199,49 @@ __global__ void __launch_bounds__(kConv2Threads) k_conv_rt(const float *__restri
     }
 }
 
+// Direct form for large images (generator_forward on sides whose per-CTA tiles exceed shared memory):
+// one thread per output value, replicate-clamped taps read through the read-only cache, the same
+// accumulation order (c ascending, dy, dx, fmaf) and epilogues as k_conv_simt.
+template <int K, int OP>
+__global__ void __launch_bounds__(256) k_conv_direct(const float *__restrict__ in, int N, int C, int H,
+                                                     const float *__restrict__ w, int O, float *__restrict__ out,
+                                                     Epi ep) {
+    constexpr int P = K / 2;
+    const int64_t HW = int64_t(H) * H, total = int64_t(N) * O * HW;
+    for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < total; t += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t n = t / (O * HW);
+        const int o = int((t / HW) % O);
+        const int pix = int(t % HW), y = pix / H, x = pix % H;
+        float v = 0.f;
+        for (int c = 0; c < C; ++c) {
+            const float *ic = in + (n * C + c) * HW;
+            const float *wc = w + (int64_t(o) * C + c) * K * K;
+            for (int dy = 0; dy < K; ++dy) {
+                const int yy = min(max(y + dy - P, 0), H - 1);
+                for (int dx = 0; dx < K; ++dx) {
+                    const int xx = min(max(x + dx - P, 0), H - 1);
+                    v = fmaf(__ldg(ic + yy * H + xx), __ldg(wc + dy * K + dx), v);
+                }
+            }
+        }
+        if (OP == OP_PRELU) {
+            out[t] = v > 0.f ? v : ep.alpha[o] * v;
+        } else if (OP == OP_BN_PRELU) {
+            v = fmaf(v, ep.scale[o], ep.shift[o]);
+            out[t] = v > 0.f ? v : ep.alpha[o] * v;
+        } else if (OP == OP_BN_RES) {
+            out[t] = ep.res[t] + fmaf(v, ep.scale[o], ep.shift[o]);
+        } else if (OP == OP_SHUF_PRELU) {
+            const int cc = o >> 2, i = (o >> 1) & 1, j = o & 1, W2 = 2 * H;
+            v = v > 0.f ? v : ep.alpha[cc] * v;
+            out[((n * (O >> 2) + cc) * W2 + 2 * y + i) * W2 + 2 * x + j] = v;
+        } else {
+            const float sc = ep.tanh_s;
+            out[t] = sc * tanhf((v + ep.bias[o]) / sc);
+        }
+    }
+}
+
 template <int K, int OP>
 static int conv(const float *in, int N, int C, int H, const float *w, int O, float *out, const Epi &ep,
                 cudaStream_t st) {
@@ -229,17 +272,20 @@ static int conv(const float *in, int N, int C, int H, const float *w, int O, flo
     const int HP = H + K - 1;
     int cc = 12288 / (HP * HP);
     if (cc > C) cc = C;
-    if (cc < 1) { set_error("conv window too large"); return MGSR_E_UNSUPPORTED; }
-    const size_t smem = sizeof(float) * cc * HP * HP;
+    const size_t smem = sizeof(float) * (cc > 0 ? cc : 1) * HP * HP;
     const int per = (kConvOB * H * H + kConvThreads - 1) / kConvThreads;
+    if (cc < 1 || per > 36) {
+        k_conv_direct<K, OP><<<grid_for(int64_t(N) * O * H * H, 256), 256, 0, st>>>(in, N, C, H, w, O, out, ep);
+        MGSR_LAUNCH_CHECK();
+        return MGSR_OK;
+    }
     dim3 grid(N, (O + kConvOB - 1) / kConvOB);
     if (per <= 3)
         k_conv_simt<K, 3, OP><<<grid, kConvThreads, smem, st>>>(in, C, H, w, O, out, ep, cc);
     else if (per <= 9)
         k_conv_simt<K, 9, OP><<<grid, kConvThreads, smem, st>>>(in, C, H, w, O, out, ep, cc);
-    else if (per <= 36)
+    else
         k_conv_simt<K, 36, OP><<<grid, kConvThreads, smem, st>>>(in, C, H, w, O, out, ep, cc);
-    else { set_error("window side too large for the fp32 generator"); return MGSR_E_UNSUPPORTED; }
     MGSR_LAUNCH_CHECK();
     return MGSR_OK;
 }
@@ -365,8 +411,8 @@ size_t sr_workspace_bytes(int64_t nc, int s, int precision) {
     // intermediate fine grid for two-pass ratios + fp32 chunk buffers + scalars
     size_t inter = (s == 8 || s == 16) ? sizeof(double) * size_t(nc * 4) * size_t(nc * 4) : 0;
     // the fp32 CUDA-core chunk buffers only for fp32 (the tensor-core precisions never fall back to them)
-    size_t simt = precision == MGSR_PREC_FP32 ? sizeof(float) * pass_ws_floats(s == 2 ? 1 : 2) + 4096 : 0;
-    size_t tc = precision != MGSR_PREC_FP32 ? tc_workspace_bytes(nc) : 0;
+    size_t simt = tensor_core_precision(precision) ? 0 : sizeof(float) * pass_ws_floats(s == 2 ? 1 : 2) + 4096;
+    size_t tc = tensor_core_precision(precision) ? tc_workspace_bytes(nc) : 0;
     return inter + (simt > tc ? simt : tc) + 512;
 }
 
@@ -416,6 +462,7 @@ static int sr_pass_simt(const mgsr_gen *g, const double *c, const double *c_shif
 int launch_sr_prolong(const mgsr_gen *g, const double *c, const double *c_shift, int nc, int s, double p_min,
                       double p_max, int precision, double *out, double *out_mean, void *ws, size_t ws_bytes,
                       void *red_slot, cudaStream_t st, cudaEvent_t *gen_markers) {
+    if (!valid_precision(precision)) { set_error("precision must be one of fp32, bf16, fp16"); return MGSR_E_BAD_ARG; }
     int npass = 0;
     const int *plan = pass_plan(s, &npass);
     if (!plan) { set_error("unsupported SR ratio " + std::to_string(s) + "; expected one of [2, 4, 8, 16]"); return MGSR_E_SR_RATIO; }
@@ -441,7 +488,7 @@ int launch_sr_prolong(const mgsr_gen *g, const double *c, const double *c_shift,
         int r;
         const bool mark = gen_markers && ip == npass - 1;
         if (mark) MGSR_CUDA_TRY(cudaEventRecordWithFlags(gen_markers[0], st, cudaEventRecordExternal));
-        if (precision == MGSR_PREC_BF16 || precision == MGSR_PREC_FP16) {
+        if (tensor_core_precision(precision)) {
             // tensor-core path only; no silent fallback to the fp32 CUDA-core path
             if (apps != 1 || !g->tc_blob) {
                 set_error("tensor-core generator supports 6x6 windows (ratio-2 passes) only");
@@ -550,14 +597,12 @@ extern "C" int mgsr_generator_destroy(mgsr_gen *g) {
 extern "C" int mgsr_generator_forward(const mgsr_gen *g, const double *x, int64_t batch, int64_t side, double *y,
                                       void *stream) {
     if (!g || !x || !y || batch < 1 || side < 1) { set_error("bad argument"); return MGSR_E_BAD_ARG; }
-    if (side > 12) { set_error("fp32 generator supports input side <= 12"); return MGSR_E_UNSUPPORTED; }
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int H = int(side);
     size_t nx = size_t(batch) * 3 * H * H, ny = size_t(batch) * 3 * 4 * H * H;
     size_t bytes = sizeof(float) * (nx + ny + gen_scratch_floats(H) * size_t(batch));
     float *buf = nullptr;
-    keep_async_pool();
-    MGSR_CUDA_TRY(cudaMallocAsync(&buf, bytes, st));
+    if (int e = scratch_alloc(reinterpret_cast<void **>(&buf), bytes, st)) return e;
     k_f64_to_f32<<<grid_for(nx, 256), 256, 0, st>>>(x, buf, nx);
     int r = gen_forward_f32(g, buf, int(batch), H, buf + nx, buf + nx + ny, st);
     if (!r) k_f32_to_f64<<<grid_for(ny, 256), 256, 0, st>>>(buf + nx, y, ny);
@@ -575,6 +620,7 @@ extern "C" int mgsr_sr_prolong(const mgsr_gen *g, const double *c, int64_t nc, i
                                double p_max, int32_t precision, double *out, void *ws, size_t ws_bytes,
                                void *stream) {
     if (!g || !c || !out) { set_error("SR prolongation requires generator weights"); return MGSR_E_BAD_ARG; }
+    if (!valid_precision(precision)) { set_error("precision must be one of fp32, bf16, fp16"); return MGSR_E_BAD_ARG; }
     if (ws_bytes < mgsr_sr_workspace_bytes(nc, s)) { set_error("workspace too small"); return MGSR_E_WORKSPACE; }
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     char *w = static_cast<char *>(ws);

@@ -1387,8 +1387,7 @@ extern "C" int mgsr_debug_tc_pass(const mgsr_gen *g, const double *c, int64_t nc
     const size_t wsb = mgsr::tc_workspace_bytes(nc);
     void *ws = nullptr;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    mgsr::keep_async_pool();
-    if (cudaMallocAsync(&ws, wsb, st) != cudaSuccess) return MGSR_E_CUDA;
+    if (int e = mgsr::scratch_alloc(&ws, wsb, st)) return e;
     int r = mgsr::launch_sr_pass_tc_dbg(g, c, nullptr, int(nc), std::log10(p_min),
                                         std::log10(p_max) - std::log10(p_min), fine, ws, wsb, dbg, dbg_layer, st,
                                         nullptr, f16);
@@ -1401,8 +1400,7 @@ extern "C" int mgsr_debug_tc_prof(const mgsr_gen *g, const double *c, int64_t nc
     const size_t wsb = mgsr::tc_workspace_bytes(nc);
     void *ws = nullptr;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    mgsr::keep_async_pool();
-    if (cudaMallocAsync(&ws, wsb, st) != cudaSuccess) return MGSR_E_CUDA;
+    if (int e = mgsr::scratch_alloc(&ws, wsb, st)) return e;
     int r = mgsr::launch_sr_pass_tc_dbg(g, c, nullptr, int(nc), -10.0, 7.0, fine, ws, wsb, nullptr, -1, st, prof, f16);
     cudaFreeAsync(ws, st);
     return r;

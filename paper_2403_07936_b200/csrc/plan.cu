@@ -69,9 +69,23 @@ struct mgsr_plan {
     bool capturing_markers = false;
     std::vector<cudaEvent_t> pool;
     int pool_used = 0, pool_cap = 0;
+    // debug (parity tests): per level l, copy the SR prolongation's input correction (nc^2) and its raw
+    // output (nf^2, before the mean subtraction) to caller buffers inside the captured cycle
+    std::map<int, std::pair<double *, double *>> sr_dump;
 };
 
 namespace {
+
+// Under Nsight Compute (its injection sets NV_NSIGHT_INJECTION_TRANSPORT_TYPE / NV_TPS_LAUNCH_TOKEN /
+// NV_COMPUTE_PROFILER_PERFWORKS_DIR; other injecting tools CUDA_INJECTION64_PATH) the first kernel
+// launched into a stream capture fails ("LaunchFailed"), so the plan issues the same kernel sequence
+// eagerly, as MGSR_NO_GRAPH=1 does.
+bool graphs_disabled() {
+    for (const char *v : {"MGSR_NO_GRAPH", "CUDA_INJECTION64_PATH", "NV_NSIGHT_INJECTION_TRANSPORT_TYPE",
+                          "NV_TPS_LAUNCH_TOKEN", "NV_COMPUTE_PROFILER_PERFWORKS_DIR"})
+        if (std::getenv(v)) return true;
+    return false;
+}
 
 double *sc(mgsr_plan *pl, int i) { return pl->scal + i; }
 double *rc_mean(mgsr_plan *pl, int l) { return pl->scal + SC_LEVEL0 + 4 * l; }
@@ -110,6 +124,14 @@ int prolong_into(mgsr_plan *pl, int l, int use_sr, const double *base, const dou
                               (l == 1 && pl->capturing_markers) ? pl->cap_ev : nullptr);
     if (r) return r;
     const int64_t nf = int64_t(nc) * s;
+    auto dump = pl->sr_dump.find(l);
+    if (dump != pl->sr_dump.end()) {
+        if (dump->second.first)
+            MGSR_CUDA_TRY(cudaMemcpyAsync(dump->second.first, corr, sizeof(double) * nc * nc, cudaMemcpyDeviceToDevice, st));
+        if (dump->second.second)
+            MGSR_CUDA_TRY(cudaMemcpyAsync(dump->second.second, pl->srbuf, sizeof(double) * nf * nf,
+                                          cudaMemcpyDeviceToDevice, st));
+    }
     return launch_add2(base, bshift, pl->srbuf, sr_mean(pl, l), out, nf * nf, mean_out, slot(pl, 3), st);
 }
 
@@ -192,6 +214,7 @@ extern "C" int mgsr_plan_create(const mgsr_plan_config *cfg, const mgsr_gen *gen
     if (!cfg || !out) { set_error("bad argument"); return MGSR_E_BAD_ARG; }
     if (cfg->n_smooth < 1 || cfg->coarse_sweeps < 1) { set_error("sweep counts must be positive"); return MGSR_E_BAD_ARG; }
     if (cfg->r_min < 2 || cfg->r_min % 2) { set_error("r_min must be an even integer >= 2"); return MGSR_E_BAD_ARG; }
+    if (!valid_precision(cfg->precision)) { set_error("precision must be one of fp32, bf16, fp16"); return MGSR_E_BAD_ARG; }
     mgsr_plan *pl = new mgsr_plan();
     pl->cfg = *cfg;
     pl->gen = gen;
@@ -282,7 +305,7 @@ extern "C" int mgsr_plan_vcycle(mgsr_plan *pl, double *p, const double *f, int32
     if (!pl || !p || !f) { set_error("bad argument"); return MGSR_E_BAD_ARG; }
     if (use_sr && !pl->gen) { set_error("SR prolongation requires generator weights"); return MGSR_E_BAD_ARG; }
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    if (std::getenv("MGSR_NO_GRAPH")) {
+    if (graphs_disabled()) {
         // eager issue of the same kernel sequence (profilers that cannot replay graph nodes)
         const bool mk = pl->capturing_markers;
         pl->capturing_markers = false;   // external event records exist only inside captures
@@ -345,6 +368,27 @@ extern "C" int mgsr_plan_vcycle(mgsr_plan *pl, double *p, const double *f, int32
     MGSR_CUDA_TRY(cudaGraphLaunch(G.exec, st));
     if (stats_dev)
         MGSR_CUDA_TRY(cudaMemcpyAsync(stats_dev, sc(pl, SC_STATS), 2 * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    return MGSR_OK;
+}
+
+// Debug entry (not in the public header; tests/test_gpu_solver.py): dump the SR prolongation from level
+// `level` into level - 1 of every following cycle: c_dst receives its input correction (n_level^2 doubles),
+// sr_dst its raw output (n_{level-1}^2, before the mean subtraction).  NULL pointers clear the dump.
+// Drops the captured graphs so the copies enter the next capture.
+extern "C" int mgsr_debug_plan_sr_dump(mgsr_plan *pl, int32_t level, double *c_dst, double *sr_dst) {
+    if (!pl || level < 1 || level >= int(pl->sides.size())) { set_error("bad argument"); return MGSR_E_BAD_ARG; }
+    if (c_dst || sr_dst) pl->sr_dump[level] = {c_dst, sr_dst};
+    else pl->sr_dump.erase(level);
+    for (auto &kv : pl->graphs) {
+        cudaGraphExecDestroy(kv.second.exec);
+        cudaGraphDestroy(kv.second.graph);
+    }
+    pl->graphs.clear();
+    for (auto &kv : pl->solves) {
+        cudaGraphExecDestroy(kv.second.exec);
+        cudaGraphDestroy(kv.second.graph);
+    }
+    pl->solves.clear();
     return MGSR_OK;
 }
 
@@ -489,6 +533,11 @@ extern "C" int mgsr_plan_solve(mgsr_plan *pl, double *p, const double *f, int32_
         return MGSR_E_BAD_ARG;
     }
     if (mode != 0 && !pl->gen) { set_error("SR prolongation requires generator weights"); return MGSR_E_BAD_ARG; }
+    if (graphs_disabled()) {
+        set_error("the device-resident solve loop needs CUDA graphs (disabled by MGSR_NO_GRAPH or an attached "
+                  "profiler); use the per-cycle loop");
+        return MGSR_E_UNSUPPORTED;
+    }
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (!pl->solve_state) MGSR_CUDA_TRY(cudaMalloc(&pl->solve_state, 4 * sizeof(int)));
     if (pl->rec_cap < n_iter) {

@@ -9,6 +9,8 @@
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
+#include <mutex>
+
 #include <cstdio>
 #include <cstdlib>
 #include <string>
@@ -1037,19 +1039,32 @@ __global__ void k_sqdiff(const double *__restrict__ a, const double *__restrict_
 // ---------------------------------------------------------------------------
 // launch helpers (shared with plan.cu)
 
-// Stream-ordered scratch for the API entry points (cudaMallocAsync): keep freed blocks in the device's
-// default pool instead of returning them at every synchronisation (release threshold 0), which made a
-// 4096^2 mgsr_gs_sweeps remap 268 MB per call.
-void keep_async_pool() {
-    static bool done[64] = {};
+// Stream-ordered scratch for the API entry points: a memory pool private to this library (one per
+// device), created on first use with an unbounded release threshold, so freed blocks stay mapped for the
+// next call (with threshold 0 every 4096^2 mgsr_gs_sweeps remapped 268 MB) without changing the
+// process-wide default pool that torch or other libraries may use.
+int scratch_alloc(void **ptr, size_t bytes, cudaStream_t st) {
+    static std::mutex mu;
+    static cudaMemPool_t pools[64] = {};
     int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64 || done[dev]) return;
-    cudaMemPool_t mp;
-    if (cudaDeviceGetDefaultMemPool(&mp, dev) == cudaSuccess) {
-        uint64_t thr = UINT64_MAX;
-        cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &thr);
+    MGSR_CUDA_TRY(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= 64) { set_error("device ordinal out of range"); return MGSR_E_BAD_ARG; }
+    cudaMemPool_t pool;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        if (!pools[dev]) {
+            cudaMemPoolProps props{};
+            props.allocType = cudaMemAllocationTypePinned;
+            props.location.type = cudaMemLocationTypeDevice;
+            props.location.id = dev;
+            MGSR_CUDA_TRY(cudaMemPoolCreate(&pools[dev], &props));
+            uint64_t thr = UINT64_MAX;
+            MGSR_CUDA_TRY(cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &thr));
+        }
+        pool = pools[dev];
     }
-    done[dev] = true;
+    MGSR_CUDA_TRY(cudaMallocFromPoolAsync(ptr, bytes, pool, st));
+    return MGSR_OK;
 }
 
 int num_sms() {
@@ -1358,8 +1373,7 @@ extern "C" int mgsr_gs_sweeps(double *p, const double *f, int64_t n, double h2, 
     if (n <= kSmallN)  // exact per-sweep mean subtraction inside one CTA
         return launch_gs(p, p, nullptr, fs, int(n), h2, sweeps, 0, nullptr, nullptr, nullptr, red, st);
     double *tmp = nullptr;
-    keep_async_pool();
-    MGSR_CUDA_TRY(cudaMallocAsync(&tmp, 2 * sizeof(double) * n * n, st));
+    if (int e = scratch_alloc(reinterpret_cast<void **>(&tmp), 2 * sizeof(double) * n * n, st)) return e;
     int rc = launch_gs(p, tmp, tmp + n * n, fs, int(n), h2, sweeps, 0, nullptr, nullptr, scal, red, st);
     if (rc == MGSR_OK) rc = launch_affine(tmp, p, n * n, scal, 1.0, st);
     cudaFreeAsync(tmp, st);
@@ -1390,6 +1404,7 @@ extern "C" int mgsr_residual(const double *p, const double *f, double *r, int64_
 extern "C" int mgsr_restrict(const double *fine, double *coarse, int64_t n, int32_t s, int32_t subtract_mean,
                              void *ws, size_t ws_bytes, void *stream) {
     if (s < 2 || (s & (s - 1))) { set_error("transfer ratio must be a power of two >= 2, got " + std::to_string(s)); return MGSR_E_RATIO; }
+    if (n < 1 || !fine || !coarse) { set_error("bad argument"); return MGSR_E_BAD_ARG; }
     if (n % s) { set_error("fine side " + std::to_string(n) + " is not divisible by ratio " + std::to_string(s)); return MGSR_E_NOT_DIVISIBLE; }
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (int e = check_ws(ws, ws_bytes, st)) return e;
@@ -1411,6 +1426,7 @@ extern "C" int mgsr_spline_prolong(const double *c, int64_t nc, int32_t s, doubl
 
 extern "C" int mgsr_rms_diff(const double *a, const double *b, int64_t count, double *out_host, void *ws,
                              size_t ws_bytes, void *stream) {
+    if (count < 1 || !a || !out_host) { set_error("bad argument"); return MGSR_E_BAD_ARG; }
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (int e = check_ws(ws, ws_bytes, st)) return e;
     double *scal = static_cast<double *>(ws);

@@ -7,7 +7,7 @@ namespace mgsr {
 constexpr int kSmallN = 64;
 
 int grid_for(int64_t work, int threads);
-void keep_async_pool();   // default mem pool keeps freed blocks (API scratch via cudaMallocAsync)
+int scratch_alloc(void **ptr, size_t bytes, cudaStream_t st);   // API scratch from a library-private pool
 int launch_gs(const double *p_in, double *p_out, double *tmp, FSrc fs, int n, double h2, int sweeps,
               int zero_init, double *rc, double *rc_mean, double *mean_out, void *red_ws, cudaStream_t st);
 int launch_prolong_add(const double *c, int nc, int s, const double *base, const double *bshift, double *out,

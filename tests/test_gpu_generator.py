@@ -97,27 +97,33 @@ def _trained(blocks):
     return srmodel.load_weights(os.path.join(ROOT, "artifacts", f"trained_b{blocks}.mgsr"))
 
 
+def _oracle_weights(orc, w):
+    return orc.Weights({k: v for k, v in w.tensors.items()}, w.num_residual_blocks, w.tanh_scale)
+
+
 @pytest.mark.parametrize("blocks", [4, 8])
-def test_tc_fp16_field_parity_trained(cuda, blocks):
-    """North-star bar: GAN-prolonged field within 1e-2 relL2 of the fp32 generator."""
+def test_tc_fp16_field_parity_trained(cuda, orc, blocks):
+    """North-star bar: GAN-prolonged field within 1e-2 relL2 of the reference generator (the fp64
+    CPU oracle on the MGSR1 weights), full field at n_c = 64, noise and smooth inputs."""
     from paper_2403_07936_b200 import srmodel
     from paper_2403_07936_b200.grid import Grid, NormBounds
     w = _trained(blocks)
-    for name, c in _fields(128).items():
-        ref = srmodel.sr_prolong(Grid(c), w, NormBounds(), 2, precision="fp32").data
+    ow = _oracle_weights(orc, w)
+    for name, c in _fields(64).items():
+        exp = orc.sr_prolong(c, ow, orc.Bounds(), 2)
         got = srmodel.sr_prolong(Grid(c), w, NormBounds(), 2, precision="fp16").data
-        assert rel_l2(got, ref) < 1e-2, name
+        assert rel_l2(got, exp) < 1e-2, name
 
 
-def test_tc_fp16_field_parity_he_init_smooth(cuda):
-    """Seeded He-init B=8 (BASELINE's fallback weights) on a smooth correction field."""
+def test_tc_fp16_field_parity_he_init_smooth(cuda, orc):
+    """Seeded He-init B=8 (BASELINE's fallback weights) on a smooth correction field, vs the oracle."""
     from paper_2403_07936_b200 import srmodel
     from paper_2403_07936_b200.grid import Grid, NormBounds
     w = srmodel.random_weights(8, 0)
-    c = _fields(128)["smooth"]
-    ref = srmodel.sr_prolong(Grid(c), w, NormBounds(), 2, precision="fp32").data
+    c = _fields(64)["smooth"]
+    exp = orc.sr_prolong(c, _oracle_weights(orc, w), orc.Bounds(), 2)
     got = srmodel.sr_prolong(Grid(c), w, NormBounds(), 2, precision="fp16").data
-    assert rel_l2(got, ref) < 1e-2
+    assert rel_l2(got, exp) < 1e-2
 
 
 def test_tc_bf16_vs_fp16_error_ordering(cuda):
@@ -145,29 +151,29 @@ def test_tc_vs_oracle_full_field(cuda, orc):
 
 
 @pytest.mark.parametrize("nc", [6, 8, 10, 16])
-def test_tc_edge_windows_and_tiny_grids(cuda, nc):
+def test_tc_edge_windows_and_tiny_grids(cuda, orc, nc):
     """Grids whose windows are all (or mostly) edge windows exercise the exact fallback tail;
-    every fine cell is written (stitch coverage) and matches the fp32 path."""
+    every fine cell is written (stitch coverage) and matches the fp64 oracle."""
     from paper_2403_07936_b200 import srmodel
     from paper_2403_07936_b200.grid import Grid, NormBounds
     w = _trained(4)
     c = _fields(nc)["noise"]
-    ref = srmodel.sr_prolong(Grid(c), w, NormBounds(), 2, precision="fp32").data
+    exp = orc.sr_prolong(c, _oracle_weights(orc, w), orc.Bounds(), 2)
     got = srmodel.sr_prolong(Grid(c), w, NormBounds(), 2, precision="fp16").data
     assert np.all(np.isfinite(got))
-    assert rel_l2(got, ref) < 1e-2
+    assert rel_l2(got, exp) < 1e-2
 
 
-def test_tc_nn_weights_upsampler(cuda):
+def test_tc_nn_weights_upsampler(cuda, orc):
     """Crafted nearest-neighbour weights: the generator copies q; the field returns to the
-    input values at the coincident fine cells up to operand rounding (tf32 head)."""
+    input values at the coincident fine cells up to operand rounding (fp16 head), vs the oracle."""
     from paper_2403_07936_b200 import srmodel
     from paper_2403_07936_b200.grid import Grid, NormBounds
     c = _fields(32)["noise"]
     w = srmodel.make_nearest_neighbor_weights()
-    ref = srmodel.sr_prolong(Grid(c), w, NormBounds(), 2, precision="fp32").data
+    exp = orc.sr_prolong(c, _oracle_weights(orc, w), orc.Bounds(), 2)
     got = srmodel.sr_prolong(Grid(c), w, NormBounds(), 2, precision="fp16").data
-    assert rel_l2(got, ref) < 1e-2
+    assert rel_l2(got, exp) < 1e-2
 
 
 def test_tc_deterministic(cuda):
@@ -222,12 +228,29 @@ def test_tc_bench_size_pass_vs_oracle_sampled_windows(cuda, orc, weights):
     m = ~np.isnan(qf)
     exp = orc.denormalize(qf[m], np.sign(qf[m]), b)
     assert m.sum() >= 256 * 16
-    # north-star bar for trained weights; seeded He-init networks amplify operand rounding (measured
-    # 2.1e-2 here, precision matrix in DESIGN.md) and are held to the documented 3e-2
-    assert rel_l2(got[m], exp) < (1e-2 if weights == "trained" else 3e-2)
+    # north-star bar for both weight sets (measured 7.1e-3 He-init; the
+    # He-init error is a handful of sign flips of saturated tanh outputs, see the full-field test below)
+    assert rel_l2(got[m], exp) < 1e-2
 
 
-def test_tc_generator_depths(cuda):
+@pytest.mark.parametrize("weights", ["trained", "he_init"])
+def test_tc_bench_size_full_field_vs_fp32_generator(cuda, weights):
+    """The whole bench-size field (n_c = 2048, 1,044,484 windows, 16.8M fine cells): fp16 tensor cores
+    vs the fp32 CUDA-core generator (itself pinned to the fp64 oracle: test_sr_prolong_fp32_golden,
+    test_sr_prolong_fp32_vs_oracle_256) at the north-star 1e-2 bar.  Measured 2.6e-3 (trained) and
+    1.7e-3 (He-init)."""
+    from paper_2403_07936_b200 import datagen, srmodel
+    from paper_2403_07936_b200.grid import Grid, NormBounds
+    nc = 2048
+    w = _trained(8) if weights == "trained" else srmodel.random_weights(8, 0)
+    f = datagen.scale_to_p_rms(datagen.grf_blobs_rhs(nc, seed=5, kmax=256.0), 1e-4)
+    c = datagen.spectral_solution(f)
+    ref = srmodel.sr_prolong(Grid(c), w, NormBounds(), 2, precision="fp32").data
+    got = srmodel.sr_prolong(Grid(c), w, NormBounds(), 2, precision="fp16").data
+    assert rel_l2(got, ref) < 1e-2
+
+
+def test_tc_generator_depths(cuda, orc):
     """Residual-block counts other than 4/8: B=1 runs on the tensor cores within the bar; B=16 (the
     deepest whose constants fit the kernel's shared memory) runs; B=17 is refused loudly, never run
     on a fallback."""
@@ -235,15 +258,15 @@ def test_tc_generator_depths(cuda):
     from paper_2403_07936_b200.grid import Grid, NormBounds
     c = _fields(32)["smooth"]
     w1 = srmodel.random_weights(1, 3)
-    ref = srmodel.sr_prolong(Grid(c), w1, NormBounds(), 2, precision="fp32").data
+    exp = orc.sr_prolong(c, _oracle_weights(orc, w1), orc.Bounds(), 2)
     got = srmodel.sr_prolong(Grid(c), w1, NormBounds(), 2, precision="fp16").data
-    assert rel_l2(got, ref) < 1e-2
+    assert rel_l2(got, exp) < 1e-2
     # B=16 with the crafted nearest-neighbour network (a He-init network this deep amplifies fp16
     # operand rounding to ~4% of its tanh output, so it would test the weights, not the kernel)
     w16 = srmodel.make_nearest_neighbor_weights(16)
-    ref = srmodel.sr_prolong(Grid(c), w16, NormBounds(), 2, precision="fp32").data
+    exp = orc.sr_prolong(c, _oracle_weights(orc, w16), orc.Bounds(), 2)
     got = srmodel.sr_prolong(Grid(c), w16, NormBounds(), 2, precision="fp16").data
-    assert rel_l2(got, ref) < 1e-2
+    assert rel_l2(got, exp) < 1e-2
     w17 = srmodel.random_weights(17, 0)
     with pytest.raises(ValueError, match="too deep"):
         srmodel.sr_prolong(Grid(c), w17, NormBounds(), 2, precision="fp16")
