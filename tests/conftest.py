@@ -25,6 +25,11 @@ def golden():
 
 
 @pytest.fixture(scope="session")
+def golden_dir():
+    return GOLDEN
+
+
+@pytest.fixture(scope="session")
 def golden_meta():
     with open(os.path.join(GOLDEN, "golden_meta.json")) as fh:
         return json.load(fh)

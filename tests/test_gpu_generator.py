@@ -270,3 +270,17 @@ def test_tc_generator_depths(cuda, orc):
     w17 = srmodel.random_weights(17, 0)
     with pytest.raises(ValueError, match="too deep"):
         srmodel.sr_prolong(Grid(c), w17, NormBounds(), 2, precision="fp16")
+
+
+@pytest.mark.parametrize("blocks", [4, 8])
+def test_generator_forward_matches_reference_trainer_fixtures(cuda, blocks):
+    """generator_forward replays the reference trainer's recorded forward passes (torch fp32, eval
+    mode; tests/golden/make_trainer_fixtures.py) within the reference's trainer-parity bar 1e-4."""
+    import os
+    from paper_2403_07936_b200 import srmodel
+    from conftest import GOLDEN
+    fx = np.load(os.path.join(GOLDEN, "trainer_fixtures.npz"))
+    w = _trained(blocks)
+    for x, y in zip(fx[f"b{blocks}_inputs"], fx[f"b{blocks}_outputs"]):
+        got = srmodel.generator_forward(w, x.astype(np.float64))
+        assert np.abs(got - y).max() < 1e-4

@@ -330,3 +330,34 @@ def test_bench_cycle_4096_each_sr_level_vs_oracle_sampled(cuda, orc):
         exp = orc.denormalize(qf[m], np.sign(qf[m]), b)
         assert m.sum() >= 96 * 16
         assert rel_l2(got[m], exp) < 1e-2, (l, rel_l2(got[m], exp))
+
+
+@pytest.mark.parametrize("precision", ["fp32", "fp16"])
+def test_config3_hybrid_1024_matches_reference_fixture(cuda, orc, golden_dir, precision):
+    """BASELINE config 3 (1024^2, GRF + blobs, latched hybrid, trained B=8) against the REFERENCE's
+    own solve (tests/golden/make_config3_golden.py -> config3_hybrid.npz): the same iteration count,
+    operator and latch sequences, the converged field, and the residual / diff histories."""
+    import json
+    import os
+    from paper_2403_07936_b200 import solver, srmodel
+    from paper_2403_07936_b200.grid import Grid
+    from paper_2403_07936_b200.smoother import PoissonProblem
+    from conftest import ROOT
+    fx = np.load(os.path.join(golden_dir, "config3_hybrid.npz"))
+    meta = json.load(open(os.path.join(golden_dir, "config3_hybrid_meta.json")))
+    f = orc.scale_to_p_rms(orc.grf_blobs_rhs(1024, seed=0, kmax=256.0), 1e-4)
+    assert np.allclose([f.sum(), np.abs(f).sum(), (f * f).sum()], fx["f_checksum"], rtol=1e-12, atol=1e-12)
+    w = srmodel.load_weights(os.path.join(ROOT, "artifacts", "trained_b8.mgsr"))
+    cfg = cfg_(mode="hybrid", N_GAN=1.0, S_thres=5e-4)
+    p, log = solver.solve(PoissonProblem(Grid(f)), cfg, w, precision=precision)
+    assert log.iterations == meta["iterations"]
+    assert [r.operator for r in log.records] == meta["operators"]
+    assert [r.switch_latched for r in log.records] == meta["latched"]
+    hist = np.array([[r.diff_norm, r.residual_norm] for r in log.records])
+    ref = fx["log"]
+    relh = np.abs(hist - ref) / ref
+    print(f"\nconfig3 {precision}: history rel diff per iteration {relh.max(axis=1)}")
+    bar = 1e-4 if precision == "fp32" else 5e-3     # measured 1.8e-5 / 1.7e-3 (generator operand precision)
+    assert relh.max() < bar
+    sub = p.data[::16, ::16]
+    assert rel_l2(sub, fx["p_sub"]) < 1e-8

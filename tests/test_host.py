@@ -297,3 +297,21 @@ def test_solve_batch_distributed_gloo_world2(tmp_path):
     for r in res:
         assert r["order"] == [0.0, 1.0, 2.0, 3.0, 4.0]
         assert r["solved_by"] == [0.0, 1.0, 0.0, 1.0, 0.0]
+
+
+def test_bench_gpus2_self_launch_gloo():
+    """`python bench.py --gpus 2` outside torchrun re-executes itself under torch.distributed.run with
+    two ranks (127.0.0.1 rendezvous); the line reports n_gpus 2 and the whole-job value from the
+    slower rank's time (plumbing self-test: gloo, fake per-rank times 100 / 110 ms)."""
+    import json
+    import subprocess
+    import sys
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--plumbing-test",
+                          "--steps", "4", "--warmup", "3"], env=env, capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["parallelism"] == "replicas x2"
+    assert abs(d["value"] - 2 * 4 / 0.110) < 1e-9

@@ -130,3 +130,16 @@ def test_oracle_against_live_reference(orc):
     theirs = solver.v_cycle(Grid(p0), smoother.PoissonProblem(Grid(f)),
                             solver.RunConfig(N_step=1, r_min=8, N_smooth=3), "spline").data
     assert rel(mine, theirs) < 1e-13
+
+
+def test_oracle_generator_matches_reference_trainer_fixtures(orc):
+    """The oracle's generator (srmodel.py restatement) replays the reference TRAINER's recorded torch
+    forward passes (tests/golden/make_trainer_fixtures.py, PROVENANCE.md:11-19) for both trained weight
+    files within the reference's own trainer-parity bar (test_acceptance.py:247-263: 1e-4)."""
+    import os
+    from conftest import GOLDEN, ROOT
+    fx = np.load(os.path.join(GOLDEN, "trainer_fixtures.npz"))
+    for b in (4, 8):
+        w = orc.read_mgsr1(os.path.join(ROOT, "artifacts", f"trained_b{b}.mgsr"))
+        got = orc.forward_batch(w, fx[f"b{b}_inputs"].astype(np.float64))
+        assert np.abs(got - fx[f"b{b}_outputs"]).max() < 1e-4, b
