@@ -363,61 +363,61 @@ def run_mine(args, rank: int, world: int, dist):
 # ---------------------------------------------------------------------------
 # CPU baseline: the reference compiled from its own sources (oracle/_ref)
 
-def cpu_reference_sample(n: int, blocks: int, windows: int, mode: str, sr_levels: int, wkind: str = "trained"):
-    """Time the reference on a bounded sample and project V-cycles/s at n^2.
-    Returns (projected cycles/s, kind, sample description)."""
+SR_SAMPLE_NC = 68        # coarse side of the timed reference sr_prolong sample: (68/2 - 2)^2 = 1024 windows
+SPLINE_SAMPLE_N = 2048   # side of the timed reference spline V-cycle
+
+
+def cpu_reference_sample(n: int, blocks: int, mode: str, sr_levels: int, wkind: str = "trained"):
+    """Time the reference on ONE bounded sample and project V-cycles/s at n^2: its
+    spline v_cycle at 2048^2 scaled by work (n^2 / 2048^2), plus -- GAN mode -- its full
+    sr_prolong (normalise, 1024 windows of 6x6, generator, stitch, denormalise) on a 68^2 coarse grid,
+    per-window cost x the cycle's SR windows.  The reference arm and the cpu_baseline leg call this
+    same function.  Returns (projected cycles/s, kind, sample description, sample wall seconds)."""
     import numpy as np
     import oracle
     ref = oracle.import_ref()
-    kind = "reference"
-    if ref is None:
-        kind = "port"
+    kind = "reference" if ref is not None else "port"
+    m = min(n, SPLINE_SAMPLE_N)
+    f = _rhs(m)
+    rng = np.random.default_rng(0)
+    c = 1e-4 * _rhs(SR_SAMPLE_NC) + 1e-6 * rng.standard_normal((SR_SAMPLE_NC, SR_SAMPLE_NC))
+    c -= c.mean()
+    nwin_sample = (SR_SAMPLE_NC // 2 - 2) ** 2
+    t_all = time.perf_counter()
     if kind == "reference":
         from mgsr import smoother, solver, srmodel
-        from mgsr.grid import Grid
+        from mgsr.grid import Grid, NormBounds
         w = bench_weights(wkind, blocks, srmodel)
-
-        def fwd(x):
-            return srmodel._forward_batch(w, x)
-
-        def spline_cycle(m):
-            f = _rhs(m)
-            cfg = solver.RunConfig(N_step=1, r_min=8, N_smooth=2)
-            p0 = np.zeros((m, m))
+        cfg = solver.RunConfig(N_step=1, r_min=8, N_smooth=2)
+        t0 = time.perf_counter()
+        solver.v_cycle(Grid(np.zeros((m, m))), smoother.PoissonProblem(Grid(f)), cfg, "spline")
+        t_spline = time.perf_counter() - t0
+        if mode == "gan":
             t0 = time.perf_counter()
-            solver.v_cycle(Grid(p0), smoother.PoissonProblem(Grid(f)), cfg, "spline")
-            return time.perf_counter() - t0
+            srmodel.sr_prolong(Grid(c), w, NormBounds(), 2)
+            t_sr_sample = time.perf_counter() - t0
     else:
         from oracle import mgsr_oracle as orc
         path = weights_path(wkind, blocks)
         w = orc.read_mgsr1(path) if path else orc.random_weights(blocks, 0)
-
-        def fwd(x):
-            return orc.forward_batch(w, x)
-
-        def spline_cycle(m):
-            f = _rhs(m)
+        t0 = time.perf_counter()
+        orc.v_cycle(np.zeros((m, m)), f, orc.Config(N_step=1, r_min=8, N_smooth=2), "spline")
+        t_spline = time.perf_counter() - t0
+        if mode == "gan":
             t0 = time.perf_counter()
-            orc.v_cycle(np.zeros((m, m)), f, orc.Config(N_step=1, r_min=8, N_smooth=2), "spline")
-            return time.perf_counter() - t0
-    m = min(n, 2048)
-    t_spline = spline_cycle(m) * (n * n) / (m * m)
-    t_sr = 0.0
+            orc.sr_prolong(c, w, orc.Bounds(), 2)
+            t_sr_sample = time.perf_counter() - t0
+    t_cycle = t_spline * (n * n) / (m * m)
     nw_total = 0
     if mode == "gan":
-        x = np.random.default_rng(0).uniform(-1, 1, (windows, 1, 6, 6)).repeat(3, axis=1)
-        t0 = time.perf_counter()
-        fwd(x)
-        t_win = (time.perf_counter() - t0) / windows
         for lev in range(1, sr_levels + 1):
             nc = n >> lev
             nw_total += (nc // 2 - 2) ** 2
-        t_sr = t_win * nw_total
-    cyc = 1.0 / (t_spline + t_sr)
+        t_cycle += t_sr_sample / nwin_sample * nw_total
     sample = (f"reference v_cycle(spline) at {m}^2 scaled by work to {n}^2"
-              + (f" + reference generator (B={blocks}) on {windows} windows, per-window cost x "
-                 f"{nw_total} windows (projected)" if mode == "gan" else ""))
-    return cyc, kind, sample
+              + (f" + reference sr_prolong (B={blocks}) on a {SR_SAMPLE_NC}^2 coarse grid ({nwin_sample} windows), "
+                 f"per-window cost x {nw_total} windows" if mode == "gan" else "") + " (projected)")
+    return 1.0 / t_cycle, kind, sample, time.perf_counter() - t_all
 
 
 def _rhs(m):
@@ -433,18 +433,21 @@ def run_reference_arm(args, rank, world):
     ncpu = os.cpu_count() or 1
     vals = []
     kind, sample = "reference", ""
-    windows = 32 if args.mode == "gan" else 0
+    walls = []
     for i in range(args.warmup + args.steps):
-        cyc, kind, sample = cpu_reference_sample(args.n, args.blocks, max(windows, 1), args.mode, args.sr_levels, wkind=args.weights)
+        cyc, kind, sample, wall = cpu_reference_sample(args.n, args.blocks, args.mode, args.sr_levels, wkind=args.weights)
         if i >= args.warmup:
             vals.append(cyc)
+            walls.append(wall)
     v = sum(vals) / len(vals)
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / v, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": workload_config(args),
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": ncpu, "kind": kind, "sample": sample},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": ncpu, "kind": kind, "sample": sample,
+                         "projected": True, "sample_wall_s": sum(walls) / len(walls)},
+        "projected": True,
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gupdates_per_s": v * args.n * args.n / 1e9,
     }
@@ -549,9 +552,10 @@ def main():
                                    "uploads and readbacks on two copy streams, double-buffered across steps"}
         if not args.no_cpu_baseline:
             try:
-                cyc, kind, sample = cpu_reference_sample(n, args.blocks, 256, args.mode, args.sr_levels, wkind=args.weights)
+                cyc, kind, sample, wall = cpu_reference_sample(n, args.blocks, args.mode, args.sr_levels,
+                                                               wkind=args.weights)
                 line["cpu_baseline"] = {"value": cyc, "unit": UNIT, "cores": os.cpu_count(), "kind": kind,
-                                        "sample": sample}
+                                        "sample": sample, "projected": True, "sample_wall_s": wall}
             except Exception as exc:  # the baseline never blocks the GPU line
                 line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
                                         "sample": f"failed: {exc}"}
