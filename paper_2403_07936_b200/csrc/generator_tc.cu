@@ -63,19 +63,26 @@ namespace mgsr {
 namespace tc {
 
 constexpr int T = 3;                 // M tiles per group
-constexpr int WPG = 8;               // windows per group (per CTA)
+constexpr int WPG = 10;              // windows per group (per CTA)
 constexpr int ROWS = 128;            // rows per tile
-// Activations: per 8-channel plane, the group's 8 windows as replicate-padded 8x8 images interleaved by
-// image row: plane row GUARD + (py * 8 + w) * 8 + px for padded row py, window w, padded column px.  Tile
-// tau holds rows py = 2 tau + 1 and 2 tau + 2 of all 8 windows (M = 2 x 8 x 8 = 128), so the pad rows
-// py = 0, 7 are stored but never computed: 48 rows per window instead of 64.  Tap (dy, dx) is the
-// descriptor shift dy * 64 + dx rows.  Two buffers (ping-pong: layer L reads buffer L % 2), because a
-// tile's taps read its neighbours' rows.
-constexpr int IMG_ROWS = 8 * WPG * 8;                 // 512
+// Activations: per 8-channel plane, padded image row py (0..7) of the group's 10 windows occupies 64 plane
+// rows: two 32-row lane blocks, each holding five windows' 6 interior pixels (px = 1..6, row 6 w5 + px - 1)
+// plus 2 spare rows (dead data).  The pad columns px = 0, 7 are not stored: replicate padding is a lane's own
+// partial (see load_dx3).  Plane row GUARD + py * 64 + 32 (w / 5) + 6 (w % 5) + px - 1.  Tile tau holds rows
+// py = 2 tau + 1 and 2 tau + 2 (M = 128), so the pad rows py = 0, 7 are stored but never computed: 38.4 M rows
+// per 36-pixel window (94% useful).  Tap row dy is the descriptor shift dy * 64 rows.  Two buffers (ping-pong:
+// layer L reads buffer L % 2), because a tile's taps read its neighbours' rows.
+constexpr int RPY = 64;                               // plane rows per padded image row
+constexpr int IMG_ROWS = 8 * RPY;                     // 512
 constexpr int GUARD = 8;                              // tap shifts reach one row past the image
 constexpr int PLANE_ROWS = GUARD + IMG_ROWS + GUARD;  // 528
 constexpr int ACT_PLANE = PLANE_ROWS * 16;            // bytes per 8-channel plane
 constexpr int ACT_BYTES = 8 * ACT_PLANE;              // 67584 per buffer
+// a tile row (0..127) -> (padded row offset pyl, window, interior column px); rows 30, 31 of each 32-row lane
+// block are spare (computed, never used)
+__host__ __device__ constexpr bool row_spare(int r) { return (r & 31) >= 30; }
+__host__ __device__ constexpr int row_window(int r) { return row_spare(r) ? 0 : ((r >> 5) & 1) * 5 + (r & 31) / 6; }
+__host__ __device__ constexpr int row_px(int r) { return row_spare(r) ? 1 : (r & 31) % 6 + 1; }
 // CTA pair (cta_group::2): the leader CTA issues M = 256 MMAs whose A rows come 128 from each CTA's
 // activations.  The three taps of a kernel row dy (dx = 0, 1, 2) are ONE MMA with N = 3 x 64 = 192: A is the
 // plane shifted by dy rows only and the accumulator holds y_dx[r] = sum_dy W(dy, dx) a[r + 64 (dy - 1)];
@@ -88,7 +95,7 @@ constexpr int UNIT_BYTES = 3 * 4096;                  // this CTA's half of a ke
 constexpr int ROW_BYTES = 2 * UNIT_BYTES;             // a kernel row in the blob (both halves)
 constexpr int RING_BYTES = NUNIT * UNIT_BYTES;        // 61440
 static_assert(3 * ROW_BYTES == 9 * TAP_BYTES, "a layer is 9 taps");
-constexpr int MISC_BYTES = 8192;                      // q tables (8 x 36 floats) + head im2col index table
+constexpr int MISC_BYTES = 8192;                      // q tables (10 x 36 floats) + head im2col index table
 constexpr int BAR_BYTES = 1024;
 // head phase, in activation buffer 1 (free until layer 0's epilogue): im2col, two buffers
 constexpr int HK = 96;                                   // head K (81 taps padded to an f16 K multiple)
@@ -101,20 +108,25 @@ static_assert(2 * I2C_BYTES <= ACT_BYTES, "im2col");
 static_assert(WPG * 36 * 4 <= IDX_OFF && IDX_OFF + 64 * HK <= MISC_BYTES, "misc");
 // up phase, in activation buffer 0 (free once the post layer's MMAs completed): the up-conv quarter
 // pixel-shuffled onto the 12x12 fine windows, as the tail's A operand: 2 planes (8 channels each) x
-// [Y 12][window 8][X 16] pixel rows of 16 B (X 12..15 never written: they only feed discarded rows).
-// Z tile j holds the kept fine row y = 4 + j of the 8 windows (A rows (window, X)), so the vertical tap dy
+// [Y 12][128 rows: 12 w + X (rows 120..127 spare)] pixel rows of 16 B.
+// Z tile j holds the kept fine row y = 4 + j of the 10 windows (A rows (window, X)), so the vertical tap dy
 // is a 128-row descriptor shift; the horizontal tap dx and the output o go along N (n = 3 dx + o, 27 of
-// 32).  Tail weights per quarter: this CTA's 16 N rows, [dy 9][k 2][16 n][8].
+// 32); the sum over dx crosses lane quadrants, so it goes through shared memory.  Tail weights per
+// quarter: this CTA's 16 N rows, [dy 9][k 2][16 n][8].
+constexpr int UROWS_Y = 128;                           // U pixel rows per fine row Y
+static_assert(WPG * 12 <= UROWS_Y, "U row");
 constexpr int UQ = 16;
 constexpr int UP_QUARTERS_C = 4;
 constexpr int ZT = 4;                                  // Z tiles (kept fine rows)
-constexpr int U_PIX = 12 * WPG * 16;                   // 1536 pixel rows
+constexpr int U_PIX = 12 * UROWS_Y;                    // 1536 pixel rows
 constexpr int U_PLANE = U_PIX * 16;                    // 24576
 constexpr int U_BYTES = 2 * U_PLANE;                   // 49152: the quarter's 16 channels
 constexpr int TW_HALF = 9 * 512;                       // 4608: this CTA's half of a quarter's tail weights
 constexpr int TW_QBYTES = 2 * TW_HALF;                 // a quarter in the blob (both halves)
 constexpr int TW_OFF0 = U_BYTES;
 static_assert(TW_OFF0 + UP_QUARTERS_C * TW_HALF <= ACT_BYTES, "up phase");
+constexpr int ZS_STRIDE = 27;                         // Z scratch: [tile 4][row 128][27] fp32 in buffer 0
+static_assert(ZT * ROWS * ZS_STRIDE * 4 <= ACT_BYTES, "Z scratch");
 constexpr int OFF_ACT = 0;                             // two buffers
 constexpr int OFF_RING = OFF_ACT + 2 * ACT_BYTES;
 constexpr int OFF_MISC = OFF_RING + RING_BYTES;
@@ -633,7 +645,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
                     const uint32_t d = tmem + COL_Z + 32 * j;
 #pragma unroll
                     for (int dy = 0; dy < 9; ++dy) {
-                        const uint64_t a = make_desc(u_base + (j + dy) * (WPG * 16 * 16), U_PLANE, 128);
+                        const uint64_t a = make_desc(u_base + (j + dy) * (UROWS_Y * 16), U_PLANE, 128);
                         const uint64_t b = make_desc(u_base + TW_OFF0 + u * TW_HALF + dy * 512, 256, 128);
                         mma_bf16(d, a, b, idz, (u | dy) > 0);
                     }
@@ -699,8 +711,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
         const int cb = 16 * cq;                // first channel of this thread
         const int et = threadIdx.x - 64;       // 0..511
         const int row = 32 * q + lane;         // row within a tile
-        const int pyl = row >> 6, wrow = (row >> 3) & 7, px = row & 7;   // tile row = (py - 2 t - 1, window, px)
-        const bool interior = px >= 1 && px <= 6;
+        const int pyl = row >> 6, wrow = row_window(row), px = row_px(row);   // tile row = (py - 2 t - 1, window, px)
+        const bool interior = !row_spare(row);
         const uint32_t lane_addr = uint32_t(32 * q) << 16;
         uint32_t af_ph = 0;   // bit b: parity of the next completion of b_acc_full[b]
         int vb = 0;           // accumulator buffer of the next unit (the MMA warp's order)
@@ -723,9 +735,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
         // a 3x3 unit: columns n = 96 h + 48 (oc' / 16) + 16 dx + oc' % 16 (h = output-channel half, so a
         // thread's 48 columns are contiguous: one x32 and one x16 load); out[r] = y_0[r - 1] + y_1[r]
         // + y_2[r + 1], the row's px -+ 1 neighbours being lanes -+ 1.  Replicate padding: the pad column
-        // px = 0 equals px = 1, so the y_0 px = 1 needs is its own (and px = 6 takes its own y_2): the pad rows'
-        // results are never used and their activations are dead data.  One indexed shuffle per partial.
-        const int src_l = px == 1 ? lane : lane - 1, src_r = px == 6 ? lane : lane + 1;
+        // px = 0 equals px = 1, so the y_0 px = 1 needs is its own (and px = 6 takes its own y_2); the pad
+        // columns are therefore never stored.  Spare lanes take their own partials (dead data).  One indexed
+        // shuffle per partial.
+        const int src_l = (px == 1 || !interior) ? lane : lane - 1, src_r = (px == 6 || !interior) ? lane : lane + 1;
         auto load_dx3 = [&](float (&y)[16]) {
             const uint32_t c = acc_wait() + (cq >> 1) * 96 + (cq & 1) * 48;
             uint32_t v01[32], v2[16];
@@ -771,8 +784,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
             ++i2c_uses[ib];
             {
                 const int r = et & 127, part4 = et >> 7;
-                const int rp = (2 * t + 1 + (r >> 6)) * 8 + (r & 7);   // padded pixel (py, px)
-                const float *qt = misc + ((r >> 3) & 7) * 36;
+                const int rp = (2 * t + 1 + (r >> 6)) * 8 + row_px(r);   // padded pixel (py, px)
+                const float *qt = misc + row_window(r) * 36;
                 const uint2 *ix = reinterpret_cast<const uint2 *>(idx_tab + rp * HK);
 #pragma unroll
                 for (int kk = 0; kk < HPLANES / 4; ++kk) {
@@ -931,7 +944,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
 #pragma unroll
                         for (int sub = 0; sub < 4; ++sub) {
                             const int Y = 2 * (py - 1) + (sub >> 1), X = 2 * (px - 1) + (sub & 1);
-                            *reinterpret_cast<uint2 *>(Ub + ((Y * WPG + wrow) * 16 + X) * 16) =
+                            *reinterpret_cast<uint2 *>(Ub + (Y * UROWS_Y + 12 * wrow + X) * 16) =
                                 make_uint2(pack_op<F16>(y[sub], y[4 + sub]), pack_op<F16>(y[8 + sub], y[12 + sub]));
                         }
                         const long long k = k0 + wrow;
@@ -968,31 +981,34 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
                 for (int t = 0; t < T; ++t) build_i2c(t);   // tile 2 reuses buffer 0 once head tile 0 multiplied
             }
             // ---- stitched pixels: warps of channel quarter cq = j finish Z tile j (kept fine row y = 4 + j).
-            // Lane (quadrant q, lane) holds Z row (window 2 q + lane / 16, X = lane % 16); the kept pixel X
-            // in 4..7 sums Z[X + dx - 4][3 dx + o] over dx by shuffles, then bias + s tanh(./s), channel
-            // mean, denormalise, straight into the fine grid.  Edge windows are k_tail_edge's. ----
+            // Lane (quadrant q, lane) holds Z row 32 q + lane = 12 w + X; its 27 partials go to shared memory
+            // (buffer 0: U and the tail weights are consumed once the last Z tile's MMAs completed), then the
+            // kept pixel (w, X' = 4..7) sums Z[12 w + X' + dx - 4][3 dx + o] over dx, adds the bias, applies
+            // s tanh(./s), the channel mean and the denormalisation, straight into the fine grid.  Edge windows
+            // are k_tail_edge's. ----
             {
                 const int j = cq;
-                mbar_wait(b_zfull + 8 * j, z_ph);
+                mbar_wait(b_zfull + 8 * (ZT - 1), z_ph);   // every Z tile done: buffer 0 is free
                 tr(13, 0, j);
                 tc_fence_after();
                 uint32_t z0[16], z1[16];
                 TMEM_LD16(tmem + lane_addr + COL_Z + 32 * j, z0);
                 TMEM_LD16(tmem + lane_addr + COL_Z + 32 * j + 16, z1);
                 tmem_wait_ld();
-                const int X = lane & 15;
-                float pre[3] = {tail_b[0], tail_b[1], tail_b[2]};
+                float *zs = reinterpret_cast<float *>(ubuf) + j * (ROWS * ZS_STRIDE);
 #pragma unroll
-                for (int dx = 0; dx < 9; ++dx) {
-                    const int src = (lane & 16) | ((X + dx - 4) & 15);
+                for (int n = 0; n < 27; ++n) zs[row * ZS_STRIDE + n] = __uint_as_float(n < 16 ? z0[n] : z1[n - 16]);
+                asm volatile("bar.sync %0, 128;" ::"r"(2 + j) : "memory");   // the 4 warps of Z tile j
+                if (row < WPG * 4) {
+                    const int w = row >> 2, X = 4 + (row & 3);
+                    float pre[3] = {tail_b[0], tail_b[1], tail_b[2]};
 #pragma unroll
-                    for (int o = 0; o < 3; ++o) {
-                        const int n = 3 * dx + o;
-                        pre[o] += __shfl_sync(0xffffffffu, __uint_as_float(n < 16 ? z0[n] : z1[n - 16]), src);
+                    for (int dx = 0; dx < 9; ++dx) {
+                        const float *zr = zs + (12 * w + X + dx - 4) * ZS_STRIDE + 3 * dx;
+#pragma unroll
+                        for (int o = 0; o < 3; ++o) pre[o] += zr[o];
                     }
-                }
-                if (X >= 4 && X < 8) {
-                    const Win W = window_of(P, k0 + 2 * q + (lane >> 4));
+                    const Win W = window_of(P, k0 + w);
                     if (W.valid && !W.edge) {
                         double m = 0.0;
 #pragma unroll
