@@ -36,10 +36,13 @@ int launch_sr_prolong(const mgsr_gen *g, const double *c, const double *c_shift,
                       double p_max, int precision, double *out, double *out_mean, void *ws, size_t ws_bytes,
                       void *red_slot, cudaStream_t st, cudaEvent_t *gen_markers = nullptr);
 
-// tensor-core generator (generator_tc.cu): windows of a 6x6 pass, ratio 2.
+// tensor-core generator (generator_tc.cu): a ratio-2 pass (one application) and a ratio-4 pass (two).
 int tc_pack_weights(mgsr_gen *g, const float *const *host_tensors);
 size_t tc_workspace_bytes(int64_t nc);
+size_t tc4_workspace_bytes(int64_t nc);
 int launch_sr_pass_tc(const mgsr_gen *g, const double *c, const double *c_shift, int nc, double log_lo,
                       double span, double *fine, void *ws, size_t ws_bytes, cudaStream_t st, int f16);
+int launch_sr_pass4_tc(const mgsr_gen *g, const double *c, const double *c_shift, int nc, double log_lo,
+                       double span, double *fine, void *ws, size_t ws_bytes, cudaStream_t st, int f16);
 
 }  // namespace mgsr

@@ -412,7 +412,12 @@ size_t sr_workspace_bytes(int64_t nc, int s, int precision) {
     size_t inter = (s == 8 || s == 16) ? sizeof(double) * size_t(nc * 4) * size_t(nc * 4) : 0;
     // the fp32 CUDA-core chunk buffers only for fp32 (the tensor-core precisions never fall back to them)
     size_t simt = tensor_core_precision(precision) ? 0 : sizeof(float) * pass_ws_floats(s == 2 ? 1 : 2) + 4096;
-    size_t tc = tensor_core_precision(precision) ? tc_workspace_bytes(nc) : 0;
+    size_t tc = 0;
+    if (tensor_core_precision(precision)) {   // the largest pass of the plan: (ratio, coarse side) per pass
+        tc = s == 2 ? tc_workspace_bytes(nc) : tc4_workspace_bytes(nc);
+        if (s == 8 && tc_workspace_bytes(4 * nc) > tc) tc = tc_workspace_bytes(4 * nc);
+        if (s == 16 && tc4_workspace_bytes(4 * nc) > tc) tc = tc4_workspace_bytes(4 * nc);
+    }
     return inter + (simt > tc ? simt : tc) + 512;
 }
 
@@ -490,12 +495,12 @@ int launch_sr_prolong(const mgsr_gen *g, const double *c, const double *c_shift,
         if (mark) MGSR_CUDA_TRY(cudaEventRecordWithFlags(gen_markers[0], st, cudaEventRecordExternal));
         if (tensor_core_precision(precision)) {
             // tensor-core path only; no silent fallback to the fp32 CUDA-core path
-            if (apps != 1 || !g->tc_blob) {
-                set_error("tensor-core generator supports 6x6 windows (ratio-2 passes) only");
-                return MGSR_E_UNSUPPORTED;
-            }
-            r = launch_sr_pass_tc(g, src, src_shift, n_in, log_lo, span, dst, w, ws_bytes - (w - static_cast<char *>(ws)), st,
-                                  precision == MGSR_PREC_FP16);
+            if (!g->tc_blob) { set_error("tensor-core weights not packed"); return MGSR_E_UNSUPPORTED; }
+            const size_t left = ws_bytes - size_t(w - static_cast<char *>(ws));
+            r = apps == 1 ? launch_sr_pass_tc(g, src, src_shift, n_in, log_lo, span, dst, w, left, st,
+                                              precision == MGSR_PREC_FP16)
+                          : launch_sr_pass4_tc(g, src, src_shift, n_in, log_lo, span, dst, w, left, st,
+                                               precision == MGSR_PREC_FP16);
         } else {
             r = sr_pass_simt(g, src, src_shift, n_in, apps, log_lo, span, dst, reinterpret_cast<float *>(w), st);
         }

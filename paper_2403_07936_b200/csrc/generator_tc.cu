@@ -63,29 +63,52 @@ namespace mgsr {
 namespace tc {
 
 constexpr int T = 3;                 // M tiles per group
-constexpr int WPG = 10;              // windows per group (per CTA)
 constexpr int ROWS = 128;            // rows per tile
-// Activations: per 8-channel plane, padded image row py (0..7) of the group's 10 windows occupies 64 plane
-// rows: two 32-row lane blocks, each holding five windows' 6 interior pixels (px = 1..6, row 6 w5 + px - 1)
-// plus 2 spare rows (dead data).  The pad columns px = 0, 7 are not stored: replicate padding is a lane's own
-// partial (see load_dx3).  Plane row GUARD + py * 64 + 32 (w / 5) + 6 (w % 5) + px - 1.  Tile tau holds rows
-// py = 2 tau + 1 and 2 tau + 2 (M = 128), so the pad rows py = 0, 7 are stored but never computed: 38.4 M rows
-// per 36-pixel window (94% useful).  Tap row dy is the descriptor shift dy * 64 rows.  Two buffers (ping-pong:
-// layer L reads buffer L % 2), because a tile's taps read its neighbours' rows.
-constexpr int RPY = 64;                               // plane rows per padded image row
-constexpr int IMG_ROWS = 8 * RPY;                     // 512
-constexpr int GUARD = 8;                              // tap shifts reach one row past the image
-constexpr int PLANE_ROWS = GUARD + IMG_ROWS + GUARD;  // 528
-constexpr int ACT_PLANE = PLANE_ROWS * 16;            // bytes per 8-channel plane
-constexpr int ACT_BYTES = 8 * ACT_PLANE;              // 67584 per buffer
-// a tile row (0..127) -> (padded row offset pyl, window, interior column px); rows 30, 31 of each 32-row lane
-// block are spare (computed, never used)
-__host__ __device__ constexpr bool row_spare(int r) { return (r & 31) >= 30; }
-__host__ __device__ constexpr int row_window(int r) { return row_spare(r) ? 0 : ((r >> 5) & 1) * 5 + (r & 31) / 6; }
-__host__ __device__ constexpr int row_px(int r) { return row_spare(r) ? 1 : (r & 31) % 6 + 1; }
+constexpr int GUARD = 8;             // plane rows before / after the image
+// Pass variants (template parameter V of k_gen_tc):
+//   V = 0  ratio-2 pass: 6x6 windows of q (3 identical channels), tail pruned to the kept pixels;
+//   V = 1  first application of a ratio-4 pass: 6x6 windows of q, the full 12x12x3 output (replicate-
+//          padded 9x9 tail at every pixel) -> X1 in global memory (fp16, the next head's operand format);
+//   V = 2  second application: 12x12 windows of X1 (3 distinct channels), tail pruned to the kept 8x8 fine
+//          pixels of the 24x24 output (srmodel.py:443-467, _PASS_PLAN).
+// Activations: per 8-channel plane, padded image row py (0 .. WS + 1) of the group's windows occupies RPY
+// plane rows: RPY / 32 lane blocks of 32 rows, each holding WPB windows' WS interior pixels (px = 1..WS, row
+// WS w' + px - 1) plus spare rows (dead data).  The pad columns px = 0, WS + 1 are not stored: replicate
+// padding is a lane's own partial (see load_dx3).  Tile tau holds rows py = TPY tau + 1 .. TPY tau + TPY
+// (M = 128), so the pad rows py = 0, WS + 1 are stored but never computed.  Tap row dy is the descriptor
+// shift dy * RPY rows.  Two buffers (ping-pong: layer L reads buffer L % 2), because a tile's taps read its
+// neighbours' rows.
+//   V = 0, 1: 10 windows per group (two lane blocks of 5 x 6 px + 2 spare; 94% useful M rows);
+//   V = 2:    2 windows per group (one lane block of 2 x 12 px + 8 spare; 75%).
+template <int V>
+struct Geo {
+    static constexpr int WS = V == 2 ? 12 : 6;            // input window side
+    static constexpr int NPY = WS + 2;                    // padded image rows
+    static constexpr int RPY = V == 2 ? 32 : 64;          // plane rows per padded image row
+    static constexpr int TPY = ROWS / RPY;                // padded rows per tile
+    static constexpr int WPB = 32 / WS;                   // windows per 32-lane block (5, 2)
+    static constexpr int WPG = (RPY / 32) * WPB;          // windows per group (per CTA): 10, 2
+    static constexpr int ACT_PLANE = (2 * GUARD + NPY * RPY) * 16;   // bytes per 8-channel plane
+    static constexpr int HK = V == 2 ? 256 : 96;          // head K: 81 (x 3 distinct channels) taps, padded
+    static constexpr int I2C_PLANES = V == 2 ? 8 : 12;    // planes per im2col build (K 64 / 96)
+    static constexpr int NBUILD = HK / (8 * I2C_PLANES);  // im2col builds per tile (4 / 1)
+    static constexpr int HUNITS = V == 2 ? 2 : 1;         // ring units of this CTA's head weights
+    static constexpr int NZC = V == 1 ? 3 : 1;            // up-phase chunks (V = 1: 4 output rows each)
+    static constexpr int ZT = V == 2 ? 2 : 4;             // Z tiles per chunk
+    static constexpr int UROWS_Y = V == 2 ? 32 : 128;     // U pixel rows per fine row
+    static constexpr int UNY = V == 2 ? 16 : 12;          // U fine rows held
+    static constexpr int U_PLANE = UNY * UROWS_Y * 16;
+    static constexpr int ZSH = V == 2 ? 4 : 1;            // fine rows per Z tile (Z tile j: shift ZSH j)
+    static constexpr int QN = V == 2 ? 432 : 36;          // input values per window (misc q tables)
+    __host__ __device__ static constexpr bool spare(int r) { return (r & 31) >= WPB * WS; }
+    __host__ __device__ static constexpr int window(int r) { return spare(r) ? 0 : ((r % RPY) >> 5) * WPB + (r & 31) / WS; }
+    __host__ __device__ static constexpr int px(int r) { return spare(r) ? 1 : (r & 31) % WS + 1; }
+};
+constexpr int ACT_BYTES = 8 * Geo<0>::ACT_PLANE;     // 67584 per buffer (the largest variant)
+static_assert(8 * Geo<2>::ACT_PLANE <= ACT_BYTES, "activation buffer");
 // CTA pair (cta_group::2): the leader CTA issues M = 256 MMAs whose A rows come 128 from each CTA's
 // activations.  The three taps of a kernel row dy (dx = 0, 1, 2) are ONE MMA with N = 3 x 64 = 192: A is the
-// plane shifted by dy rows only and the accumulator holds y_dx[r] = sum_dy W(dy, dx) a[r + 64 (dy - 1)];
+// plane shifted by dy rows only and the accumulator holds y_dx[r] = sum_dy W(dy, dx) a[r + RPY (dy - 1)];
 // the epilogue forms out[r] = y_0[r - 1] + y_1[r] + y_2[r + 1] with lane shuffles (a row's px -+ 1
 // neighbours are the adjacent lanes), so A is read from shared memory 3 times per layer instead of 9.
 // B is split along N: each CTA's ring unit holds its 32 output channels for the 3 dx taps (N = 96).
@@ -95,38 +118,44 @@ constexpr int UNIT_BYTES = 3 * 4096;                  // this CTA's half of a ke
 constexpr int ROW_BYTES = 2 * UNIT_BYTES;             // a kernel row in the blob (both halves)
 constexpr int RING_BYTES = NUNIT * UNIT_BYTES;        // 61440
 static_assert(3 * ROW_BYTES == 9 * TAP_BYTES, "a layer is 9 taps");
-constexpr int MISC_BYTES = 8192;                      // q tables (10 x 36 floats) + head im2col index table
+constexpr int MISC_BYTES = 8192;                      // q tables (10 x 36 / 2 x 432 floats) + head im2col index table
 constexpr int BAR_BYTES = 1024;
-// head phase, in activation buffer 1 (free until layer 0's epilogue): im2col, two buffers
-constexpr int HK = 96;                                   // head K (81 taps padded to an f16 K multiple)
-constexpr int HPLANES = HK / 8;                          // 12 planes of 8 fp16
-constexpr int I2C_BYTES = HPLANES * ROWS * 16;           // 24576 per im2col buffer (two buffers)
+// head phase, in activation buffer 1 (free until layer 0's epilogue): im2col, two buffers.  V = 0, 1: fp16
+// MMA over the 81 folded taps (the 3 identical input channels summed into the weights) padded to K = 96,
+// indices from a table; V = 2: K = 3 x 81 padded to 256, built in four K = 64 parts per tile.
+constexpr int HPLANES = 12;                              // V = 0, 1 head K planes of 8 fp16
+constexpr int I2C_BYTES = 12 * ROWS * 16;                // 24576 per im2col buffer (two buffers)
 constexpr int HB_BYTES = HPLANES * 64 * 16;              // 12288: two halves of 32 oc
 constexpr int HB_HALF = HB_BYTES / 2;                    // 6144, streamed through the ring (one unit)
+constexpr int HB4_BYTES = 32 * 64 * 16;                  // V = 2: 32768, halves of 16384 = two ring units
+constexpr int HB4_HALF = HB4_BYTES / 2;
 constexpr int IDX_OFF = 2048;                            // in misc: uint8 [64 padded pixels][96 k] -> q index
 static_assert(2 * I2C_BYTES <= ACT_BYTES, "im2col");
-static_assert(WPG * 36 * 4 <= IDX_OFF && IDX_OFF + 64 * HK <= MISC_BYTES, "misc");
+static_assert(Geo<0>::WPG * 36 * 4 <= IDX_OFF && IDX_OFF + 64 * 96 <= MISC_BYTES, "misc");
+static_assert(Geo<2>::WPG * 432 * 4 <= MISC_BYTES, "misc (V = 2)");
 // up phase, in activation buffer 0 (free once the post layer's MMAs completed): the up-conv quarter
-// pixel-shuffled onto the 12x12 fine windows, as the tail's A operand: 2 planes (8 channels each) x
-// [Y 12][128 rows: 12 w + X (rows 120..127 spare)] pixel rows of 16 B.
-// Z tile j holds the kept fine row y = 4 + j of the 10 windows (A rows (window, X)), so the vertical tap dy
-// is a 128-row descriptor shift; the horizontal tap dx and the output o go along N (n = 3 dx + o, 27 of
-// 32); the sum over dx crosses lane quadrants, so it goes through shared memory.  Tail weights per
-// quarter: this CTA's 16 N rows, [dy 9][k 2][16 n][8].
-constexpr int UROWS_Y = 128;                           // U pixel rows per fine row Y
-static_assert(WPG * 12 <= UROWS_Y, "U row");
+// pixel-shuffled onto the fine windows, as the tail's A operand: 2 planes (8 channels each) x UNY fine rows x
+// UROWS_Y pixel rows of 16 B.
+//   V = 0: rows [Y 12][12 w + X] (120 of 128 used); Z tile j = kept fine row y = 4 + j of the 10 windows
+//          (A rows (window, X)), so the vertical tap dy is a 128-row descriptor shift;
+//   V = 1: chunk zc holds fine rows 4 zc - 4 .. 4 zc + 7 (replicate-clamped at the window edge); Z tile j =
+//          fine row 4 zc + j;
+//   V = 2: rows [Y 4..19][16 w + X - 4] (X 4..19: what the kept X 8..15 read); Z tile j = fine rows
+//          8 + 4 j .. 11 + 4 j.
+// The horizontal tap dx and the output o go along N (n = 3 dx + o, 27 of 32).  V = 0, 1 sum over dx through
+// shared memory (a window's row crosses lane quadrants), V = 2 by lane shuffles.  Tail weights per quarter:
+// this CTA's 16 N rows, [dy 9][k 2][16 n][8].
 constexpr int UQ = 16;
 constexpr int UP_QUARTERS_C = 4;
-constexpr int ZT = 4;                                  // Z tiles (kept fine rows)
-constexpr int U_PIX = 12 * UROWS_Y;                    // 1536 pixel rows
-constexpr int U_PLANE = U_PIX * 16;                    // 24576
-constexpr int U_BYTES = 2 * U_PLANE;                   // 49152: the quarter's 16 channels
+constexpr int U_BYTES_MAX = 2 * Geo<0>::U_PLANE;       // 49152
 constexpr int TW_HALF = 9 * 512;                       // 4608: this CTA's half of a quarter's tail weights
 constexpr int TW_QBYTES = 2 * TW_HALF;                 // a quarter in the blob (both halves)
-constexpr int TW_OFF0 = U_BYTES;
+constexpr int TW_OFF0 = U_BYTES_MAX;
+static_assert(2 * Geo<2>::U_PLANE <= TW_OFF0 && 2 * Geo<1>::U_PLANE <= TW_OFF0, "U");
 static_assert(TW_OFF0 + UP_QUARTERS_C * TW_HALF <= ACT_BYTES, "up phase");
-constexpr int ZS_STRIDE = 27;                         // Z scratch: [tile 4][row 128][27] fp32 in buffer 0
-static_assert(ZT * ROWS * ZS_STRIDE * 4 <= ACT_BYTES, "Z scratch");
+constexpr int ZS_STRIDE = 27;                         // Z scratch: [tile][row 128][27] fp32 in buffer 0
+static_assert(4 * ROWS * ZS_STRIDE * 4 <= ACT_BYTES, "Z scratch (V = 0)");
+static_assert(2 * ROWS * ZS_STRIDE * 4 <= U_BYTES_MAX, "Z scratch (V = 1, in U)");
 constexpr int OFF_ACT = 0;                             // two buffers
 constexpr int OFF_RING = OFF_ACT + 2 * ACT_BYTES;
 constexpr int OFF_MISC = OFF_RING + RING_BYTES;
@@ -135,7 +164,7 @@ constexpr int OFF_CONST = OFF_BAR + BAR_BYTES;
 // TMEM columns: two 192-column accumulator buffers (accumulator units alternate between them: head tiles,
 // body / post tiles, up-quarter tiles), then the packed global skip
 constexpr int COL_ACC = 0, ACC_COLS = 192, COL_SKIP = 384;
-constexpr int COL_Z = COL_SKIP;   // tail accumulators (32 per Z tile, 4 tiles) reuse the skip columns + the spare 32
+constexpr int COL_Z = COL_SKIP;   // tail accumulators (32 per Z tile, <= 4 tiles) reuse the skip columns + the spare 32
 
 constexpr int NEPI = 16;                       // epilogue warps
 constexpr int NTHREADS = 64 + 32 * NEPI;       // 576
@@ -148,7 +177,7 @@ __host__ __device__ inline int smem_bytes(int nl) { return OFF_CONST + 4 * const
 
 // blob layout (bytes); body layer count NL = 2B + 1
 struct BlobLayout {
-    size_t head_b, body, up, tail, tail_f32, consts, fmt_stride, total;
+    size_t head_b, body, up, tail, tail_f32, consts, head4, fmt_stride, total;
     int nl;
 };
 
@@ -159,10 +188,12 @@ __host__ __device__ inline BlobLayout blob_layout(int blocks) {
     L.body = L.head_b + HB_BYTES;
     L.up = L.body + size_t(L.nl) * 3 * ROW_BYTES;
     L.tail = L.up + size_t(UP_QUARTERS) * 3 * ROW_BYTES;
-    L.tail_f32 = L.tail + size_t(UP_QUARTERS) * TW_QBYTES;   // then [3][64][81] fp32 (edge kernel)
+    L.tail_f32 = L.tail + size_t(UP_QUARTERS) * TW_QBYTES;   // then [3][64][81] fp32 (edge kernels)
     L.consts = L.tail_f32 + sizeof(float) * 3 * 64 * 81;
+    // V = 2 head (3 distinct input channels, fp16): [half][kc 32][32 oc][8]
+    L.head4 = ((L.consts + sizeof(float) * const_floats(L.nl)) + 1023) & ~size_t(1023);
     // fp16 operand set (body, up, tail) follows at +fmt_stride from the bf16 set
-    L.fmt_stride = ((L.consts + sizeof(float) * const_floats(L.nl)) + 1023) & ~size_t(1023);
+    L.fmt_stride = (L.head4 + HB4_BYTES + 1023) & ~size_t(1023);
     L.total = L.fmt_stride + L.tail_f32;
     return L;
 }
@@ -358,6 +389,7 @@ struct Params {
     float *dbg;
     int dbg_layer;
     unsigned long long *prof;   // optional event trace (bring-up instrumentation, tests/tc_trace.py)
+    uint16_t *x1;               // ratio-4 passes: [nwin][3][12][12] fp16 first-application output (V = 1 -> V = 2)
 };
 
 // Event trace of one steady-state group of CTA 0: role r (0 producer, 1 MMA, 2 epilogue warp 2,
@@ -414,8 +446,10 @@ __device__ __forceinline__ double denormalize_q(double q, double log_lo, double 
 }
 
 // INSTR: bring-up instrumentation (P.prof event trace, P.dbg layer dumps) compiled in
-template <bool F16, bool INSTR>
+template <bool F16, bool INSTR, int V>
 __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
+    using G = Geo<V>;
+    constexpr int RPY = G::RPY, TPY = G::TPY, GWPG = G::WPG, ACT_PLANE = G::ACT_PLANE;
     extern __shared__ __align__(128) uint8_t smem[];
     uint8_t *act = smem + OFF_ACT;   // two buffers of ACT_BYTES
     uint8_t *ring = smem + OFF_RING;
@@ -438,7 +472,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
     const uint32_t b_i2c_empty = smem_u32(bars + BB + 9);   // [2] (both) im2col buffer consumed
     const uint32_t b_ubuf_full = smem_u32(bars + BB + 11);  // (leader) drains -> MMA: the quarter's U written
     const uint32_t b_ubuf_free = smem_u32(bars + BB + 12);  // (both) tail MMAs -> drains: U consumed
-    const uint32_t b_zfull = smem_u32(bars + BB + 13);      // [ZT] (both) last tail MMAs -> epilogue: Z ready
+    const uint32_t b_zfull = smem_u32(bars + BB + 13);      // [4] (both) last tail MMAs -> epilogue: Z ready
     const uint32_t b_tw_full = smem_u32(bars + BB + 17);    // [4] this CTA's quarter tail weights landed
     const uint32_t b_tw_peerfull = smem_u32(bars + BB + 21);   // [4] (leader) the peer's landed
     const uint32_t b_tw_empty = smem_u32(bars + BB + 25);   // [4] (both) tail MMAs of the quarter done
@@ -477,7 +511,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
         mbar_init(b_ubuf_full, 2 * NEPI);
         mbar_init(b_ubuf_free, 1);
         mbar_init(b_post_done, 1);
-        for (int j = 0; j < ZT; ++j) mbar_init(b_zfull + 8 * j, 1);
+        for (int j = 0; j < 4; ++j) mbar_init(b_zfull + 8 * j, 1);
         for (int u = 0; u < UP_QUARTERS_C; ++u) {
             mbar_init(b_tw_full + 8 * u, 1);
             mbar_init(b_tw_peerfull + 8 * u, 1);
@@ -512,25 +546,33 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
             slot = slot == NUNIT - 1 ? 0 : slot + 1;
         };
         for (int gp = pair; gp < ngp; gp += npairs) {
-            fill(wblob + BL.head_b + rank * HB_HALF, HB_HALF);   // this CTA's half of the head weights
+            if constexpr (V == 2) {   // this CTA's half of the 3-channel head weights, two K halves
+                fill(wblob + BL.head4 + rank * HB4_HALF, HB4_HALF / 2);
+                fill(wblob + BL.head4 + rank * HB4_HALF + HB4_HALF / 2, HB4_HALF / 2);
+            } else {
+                fill(wblob + BL.head_b + rank * HB_HALF, HB_HALF);   // this CTA's half of the head weights
+            }
             for (int L = 0; L < NLAYERS; ++L)
                 for (int dy = 0; dy < 3; ++dy)
                     fill(wblob + P.wfmt + BL.body + (size_t(L) * 3 + dy) * ROW_BYTES + rank * UNIT_BYTES);
-            for (int u = 0; u < UP_QUARTERS; ++u) {
-                for (int dy = 0; dy < 3; ++dy)
-                    fill(wblob + P.wfmt + BL.up + (size_t(u) * 3 + dy) * ROW_BYTES + rank * UNIT_BYTES);
-                // this CTA's half of the quarter's tail weights -> buffer 0, once the post layer's MMAs
-                // released it and the last group's tail MMAs of quarter u completed
-                if (u == 0) mbar_wait(b_post_done, grp_ph);
-                mbar_wait(b_tw_empty + 8 * u, tw_ph[u] ^ 1u);
-                tw_ph[u] ^= 1u;
-                if (elect_one()) {
-                    mbar_expect_tx(b_tw_full + 8 * u, TW_HALF);
-                    bulk_g2s(smem_u32(ubuf + TW_OFF0 + u * TW_HALF),
-                             wblob + P.wfmt + BL.tail + size_t(u) * TW_QBYTES + rank * TW_HALF, TW_HALF, b_tw_full + 8 * u);
+            for (int zc = 0; zc < G::NZC; ++zc)
+                for (int u = 0; u < UP_QUARTERS; ++u) {
+                    for (int dy = 0; dy < 3; ++dy)
+                        fill(wblob + P.wfmt + BL.up + (size_t(u) * 3 + dy) * ROW_BYTES + rank * UNIT_BYTES);
+                    if (zc > 0) continue;   // the tail weights stay for every chunk of the group
+                    // this CTA's half of the quarter's tail weights -> buffer 0, once the post layer's MMAs
+                    // released it and the last group's tail MMAs of quarter u completed
+                    if (u == 0) mbar_wait(b_post_done, grp_ph);
+                    mbar_wait(b_tw_empty + 8 * u, tw_ph[u] ^ 1u);
+                    tw_ph[u] ^= 1u;
+                    if (elect_one()) {
+                        mbar_expect_tx(b_tw_full + 8 * u, TW_HALF);
+                        bulk_g2s(smem_u32(ubuf + TW_OFF0 + u * TW_HALF),
+                                 wblob + P.wfmt + BL.tail + size_t(u) * TW_QBYTES + rank * TW_HALF, TW_HALF,
+                                 b_tw_full + 8 * u);
+                    }
+                    __syncwarp();
                 }
-                __syncwarp();
-            }
             grp_ph ^= 1u;
         }
     } else if (warp == 1 && !leader) {
@@ -547,13 +589,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
             }
         };
         for (int gp = pair; gp < ngp; gp += npairs) {   // same order as the producer's fills
-            fwd(1 + NLAYERS * 3);
-            for (int u = 0; u < UP_QUARTERS; ++u) {
-                fwd(3);
-                mbar_wait(b_tw_full + 8 * u, twp);
-                if (elect_one()) mbar_arrive_leader(b_tw_peerfull + 8 * u);
-                __syncwarp();
-            }
+            fwd(G::HUNITS + NLAYERS * 3);
+            for (int zc = 0; zc < G::NZC; ++zc)
+                for (int u = 0; u < UP_QUARTERS; ++u) {
+                    fwd(3);
+                    if (zc > 0) continue;
+                    mbar_wait(b_tw_full + 8 * u, twp);
+                    if (elect_one()) mbar_arrive_leader(b_tw_peerfull + 8 * u);
+                    __syncwarp();
+                }
             twp ^= 1u;
         }
     } else if (warp == 1) {
@@ -574,9 +618,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
         };
         // one 3x3 64 -> 64 layer over the three tiles (body, post, up quarter), reading buffer `buf`: per tile
         // three N = 192 MMA chains (kernel rows dy) of K = 64.  wait_act: the rows each kernel row reads are
-        // written -- tile t's rows dy = 0, 1 read padded rows 2t .. 2t + 2 (tiles <= t), only dy = 2 reaches
-        // row 2t + 3 of tile t + 1, so the previous layer's tile t + 1 epilogue is waited for just before it
-        // (two thirds of a tile's MMAs of extra slack for the epilogue)
+        // written -- tile t's rows dy = 0, 1 read padded rows up to its own, only dy = 2 reaches the first row
+        // of tile t + 1, so the previous layer's tile t + 1 epilogue is waited for just before it
         auto conv_layer = [&](int lid, int buf, bool wait_act, auto &&after_t0) {
             const uint64_t a_desc0 = make_desc(act_base + buf * ACT_BYTES, ACT_PLANE, 128);
 #pragma unroll
@@ -585,7 +628,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
                 acquire_acc();
                 if (lane == 0) tr(2, lid, t);
                 tc_fence_after();
-                const uint64_t a_t = a_desc0 + uint64_t(GUARD + (2 * t + 1) * 64);
+                const uint64_t a_t = a_desc0 + uint64_t(GUARD + (TPY * t + 1) * RPY);
                 const uint32_t d = tmem + COL_ACC + ACC_COLS * vb;
                 if (elect_one()) {
 #pragma unroll
@@ -603,7 +646,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
                             if (dy == 0) tr(4, lid, 0);
                             tc_fence_after();
                         }
-                        const uint64_t a = a_t + uint64_t(int64_t((dy - 1) * 64));
+                        const uint64_t a = a_t + uint64_t(int64_t((dy - 1) * RPY));
                         const uint64_t b = make_desc(ring_base + s * UNIT_BYTES, 128, 1024);   // 12 n-groups of 8
 #pragma unroll
                         for (int ks = 0; ks < 4; ++ks)
@@ -629,11 +672,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
             slot0 += 3;
             slot0 = slot0 >= NUNIT ? slot0 - NUNIT : slot0;
         };
-        // pruned 9x9 tail, quarter u: Z[j] (M = 256 pixels of kept fine row 4 + j, N = 32 = 3 dx + o) +=
-        // sum over dy of U shifted by j + dy fine rows x TW[u][dy]; 36 MMAs
+        // pruned 9x9 tail, quarter u: Z[j] (M = 256 pixels of the tile's fine rows, N = 32 = 3 dx + o) +=
+        // sum over dy of U shifted by ZSH j + dy fine rows x TW[u][dy]
         const uint32_t idz = F16 ? idesc_f16(32) : idesc_bf16(32);
-        uint32_t grp_ph = 0;   // parity of this pair's group iteration (one TW / Z completion per group)
-        auto tail_mma = [&](int u) {
+        uint32_t grp_ph = 0;   // parity of this pair's group iteration (one TW completion per group)
+        auto tail_mma = [&](int u, bool last_chunk) {
             mbar_wait(b_tw_full + 8 * u, grp_ph);
             mbar_wait(b_tw_peerfull + 8 * u, grp_ph);
             mbar_wait(b_ubuf_full, uint32_t(u & 1));
@@ -641,66 +684,82 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
             tc_fence_after();
             if (elect_one()) {
 #pragma unroll 1
-                for (int j = 0; j < ZT; ++j) {
+                for (int j = 0; j < G::ZT; ++j) {
                     const uint32_t d = tmem + COL_Z + 32 * j;
 #pragma unroll
                     for (int dy = 0; dy < 9; ++dy) {
-                        const uint64_t a = make_desc(u_base + (j + dy) * (UROWS_Y * 16), U_PLANE, 128);
+                        const uint64_t a = make_desc(u_base + (G::ZSH * j + dy) * (G::UROWS_Y * 16), G::U_PLANE, 128);
                         const uint64_t b = make_desc(u_base + TW_OFF0 + u * TW_HALF + dy * 512, 256, 128);
                         mma_bf16(d, a, b, idz, (u | dy) > 0);
                     }
                     if (u == UP_QUARTERS - 1) umma_commit(b_zfull + 8 * j);
                 }
                 umma_commit(b_ubuf_free);
-                umma_commit(b_tw_empty + 8 * u);
+                if (last_chunk) umma_commit(b_tw_empty + 8 * u);
             }
             __syncwarp();
         };
+        int hb = 0;   // im2col builds consumed (buffer hb & 1)
         for (int gp = pair; gp < ngp; gp += npairs) {
             tr.buf = (P.prof && blockIdx.x == 0 && gp == TRACE_GROUP * npairs) ? P.prof + 4096 : nullptr;
-            // head: D[t] = im2col(q) (128 x 96, fp16) x Wh^T (96 x 64); im2col buffer t & 1
+            // head: D[t] = im2col (128 x HK, fp16) x Wh^T (HK x 64), in G::NBUILD K parts per tile, each part one
+            // im2col build (buffers alternate)
             for (int t = 0; t < T; ++t) {
-                const int ib = t & 1;
                 acquire_acc();
                 if (lane == 0) tr(2, 0, t);
-                mbar_wait(b_i2c_full + 8 * ib, (i2c_ph >> ib) & 1u);
-                if (lane == 0) tr(5, 0, t);
-                i2c_ph ^= 1u << ib;
-                tc_fence_after();
                 const uint32_t d = tmem + COL_ACC + ACC_COLS * vb;
-                if (elect_one()) {
-                    if (t == 0) {
-                        mbar_wait(b_full + 8 * slot0, (ph >> slot0) & 1u);
-                        mbar_wait(b_peerfull + 8 * slot0, (ph >> slot0) & 1u);
-                        tc_fence_after();
-                    }
+#pragma unroll 1
+                for (int kq = 0; kq < G::NBUILD; ++kq) {
+                    const int ib = hb & 1;
+                    mbar_wait(b_i2c_full + 8 * ib, (i2c_ph >> ib) & 1u);
+                    if (lane == 0) tr(5, kq, t);
+                    i2c_ph ^= 1u << ib;
+                    tc_fence_after();
+                    int s = slot0 + (V == 2 ? (kq >> 1) : 0);
+                    s = s >= NUNIT ? s - NUNIT : s;
+                    if (elect_one()) {
+                        if (t == 0 && (V != 2 || (kq & 1) == 0)) {
+                            mbar_wait(b_full + 8 * s, (ph >> s) & 1u);
+                            mbar_wait(b_peerfull + 8 * s, (ph >> s) & 1u);
+                            tc_fence_after();
+                        }
 #pragma unroll
-                    for (int ks = 0; ks < HK / 16; ++ks) {
-                        uint64_t a = make_desc(i2c_base + ib * I2C_BYTES + 2 * ks * (ROWS * 16), ROWS * 16, 128);
-                        uint64_t b = make_desc(ring_base + slot0 * UNIT_BYTES + ks * 1024, 32 * 16, 128);
-                        mma_bf16(d, a, b, idesc_f16(64), ks > 0);
+                        for (int ks = 0; ks < G::I2C_PLANES / 2; ++ks) {
+                            uint64_t a = make_desc(i2c_base + ib * I2C_BYTES + 2 * ks * (ROWS * 16), ROWS * 16, 128);
+                            const int bk = V == 2 ? (kq & 1) * 4 + ks : ks;
+                            uint64_t b = make_desc(ring_base + s * UNIT_BYTES + bk * 1024, 32 * 16, 128);
+                            mma_bf16(d, a, b, idesc_f16(64), (kq | ks) > 0);
+                        }
+                        if (t == T - 1 && (V != 2 || (kq & 1) == 1)) umma_commit(b_empty + 8 * s);
+                        if (kq == G::NBUILD - 1) umma_commit(b_acc_full + 8 * vb);
+                        umma_commit(b_i2c_empty + 8 * ib);
                     }
-                    if (t == T - 1) umma_commit(b_empty + 8 * slot0);
-                    umma_commit(b_acc_full + 8 * vb);
-                    umma_commit(b_i2c_empty + 8 * ib);
+                    __syncwarp();
+                    ++hb;
                 }
-                __syncwarp();
                 vb ^= 1;
                 if (lane == 0) tr(3, 0, t);
             }
-            ph ^= 1u << slot0;
-            slot0 = slot0 == NUNIT - 1 ? 0 : slot0 + 1;
+#pragma unroll
+            for (int h = 0; h < G::HUNITS; ++h) {
+                ph ^= 1u << slot0;
+                slot0 = slot0 == NUNIT - 1 ? 0 : slot0 + 1;
+            }
             auto none = [] {};
 #pragma unroll 1
             for (int L = 0; L < NLAYERS; ++L) conv_layer(L + 1, L & 1, true, none);
             // up quarters (reading buffer NL & 1 = 1); the tail of quarter u issues after tile 0 of up
             // quarter u + 1 (u is drained into U by then), so it completes before that quarter's tiles 1, 2
             // and the drain of u + 1 (which rewrites U) overlaps their MMAs
-            conv_layer(40, 1, true, none);
-            conv_layer(41, 1, false, [&] { tail_mma(0); });
-            conv_layer(42, 1, false, [&] { tail_mma(1); });
-            conv_layer(43, 1, false, [&] { tail_mma(2); });
-            tail_mma(3);
+#pragma unroll 1
+            for (int zc = 0; zc < G::NZC; ++zc) {
+                const bool lc = zc == G::NZC - 1;
+                conv_layer(40, 1, zc == 0, none);
+                conv_layer(41, 1, false, [&] { tail_mma(0, lc); });
+                conv_layer(42, 1, false, [&] { tail_mma(1, lc); });
+                conv_layer(43, 1, false, [&] { tail_mma(2, lc); });
+                tail_mma(3, lc);
+            }
             grp_ph ^= 1u;
         }
     } else {
@@ -711,12 +770,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
         const int cb = 16 * cq;                // first channel of this thread
         const int et = threadIdx.x - 64;       // 0..511
         const int row = 32 * q + lane;         // row within a tile
-        const int pyl = row >> 6, wrow = row_window(row), px = row_px(row);   // tile row = (py - 2 t - 1, window, px)
-        const bool interior = !row_spare(row);
+        const int pyl = row / RPY, wrow = G::window(row), px = G::px(row);   // tile row = (py - TPY t - 1, window, px)
+        const bool interior = !G::spare(row);
         const uint32_t lane_addr = uint32_t(32 * q) << 16;
         uint32_t af_ph = 0;   // bit b: parity of the next completion of b_acc_full[b]
         int vb = 0;           // accumulator buffer of the next unit (the MMA warp's order)
-        int i2c_uses[2] = {0, 0};   // builds into im2col buffer b so far
+        int nbuilt = 0;             // im2col builds so far (buffer nbuilt & 1)
         if (lane == 0)
             for (int b2 = 0; b2 < 2; ++b2) mbar_arrive_leader(b_drained + 8 * b2);   // both buffers start free
         // wait for the next accumulator unit; returns this lane's TMEM address of its buffer
@@ -735,10 +794,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
         // a 3x3 unit: columns n = 96 h + 48 (oc' / 16) + 16 dx + oc' % 16 (h = output-channel half, so a
         // thread's 48 columns are contiguous: one x32 and one x16 load); out[r] = y_0[r - 1] + y_1[r]
         // + y_2[r + 1], the row's px -+ 1 neighbours being lanes -+ 1.  Replicate padding: the pad column
-        // px = 0 equals px = 1, so the y_0 px = 1 needs is its own (and px = 6 takes its own y_2); the pad
+        // px = 0 equals px = 1, so the y_0 px = 1 needs is its own (and px = WS takes its own y_2); the pad
         // columns are therefore never stored.  Spare lanes take their own partials (dead data).  One indexed
         // shuffle per partial.
-        const int src_l = (px == 1 || !interior) ? lane : lane - 1, src_r = (px == 6 || !interior) ? lane : lane + 1;
+        const int src_l = (px == 1 || !interior) ? lane : lane - 1, src_r = (px == G::WS || !interior) ? lane : lane + 1;
         auto load_dx3 = [&](float (&y)[16]) {
             const uint32_t c = acc_wait() + (cq >> 1) * 96 + (cq & 1) * 48;
             uint32_t v01[32], v2[16];
@@ -753,40 +812,76 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
         };
         const float *head_a = cs;
         uint8_t *idx_tab = reinterpret_cast<uint8_t *>(smem + OFF_MISC + IDX_OFF);
-        for (int i = et; i < 64 * HK; i += 32 * NEPI) {   // im2col index table (replicate-clamped 9x9 taps)
-            const int rp = i / HK, k = i - rp * HK;
-            const int cy = min(max((rp >> 3) - 1, 0), 5), cx = min(max((rp & 7) - 1, 0), 5);
-            uint8_t v = 255;
-            if (k < 81) {
-                const int y = min(max(cy + k / 9 - 4, 0), 5), x = min(max(cx + k % 9 - 4, 0), 5);
-                v = uint8_t(y * 6 + x);
+        if constexpr (V != 2) {
+            for (int i = et; i < 64 * 96; i += 32 * NEPI) {   // im2col index table (replicate-clamped 9x9 taps)
+                const int rp = i / 96, k = i - rp * 96;
+                const int cy = min(max((rp >> 3) - 1, 0), 5), cx = min(max((rp & 7) - 1, 0), 5);
+                uint8_t v = 255;
+                if (k < 81) {
+                    const int y = min(max(cy + k / 9 - 4, 0), 5), x = min(max(cx + k % 9 - 4, 0), 5);
+                    v = uint8_t(y * 6 + x);
+                }
+                idx_tab[i] = v;
             }
-            idx_tab[i] = v;
         }
         const float *up_a = cs + 64 + 192 * NL;
         const float *tail_b = up_a + 64;
         Tracer<INSTR> tr{nullptr, 0};
-        uint32_t z_ph = 0;     // parity of the next completion of b_zfull (one per group)
-        // q tables of a group's 8 windows (fp64 normalise -> fp32) -> misc
+        uint32_t z_ph = 0;     // parity of the next completion of b_zfull (one per chunk)
+        // input tables of a group's windows -> misc: V = 0, 1 the 6x6 q values (fp64 normalise -> fp32);
+        // V = 2 the 3 x 12 x 12 X1 values
         auto load_q = [&](int gq) {
-            const long long kq = (long long)(2 * gq + int(rank)) * WPG;
-            if (et < WPG * 36) {
-                const int wk = et / 36, pp = et % 36;
+            const long long kq = (long long)(2 * gq + int(rank)) * GWPG;
+            for (int i = et; i < GWPG * G::QN; i += 32 * NEPI) {
+                const int wk = i / G::QN, pp = i - wk * G::QN;
                 const Win W = window_of(P, kq + wk);
-                misc[et] = __ldg(P.qgrid + (long long)(W.iw + pp / 6) * P.nc + W.jw + pp % 6);
+                if constexpr (V == 2) {
+                    const long long kk = W.valid ? kq + wk : P.nwin - 1;
+                    misc[i] = __half2float(__ushort_as_half(P.x1[kk * 432 + pp]));
+                } else {
+                    misc[i] = __ldg(P.qgrid + (long long)(W.iw + pp / 6) * P.nc + W.jw + pp % 6);
+                }
             }
             epi_bar();
         };
-        // head im2col of tile t from misc (fp16, two buffers: tile t + 1 builds while tile t multiplies)
-        auto build_i2c = [&](int t) {
-            const int ib = t & 1;
-            if (i2c_uses[ib] > 0) mbar_wait(b_i2c_empty + 8 * ib, uint32_t(i2c_uses[ib] - 1) & 1u);
-            ++i2c_uses[ib];
-            {
-                const int r = et & 127, part4 = et >> 7;
-                const int rp = (2 * t + 1 + (r >> 6)) * 8 + row_px(r);   // padded pixel (py, px)
-                const float *qt = misc + row_window(r) * 36;
-                const uint2 *ix = reinterpret_cast<const uint2 *>(idx_tab + rp * HK);
+        // head im2col build b (tile b / NBUILD, K part b % NBUILD) from misc (fp16, two buffers: build b + 1
+        // is written while build b multiplies)
+        auto build_i2c = [&](int b) {
+            const int ib = nbuilt & 1;   // the (nbuilt / 2)-th use of buffer ib: wait for the MMAs of the previous one
+            if (nbuilt >= 2) mbar_wait(b_i2c_empty + 8 * ib, uint32_t((nbuilt >> 1) - 1) & 1u);
+            ++nbuilt;
+            const int t = b / G::NBUILD, kq = b - t * G::NBUILD;
+            const int r = et & 127, part4 = et >> 7;
+            const int py = TPY * t + 1 + (r / RPY);
+            if constexpr (V == 2) {
+                // K = 64 kq + 16 part4 + e: channel c = k / 81, tap (dy, dx), replicate-clamped in the 12x12 window
+                const float *qt = misc + G::window(r) * 432;
+                const int pxr = G::px(r);
+                uint32_t w[8];
+#pragma unroll
+                for (int e2 = 0; e2 < 8; ++e2) {
+                    float v2[2];
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int k = 64 * kq + 16 * part4 + 2 * e2 + h;
+                        float v = 0.f;
+                        if (k < 243) {
+                            const int c = k / 81, tap = k - 81 * c, dy = tap / 9, dx = tap - 9 * dy;
+                            const int y = min(max(py - 1 + dy - 4, 0), 11), x = min(max(pxr - 1 + dx - 4, 0), 11);
+                            v = qt[c * 144 + y * 12 + x];
+                        }
+                        v2[h] = v;
+                    }
+                    w[e2] = pack_op<true>(v2[0], v2[1]);
+                }
+                uint8_t *base = i2c + ib * I2C_BYTES + (2 * part4) * (ROWS * 16) + r * 16;
+                *reinterpret_cast<uint4 *>(base) = make_uint4(w[0], w[1], w[2], w[3]);
+                *reinterpret_cast<uint4 *>(base + ROWS * 16) = make_uint4(w[4], w[5], w[6], w[7]);
+            } else {
+                (void)kq;
+                const int rp = py * 8 + G::px(r);   // padded pixel (py, px)
+                const float *qt = misc + G::window(r) * 36;
+                const uint2 *ix = reinterpret_cast<const uint2 *>(idx_tab + rp * 96);
 #pragma unroll
                 for (int kk = 0; kk < HPLANES / 4; ++kk) {
                     const int kc = part4 * (HPLANES / 4) + kk;
@@ -805,20 +900,22 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
             fence_async_smem();
             epi_bar();
             if (et == 0) mbar_arrive_leader(b_i2c_full + 8 * ib);
-            tr(12, 0, t);
+            tr(12, kq, t);
         };
-        // A group's head im2col tiles are built before the previous group's stitched-pixel epilogue
-        // (activation buffer 1 is free once the last up quarter's MMAs completed), so the head MMAs of
-        // the next group issue right behind the last tail MMAs and overlap that epilogue; tile 2 reuses
-        // im2col buffer 0 once tile 0's head MMAs completed.
+        // Builds made before the previous group's stitched-pixel epilogue (activation buffer 1 is free once
+        // the last up quarter's MMAs completed), so the head MMAs of the next group issue right behind the
+        // last tail MMAs and overlap that epilogue.  V = 0, 1: all three (tile 2 reuses buffer 0 once tile 0's
+        // head MMAs completed); V = 2: the first two of twelve, the rest interleaved with the head epilogues
+        // (a build waits for the MMAs two builds back, which for tile 2 need tile 0's accumulator drained).
+        constexpr int PRE = V == 2 ? 2 : T;
         epi_bar();   // the index table is complete
         if (pair < ngp) {
             load_q(pair);
-            for (int t = 0; t < T; ++t) build_i2c(t);
+            for (int b = 0; b < PRE; ++b) build_i2c(b);
         }
         for (int gp = pair; gp < ngp; gp += npairs) {
             const int g = 2 * gp + int(rank);
-            const long long k0 = (long long)g * WPG;
+            const long long k0 = (long long)g * GWPG;
             tr.buf = (P.prof && blockIdx.x == 0 && gp == TRACE_GROUP * npairs && lane == 0 &&
                       (warp == 2 || warp == 10)) ? P.prof + (warp == 2 ? 2 : 3) * 4096 : nullptr;
             tr(11, 0, 0);
@@ -827,10 +924,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
             for (int L = -1; L < NL; ++L) {
                 uint8_t *obuf = act + ((L + 1) & 1) * ACT_BYTES;
                 for (int t = 0; t < T; ++t) {
+                    if constexpr (V == 2) {
+                        if (L < 0 && t == 0)
+                            for (int b = PRE; b < 8; ++b) build_i2c(b);
+                        if (L < 0 && t == 1)
+                            for (int b = 8; b < 12; ++b) build_i2c(b);
+                    }
                     tr(6, L + 1, t);
                     // this thread's row of the output buffer (for a residual block's second conv it holds the
                     // block input x_k: the fp16 residual stream, updated in place)
-                    uint8_t *dst = obuf + (2 * cq) * ACT_PLANE + (GUARD + (2 * t + 1) * 64 + row) * 16;
+                    uint8_t *dst = obuf + (2 * cq) * ACT_PLANE + (GUARD + (TPY * t + 1) * RPY + row) * 16;
                     float y[16];
                     if (L < 0) {
                         uint32_t v[16];
@@ -888,25 +991,27 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
                     uint32_t pk[8];
 #pragma unroll
                     for (int j = 0; j < 8; ++j) pk[j] = pack_op<F16>(y[2 * j], y[2 * j + 1]);
-                    {   // every lane writes its own row (the pad columns px = 0, 7 are dead data, see load_dx3); the
-                        // first and last image rows (tiles 0 and 2) also write the pad rows py = 0 and 7 (the kernel
-                        // rows dy = 0, 2 read them)
+                    {   // every lane writes its own row (spare rows are dead data, see load_dx3); the first and
+                        // last image rows (tiles 0 and T - 1) also write the pad rows py = 0 and WS + 1 (the
+                        // kernel rows dy = 0, 2 read them)
                         const uint32_t *sv = pk;
                         const uint4 v0 = make_uint4(sv[0], sv[1], sv[2], sv[3]), v1 = make_uint4(sv[4], sv[5], sv[6], sv[7]);
                         *reinterpret_cast<uint4 *>(dst) = v0;
                         *reinterpret_cast<uint4 *>(dst + ACT_PLANE) = v1;
-                        if ((t == 0 && pyl == 0) || (t == T - 1 && pyl == 1)) {
-                            uint8_t *dp = dst + (t == 0 ? -64 : 64) * 16;
+                        if ((t == 0 && pyl == 0) || (t == T - 1 && pyl == TPY - 1)) {
+                            uint8_t *dp = dst + (t == 0 ? -RPY : RPY) * 16;
                             *reinterpret_cast<uint4 *>(dp) = v0;
                             *reinterpret_cast<uint4 *>(dp + ACT_PLANE) = v1;
                         }
                     }
-                    if (INSTR && P.dbg && P.dbg_layer == L + 1 && interior) {
-                        const long long k = k0 + wrow;
-                        if (k < P.nwin) {
-                            const int pp = (2 * t + pyl) * 6 + (px - 1);
+                    if constexpr (INSTR && V == 0) {
+                        if (P.dbg && P.dbg_layer == L + 1 && interior) {
+                            const long long k = k0 + wrow;
+                            if (k < P.nwin) {
+                                const int pp = (2 * t + pyl) * 6 + (px - 1);
 #pragma unroll
-                            for (int j = 0; j < 16; ++j) P.dbg[(k * 36 + pp) * 64 + cb + j] = y[j];
+                                for (int j = 0; j < 16; ++j) P.dbg[(k * 36 + pp) * 64 + cb + j] = y[j];
+                            }
                         }
                     }
                     fence_async_smem();
@@ -916,114 +1021,215 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
                     tr(7, L + 1, t);
                 }
             }
-            // ---- up quarters: every epilogue warp drains 16 columns (4 shuffled channels x 4 sub-pixels) of
-            // its lane quadrant: PReLU, then the quarter goes pixel-shuffled into U, the A operand of the
-            // tail MMAs (edge windows also spill it for k_tail_edge).  U is rewritten for quarter u once the
-            // tail MMAs of quarter u - 1 released it. ----
-            for (int u = 0; u < UP_QUARTERS; ++u) {
-                float ua[4];
+            for (int zc = 0; zc < G::NZC; ++zc) {
+                // ---- up quarters: every epilogue warp drains 16 columns (4 shuffled channels x 4 sub-pixels) of
+                // its lane quadrant: PReLU, then the quarter goes pixel-shuffled into U, the A operand of the
+                // tail MMAs (V = 0, 2: edge windows also spill it for the edge-tail kernel).  U is rewritten
+                // for quarter u once the tail MMAs of quarter u - 1 released it. ----
+                for (int u = 0; u < UP_QUARTERS; ++u) {
+                    float ua[4];
 #pragma unroll
-                for (int m = 0; m < 4; ++m) ua[m] = up_a[UQ * u + 4 * cq + m];
+                    for (int m = 0; m < 4; ++m) ua[m] = up_a[UQ * u + 4 * cq + m];
 #pragma unroll
-                for (int t = 0; t < T; ++t) {
-                    tr(8, u, t);
-                    float a[16];
-                    load_dx3(a);
-                    if (u > 0 && t == 0) mbar_wait(b_ubuf_free, uint32_t(u - 1) & 1u);
-                    tr(9, u, t);
-                    if (interior) {
-                        // column 16 cq + j -> shuffled channel 16 u + 4 cq + j / 4, sub-pixel ((j >> 1) & 1, j & 1)
-                        const int py = 2 * t + 1 + pyl;
-                        float y[16];
-#pragma unroll
-                        for (int j = 0; j < 16; ++j) {
-                            const float x = a[j];
-                            y[j] = x > 0.f ? x : ua[j >> 2] * x;
-                        }
-                        uint8_t *Ub = ubuf + (cq >> 1) * U_PLANE + 8 * (cq & 1);
-#pragma unroll
-                        for (int sub = 0; sub < 4; ++sub) {
-                            const int Y = 2 * (py - 1) + (sub >> 1), X = 2 * (px - 1) + (sub & 1);
-                            *reinterpret_cast<uint2 *>(Ub + (Y * UROWS_Y + 12 * wrow + X) * 16) =
-                                make_uint2(pack_op<F16>(y[sub], y[4 + sub]), pack_op<F16>(y[8 + sub], y[12 + sub]));
-                        }
-                        const long long k = k0 + wrow;
-                        const Win &W = Wd;
-                        const int pp = (py - 1) * 6 + (px - 1);
-                        if (W.valid && W.edge) {
-                            uint32_t pk[8];
-#pragma unroll
-                            for (int j = 0; j < 8; ++j) pk[j] = pack_op<F16>(y[2 * j], y[2 * j + 1]);
-                            uint4 *dst = reinterpret_cast<uint4 *>(
-                                P.edge_u + (size_t(edge_index(W.wi, W.wj, P.npos)) * 36 + pp) * 256 + 64 * u + cb);
-                            dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-                            dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
-                        }
-                        if (INSTR && P.dbg && P.dbg_layer == NL + 1 && W.valid) {
+                    for (int t = 0; t < T; ++t) {
+                        tr(8, u, t);
+                        float a[16];
+                        load_dx3(a);
+                        if (u > 0 && t == 0) mbar_wait(b_ubuf_free, uint32_t(u - 1) & 1u);
+                        tr(9, u, t);
+                        if (interior) {
+                            // column 16 cq + j -> shuffled channel 16 u + 4 cq + j / 4, sub-pixel ((j >> 1) & 1, j & 1)
+                            const int py = TPY * t + 1 + pyl;
+                            float y[16];
 #pragma unroll
                             for (int j = 0; j < 16; ++j) {
-                                const int c = UQ * u + 4 * cq + (j >> 2), Y = 2 * (py - 1) + ((j >> 1) & 1),
-                                          X = 2 * (px - 1) + (j & 1);
-                                P.dbg[(k * 144 + Y * 12 + X) * 64 + c] = y[j];
+                                const float x = a[j];
+                                y[j] = x > 0.f ? x : ua[j >> 2] * x;
+                            }
+                            uint8_t *Ub = ubuf + (cq >> 1) * G::U_PLANE + 8 * (cq & 1);
+#pragma unroll
+                            for (int sub = 0; sub < 4; ++sub) {
+                                const int Y = 2 * (py - 1) + (sub >> 1), X = 2 * (px - 1) + (sub & 1);
+                                const uint2 val = make_uint2(pack_op<F16>(y[sub], y[4 + sub]), pack_op<F16>(y[8 + sub], y[12 + sub]));
+                                if constexpr (V == 0) {
+                                    *reinterpret_cast<uint2 *>(Ub + (Y * G::UROWS_Y + 12 * wrow + X) * 16) = val;
+                                } else if constexpr (V == 1) {
+                                    // chunk rows 4 zc - 4 .. 4 zc + 7, replicate-clamped at the window edge
+                                    const int Yu = Y - 4 * zc + 4;
+                                    if (Yu >= 0 && Yu < 12)
+                                        *reinterpret_cast<uint2 *>(Ub + (Yu * G::UROWS_Y + 12 * wrow + X) * 16) = val;
+                                    if (zc == 0 && Y == 0)
+#pragma unroll
+                                        for (int e = 0; e < 4; ++e)
+                                            *reinterpret_cast<uint2 *>(Ub + (e * G::UROWS_Y + 12 * wrow + X) * 16) = val;
+                                    if (zc == 2 && Y == 11)
+#pragma unroll
+                                        for (int e = 8; e < 12; ++e)
+                                            *reinterpret_cast<uint2 *>(Ub + (e * G::UROWS_Y + 12 * wrow + X) * 16) = val;
+                                } else {
+                                    if (Y >= 4 && Y < 20 && X >= 4 && X < 20)
+                                        *reinterpret_cast<uint2 *>(Ub + ((Y - 4) * G::UROWS_Y + 16 * wrow + X - 4) * 16) = val;
+                                }
+                            }
+                            if constexpr (V != 1) {
+                                const Win &W = Wd;
+                                const int pp = (py - 1) * G::WS + (px - 1);
+                                if (W.valid && W.edge) {
+                                    uint32_t pk[8];
+#pragma unroll
+                                    for (int j = 0; j < 8; ++j) pk[j] = pack_op<F16>(y[2 * j], y[2 * j + 1]);
+                                    uint4 *dst = reinterpret_cast<uint4 *>(
+                                        P.edge_u + (size_t(edge_index(W.wi, W.wj, P.npos)) * (G::WS * G::WS) + pp) * 256 +
+                                        64 * u + cb);
+                                    dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                                    dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+                                }
+                            }
+                            if constexpr (INSTR && V == 0) {
+                                const long long k = k0 + wrow;
+                                if (P.dbg && P.dbg_layer == NL + 1 && Wd.valid) {
+#pragma unroll
+                                    for (int j = 0; j < 16; ++j) {
+                                        const int c = UQ * u + 4 * cq + (j >> 2), Y = 2 * (py - 1) + ((j >> 1) & 1),
+                                                  X = 2 * (px - 1) + (j & 1);
+                                        P.dbg[(k * 144 + Y * 12 + X) * 64 + c] = y[j];
+                                    }
+                                }
+                            }
+                        }
+                        tr(10, u, t);
+                    }
+                    fence_async_smem();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_leader(b_ubuf_full);
+                }
+                // ---- next group's input tables and head im2col (buffer 1: the up MMAs are complete) ----
+                if (zc == G::NZC - 1 && gp + npairs < ngp) {
+                    load_q(gp + npairs);
+                    tr(11, 1, 0);
+                    for (int b = 0; b < PRE; ++b) build_i2c(b);
+                }
+                if constexpr (V == 0) {
+                    // ---- stitched pixels: warps of channel quarter cq = j finish Z tile j (kept fine row y = 4 + j).
+                    // Lane (quadrant q, lane) holds Z row 32 q + lane = 12 w + X; its 27 partials go to shared
+                    // memory (buffer 0: U and the tail weights are consumed once the last Z tile's MMAs completed),
+                    // then the kept pixel (w, X' = 4..7) sums Z[12 w + X' + dx - 4][3 dx + o] over dx, adds the bias,
+                    // applies s tanh(./s), the channel mean and the denormalisation, straight into the fine grid.
+                    // Edge windows are k_tail_edge's. ----
+                    const int j = cq;
+                    mbar_wait(b_zfull + 8 * (G::ZT - 1), z_ph);   // every Z tile done: buffer 0 is free
+                    tr(13, 0, j);
+                    tc_fence_after();
+                    uint32_t z0[16], z1[16];
+                    TMEM_LD16(tmem + lane_addr + COL_Z + 32 * j, z0);
+                    TMEM_LD16(tmem + lane_addr + COL_Z + 32 * j + 16, z1);
+                    tmem_wait_ld();
+                    float *zs = reinterpret_cast<float *>(ubuf) + j * (ROWS * ZS_STRIDE);
+#pragma unroll
+                    for (int n = 0; n < 27; ++n) zs[row * ZS_STRIDE + n] = __uint_as_float(n < 16 ? z0[n] : z1[n - 16]);
+                    asm volatile("bar.sync %0, 128;" ::"r"(2 + j) : "memory");   // the 4 warps of Z tile j
+                    if (row < GWPG * 4) {
+                        const int w = row >> 2, X = 4 + (row & 3);
+                        float pre[3] = {tail_b[0], tail_b[1], tail_b[2]};
+#pragma unroll
+                        for (int dx = 0; dx < 9; ++dx) {
+                            const float *zr = zs + (12 * w + X + dx - 4) * ZS_STRIDE + 3 * dx;
+#pragma unroll
+                            for (int o = 0; o < 3; ++o) pre[o] += zr[o];
+                        }
+                        const Win W = window_of(P, k0 + w);
+                        if (W.valid && !W.edge) {
+                            double m = 0.0;
+#pragma unroll
+                            for (int o = 0; o < 3; ++o) m += double(P.tanh_s * tanhf(pre[o] / P.tanh_s));
+                            m = m / 3.0;
+                            // sign(q) 10^(log_lo + |q| span) in fp32 (exp2f; <= 3e-6 relative, far inside the fp16
+                            // operands' error), off the critical path's fp64 pow
+                            const float e = (float(P.log_lo) + float(fabs(m)) * float(P.span)) * 3.32192809488736f;
+                            const double mag = double(exp2f(e));
+                            P.fine[(long long)(2 * W.iw + 4 + j) * P.nf + 2 * W.jw + X] = m > 0.0 ? mag : (m < 0.0 ? -mag : 0.0);
+                        }
+                    }
+                    tr(14, 0, j);
+                } else if constexpr (V == 1) {
+                    // ---- full output rows 4 zc + j of every window -> X1 (fp16): the dx sum (replicate-clamped at
+                    // the window edge) through shared memory in U, two Z tiles at a time ----
+                    const int j = cq;
+                    mbar_wait(b_zfull + 8 * (G::ZT - 1), z_ph);
+                    tc_fence_after();
+                    uint32_t z0[16], z1[16];
+                    TMEM_LD16(tmem + lane_addr + COL_Z + 32 * j, z0);
+                    TMEM_LD16(tmem + lane_addr + COL_Z + 32 * j + 16, z1);
+                    tmem_wait_ld();
+#pragma unroll 1
+                    for (int h = 0; h < 2; ++h) {
+                        if ((j >> 1) == h) {
+                            float *zs = reinterpret_cast<float *>(ubuf) + (j & 1) * (ROWS * ZS_STRIDE);
+#pragma unroll
+                            for (int n = 0; n < 27; ++n)
+                                zs[row * ZS_STRIDE + n] = __uint_as_float(n < 16 ? z0[n] : z1[n - 16]);
+                            asm volatile("bar.sync %0, 128;" ::"r"(2 + j) : "memory");
+                            if (row < GWPG * 12) {
+                                const int w = row / 12, X = row - 12 * w, Y = 4 * zc + j;
+                                float pre[3] = {tail_b[0], tail_b[1], tail_b[2]};
+#pragma unroll
+                                for (int dx = 0; dx < 9; ++dx) {
+                                    const int xs = min(max(X + dx - 4, 0), 11);
+                                    const float *zr = zs + (12 * w + xs) * ZS_STRIDE + 3 * dx;
+#pragma unroll
+                                    for (int o = 0; o < 3; ++o) pre[o] += zr[o];
+                                }
+                                const long long k = k0 + w;
+                                if (k < P.nwin) {
+#pragma unroll
+                                    for (int o = 0; o < 3; ++o)
+                                        P.x1[(k * 3 + o) * 144 + Y * 12 + X] =
+                                            __half_as_ushort(__float2half_rn(P.tanh_s * tanhf(pre[o] / P.tanh_s)));
+                                }
+                            }
+                        }
+                        epi_bar();   // the scratch half is read before the next half (or the next chunk's U) reuses it
+                    }
+                } else {
+                    // ---- stitched pixels (V = 2): warps of channel quarters 0, 1 finish Z tile j = cq (fine rows
+                    // 8 + 4 j + q).  Lane holds Z row (window lane / 16, X = 4 + lane % 16); the kept X = 8..15 sums
+                    // Z[X + dx - 4][3 dx + o] over dx by lane shuffles. ----
+                    if (cq < G::ZT) {
+                        const int j = cq;
+                        mbar_wait(b_zfull + 8 * j, z_ph);
+                        tc_fence_after();
+                        uint32_t z0[16], z1[16];
+                        TMEM_LD16(tmem + lane_addr + COL_Z + 32 * j, z0);
+                        TMEM_LD16(tmem + lane_addr + COL_Z + 32 * j + 16, z1);
+                        tmem_wait_ld();
+                        const int Xp = lane & 15;
+                        float pre[3] = {tail_b[0], tail_b[1], tail_b[2]};
+#pragma unroll
+                        for (int dx = 0; dx < 9; ++dx) {
+                            const int src = (lane & 16) | ((Xp + dx - 4) & 15);
+#pragma unroll
+                            for (int o = 0; o < 3; ++o) {
+                                const int n = 3 * dx + o;
+                                pre[o] += __shfl_sync(0xffffffffu, __uint_as_float(n < 16 ? z0[n] : z1[n - 16]), src);
+                            }
+                        }
+                        if (Xp >= 4 && Xp < 12) {
+                            const Win W = window_of(P, k0 + (lane >> 4));
+                            if (W.valid && !W.edge) {
+                                double m = 0.0;
+#pragma unroll
+                                for (int o = 0; o < 3; ++o) m += double(P.tanh_s * tanhf(pre[o] / P.tanh_s));
+                                m = m / 3.0;
+                                const float e = (float(P.log_lo) + float(fabs(m)) * float(P.span)) * 3.32192809488736f;
+                                const double mag = double(exp2f(e));
+                                P.fine[(long long)(4 * W.iw + 8 + 4 * j + q) * P.nf + 4 * W.jw + 4 + Xp] =
+                                    m > 0.0 ? mag : (m < 0.0 ? -mag : 0.0);
                             }
                         }
                     }
-                    tr(10, u, t);
                 }
-                fence_async_smem();
-                __syncwarp();
-                if (lane == 0) mbar_arrive_leader(b_ubuf_full);
+                z_ph ^= 1u;
             }
-            // ---- next group's q tables and head im2col (buffer 1: the up MMAs are complete) ----
-            if (gp + npairs < ngp) {
-                load_q(gp + npairs);
-                tr(11, 1, 0);
-                for (int t = 0; t < T; ++t) build_i2c(t);   // tile 2 reuses buffer 0 once head tile 0 multiplied
-            }
-            // ---- stitched pixels: warps of channel quarter cq = j finish Z tile j (kept fine row y = 4 + j).
-            // Lane (quadrant q, lane) holds Z row 32 q + lane = 12 w + X; its 27 partials go to shared memory
-            // (buffer 0: U and the tail weights are consumed once the last Z tile's MMAs completed), then the
-            // kept pixel (w, X' = 4..7) sums Z[12 w + X' + dx - 4][3 dx + o] over dx, adds the bias, applies
-            // s tanh(./s), the channel mean and the denormalisation, straight into the fine grid.  Edge windows
-            // are k_tail_edge's. ----
-            {
-                const int j = cq;
-                mbar_wait(b_zfull + 8 * (ZT - 1), z_ph);   // every Z tile done: buffer 0 is free
-                tr(13, 0, j);
-                tc_fence_after();
-                uint32_t z0[16], z1[16];
-                TMEM_LD16(tmem + lane_addr + COL_Z + 32 * j, z0);
-                TMEM_LD16(tmem + lane_addr + COL_Z + 32 * j + 16, z1);
-                tmem_wait_ld();
-                float *zs = reinterpret_cast<float *>(ubuf) + j * (ROWS * ZS_STRIDE);
-#pragma unroll
-                for (int n = 0; n < 27; ++n) zs[row * ZS_STRIDE + n] = __uint_as_float(n < 16 ? z0[n] : z1[n - 16]);
-                asm volatile("bar.sync %0, 128;" ::"r"(2 + j) : "memory");   // the 4 warps of Z tile j
-                if (row < WPG * 4) {
-                    const int w = row >> 2, X = 4 + (row & 3);
-                    float pre[3] = {tail_b[0], tail_b[1], tail_b[2]};
-#pragma unroll
-                    for (int dx = 0; dx < 9; ++dx) {
-                        const float *zr = zs + (12 * w + X + dx - 4) * ZS_STRIDE + 3 * dx;
-#pragma unroll
-                        for (int o = 0; o < 3; ++o) pre[o] += zr[o];
-                    }
-                    const Win W = window_of(P, k0 + w);
-                    if (W.valid && !W.edge) {
-                        double m = 0.0;
-#pragma unroll
-                        for (int o = 0; o < 3; ++o) m += double(P.tanh_s * tanhf(pre[o] / P.tanh_s));
-                        m = m / 3.0;
-                        // sign(q) 10^(log_lo + |q| span) in fp32 (exp2f; <= 3e-6 relative, far inside the fp16
-                        // operands' error), off the critical path's fp64 pow
-                        const float e = (float(P.log_lo) + float(fabs(m)) * float(P.span)) * 3.32192809488736f;
-                        const double mag = double(exp2f(e));
-                        P.fine[(long long)(2 * W.iw + 4 + j) * P.nf + 2 * W.jw + X] = m > 0.0 ? mag : (m < 0.0 ? -mag : 0.0);
-                    }
-                }
-                tr(14, 0, j);
-            }
-            z_ph ^= 1u;
             tc_fence_before();
             tr(15, 0, 0);
             epi_bar();
@@ -1173,6 +1379,76 @@ __global__ void __launch_bounds__(TE_THREADS) k_tail_edge(Params P, int nedge) {
     }
 }
 
+// Tail of the edge windows of a ratio-4 pass's second application (V = 2), exact fp32 with the reference's
+// replicate clamping on the 24x24 field: one CTA per edge window, one thread per kept fine pixel (the band
+// touching the grid edge: at most 16 x 16), the up-conv output staged 16 channels at a time as replicate-
+// padded [16][32][32] fp32 images, the chunk's tail weights as [16][3][81].
+constexpr int TE4_THREADS = 256, TE4_PAD = 32, TE4_CH = 16;
+constexpr size_t TE4_SMEM = sizeof(float) * (TE4_CH * TE4_PAD * TE4_PAD + TE4_CH * 3 * 81);
+
+template <bool F16>
+__global__ void __launch_bounds__(TE4_THREADS) k_tail_edge4(Params P, int nedge) {
+    extern __shared__ __align__(16) float te4[];
+    float *U = te4, *Wc = te4 + TE4_CH * TE4_PAD * TE4_PAD;
+    const int tid = threadIdx.x;
+    const BlobLayout BL = blob_layout((P.nl - 1) / 2);
+    const float *w = reinterpret_cast<const float *>(P.blob + BL.tail_f32);   // [3][64][81]
+    const float *bias = reinterpret_cast<const float *>(P.blob + BL.consts) + 64 + 192 * P.nl + 64;
+    const int n = P.npos, last = n - 1;
+    for (int e = blockIdx.x; e < nedge; e += gridDim.x) {
+        int wi, wj;
+        if (n == 1) { wi = 0; wj = 0; }
+        else if (e < n) { wi = 0; wj = e; }
+        else if (e < 2 * n) { wi = n - 1; wj = e - n; }
+        else { wi = 1 + (e - 2 * n) / 2; wj = ((e - 2 * n) & 1) ? n - 1 : 0; }
+        const int lo_i = wi == 0 ? 0 : 8, hi_i = wi == last ? 24 : 16, lo_j = wj == 0 ? 0 : 8, hi_j = wj == last ? 24 : 16;
+        const int wk = hi_j - lo_j, npx = (hi_i - lo_i) * wk;
+        const int fy = tid < npx ? lo_i + tid / wk : lo_i, fx = tid < npx ? lo_j + tid % wk : lo_j;
+        float acc[3] = {0.f, 0.f, 0.f};
+        const uint16_t *src = P.edge_u + size_t(e) * 144 * 256;
+#pragma unroll 1
+        for (int c0 = 0; c0 < 64; c0 += TE4_CH) {
+            __syncthreads();   // the previous chunk / window is consumed
+            for (int i = tid; i < TE4_CH * TE4_PAD * TE4_PAD; i += TE4_THREADS) {
+                const int c = i / (TE4_PAD * TE4_PAD), yp = (i / TE4_PAD) % TE4_PAD, xp = i % TE4_PAD;
+                const int Y = min(max(yp - 4, 0), 23), X = min(max(xp - 4, 0), 23);
+                const int oc = 4 * (c0 + c) + 2 * (Y & 1) + (X & 1);
+                U[i] = op_lo<F16>(uint32_t(src[((Y >> 1) * 12 + (X >> 1)) * 256 + oc]));
+            }
+            for (int i = tid; i < TE4_CH * 3 * 81; i += TE4_THREADS) {
+                const int c = i / 243, o = (i / 81) % 3, tap = i % 81;
+                Wc[i] = __ldg(w + (o * 64 + c0 + c) * 81 + tap);
+            }
+            __syncthreads();
+            if (tid < npx) {
+#pragma unroll 1
+                for (int c = 0; c < TE4_CH; ++c)
+#pragma unroll 1
+                    for (int dy = 0; dy < 9; ++dy) {
+                        const float *ur = U + (c * TE4_PAD + fy + dy) * TE4_PAD + fx;
+                        const float *wr = Wc + c * 243 + dy * 9;
+#pragma unroll
+                        for (int dx = 0; dx < 9; ++dx) {
+                            const float u = ur[dx];
+#pragma unroll
+                            for (int o = 0; o < 3; ++o) acc[o] = fmaf(u, wr[o * 81 + dx], acc[o]);
+                        }
+                    }
+            }
+        }
+        if (tid < npx) {
+            double m = 0.0;
+#pragma unroll
+            for (int o = 0; o < 3; ++o) {
+                const float pre = acc[o] + __ldg(bias + o);
+                m += double(P.tanh_s * tanhf(pre / P.tanh_s));
+            }
+            m = m / 3.0;
+            P.fine[(long long)(4 * (2 * wi) + fy) * P.nf + 4 * (2 * wj) + fx] = denormalize_q(m, P.log_lo, P.span);
+        }
+    }
+}
+
 }  // namespace tc
 
 // ---------------------------------------------------------------------------
@@ -1214,6 +1490,22 @@ int tc_pack_weights(mgsr_gen *g, const float *const *t) {
                         v = float(s);
                     }
                     hb[(((oc >> 5) * HPLANES + kc) * 32 + (oc & 31)) * 8 + e] = f2h(v);   // [half][kc][32 oc][8] fp16
+                }
+    }
+    // ratio-4 second-application head (3 distinct input channels): [half][kc 32][32 oc][8] fp16, k = 81 c + tap
+    {
+        uint16_t *hb = reinterpret_cast<uint16_t *>(blob.data() + BL.head4);
+        const float *w = t[0];
+        for (int kc = 0; kc < 32; ++kc)
+            for (int oc = 0; oc < 64; ++oc)
+                for (int e = 0; e < 8; ++e) {
+                    const int k = 8 * kc + e;
+                    float v = 0.f;
+                    if (k < 243) {
+                        const int c = k / 81, tap = k % 81;
+                        v = w[(oc * 3 + c) * 81 + tap];
+                    }
+                    hb[(((oc >> 5) * 32 + kc) * 32 + (oc & 31)) * 8 + e] = f2h(v);
                 }
     }
     auto conv_index = [&](int L) -> int {   // tensor index of body layer L's conv weight
@@ -1307,7 +1599,7 @@ int tc_pack_weights(mgsr_gen *g, const float *const *t) {
     return MGSR_OK;
 }
 
-// workspace: [edge-window up outputs (bf16)][normalised coarse grid q (fp32)]
+// workspace: [edge-window up outputs (fp16)][normalised coarse grid q (fp32)]
 static size_t tc_edge_bytes(int64_t nc) {
     const int npos = int(nc / 2 - 2);
     const size_t b = npos >= 1 ? size_t(tc::edge_count(npos)) * 36 * 256 * sizeof(uint16_t) : 0;
@@ -1315,45 +1607,34 @@ static size_t tc_edge_bytes(int64_t nc) {
 }
 size_t tc_workspace_bytes(int64_t nc) { return tc_edge_bytes(nc) + sizeof(float) * size_t(nc) * nc + 256; }
 
-int launch_sr_pass_tc_dbg(const mgsr_gen *g, const double *c, const double *c_shift, int nc, double log_lo,
-                          double span, double *fine, void *ws, size_t ws_bytes, float *dbg, int dbg_layer,
-                          cudaStream_t st, unsigned long long *prof = nullptr, int f16 = 0) {
+// ratio-4 pass workspace: [edge-window up outputs of the second application (144 px)][X1 (fp16)][q (fp32)]
+static size_t tc4_edge_bytes(int64_t nc) {
+    const int npos = int(nc / 2 - 2);
+    const size_t b = npos >= 1 ? size_t(tc::edge_count(npos)) * 144 * 256 * sizeof(uint16_t) : 0;
+    return (b + 255) & ~size_t(255);
+}
+static size_t tc4_x1_bytes(int64_t nc) {
+    const int64_t npos = nc / 2 - 2;
+    return (size_t(npos > 0 ? npos * npos : 0) * 432 * sizeof(uint16_t) + 255) & ~size_t(255);
+}
+size_t tc4_workspace_bytes(int64_t nc) {
+    return tc4_edge_bytes(nc) + tc4_x1_bytes(nc) + sizeof(float) * size_t(nc) * nc + 256;
+}
+
+// one persistent k_gen_tc<F16, INSTR, V> launch: CTA pairs (clusters of 2), one CTA per SM, as many pairs as
+// can be co-resident
+template <int V>
+static int launch_gen(tc::Params &P, bool f16, bool instr, cudaStream_t st) {
     using namespace tc;
-    if (!g->tc_blob) { set_error("tensor-core weights not packed"); return MGSR_E_UNSUPPORTED; }
-    if (ws_bytes < tc_workspace_bytes(nc)) { set_error("tensor-core workspace too small"); return MGSR_E_WORKSPACE; }
-    Params P{};
-    P.c = c;
-    P.c_shift = c_shift;
-    P.nc = nc;
-    P.npos = nc / 2 - 2;
-    P.nwin = (long long)P.npos * P.npos;
-    P.ngroups = int((P.nwin + WPG - 1) / WPG);
-    P.log_lo = log_lo;
-    P.span = span;
-    P.fine = fine;
-    P.nf = 2 * nc;
-    P.blob = static_cast<const uint8_t *>(g->tc_blob);
-    P.nl = 2 * g->blocks + 1;
-    P.tanh_s = float(g->tanh_scale);
-    P.edge_u = static_cast<uint16_t *>(ws);
-    float *qgrid = reinterpret_cast<float *>(static_cast<char *>(ws) + tc_edge_bytes(nc));
-    P.qgrid = qgrid;
-    P.dbg = dbg;
-    P.dbg_layer = dbg_layer;
-    P.prof = prof;
-    P.wfmt = f16 ? blob_layout(g->blocks).fmt_stride : 0;
     const int smem = smem_bytes(P.nl);
     if (smem > 232448) { set_error("generator too deep for the tensor-core kernel's shared memory"); return MGSR_E_UNSUPPORTED; }
     int dev = 0, nsm = 0;
     MGSR_CUDA_TRY(cudaGetDevice(&dev));
     MGSR_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    const bool instr = dbg != nullptr || prof != nullptr;
-    auto kern = f16 ? (instr ? k_gen_tc<true, true> : k_gen_tc<true, false>)
-                    : (instr ? k_gen_tc<false, true> : k_gen_tc<false, false>);
+    auto kern = f16 ? (instr ? k_gen_tc<true, true, V> : k_gen_tc<true, false, V>)
+                    : (instr ? k_gen_tc<false, true, V> : k_gen_tc<false, false, V>);
     MGSR_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    k_normalize<<<grid_for((long long)nc * nc, 256), 256, 0, st>>>(c, c_shift, nc, log_lo, span, qgrid);
-    MGSR_LAUNCH_CHECK();
-    // CTA pairs (clusters of 2), one CTA per SM, as many pairs as can be co-resident
+    P.ngroups = int((P.nwin + Geo<V>::WPG - 1) / Geo<V>::WPG);
     cudaLaunchConfig_t cfg{};
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -1377,6 +1658,47 @@ int launch_sr_pass_tc_dbg(const mgsr_gen *g, const double *c, const double *c_sh
     const int pairs = ngp < mp ? ngp : mp;
     cfg.gridDim = dim3(2 * pairs);
     MGSR_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, P));
+    return MGSR_OK;
+}
+
+static void fill_params(tc::Params &P, const mgsr_gen *g, const double *c, const double *c_shift, int nc, double log_lo,
+                        double span, double *fine, int ratio, int f16) {
+    using namespace tc;
+    P.c = c;
+    P.c_shift = c_shift;
+    P.nc = nc;
+    P.npos = nc / 2 - 2;
+    P.nwin = (long long)P.npos * P.npos;
+    P.log_lo = log_lo;
+    P.span = span;
+    P.fine = fine;
+    P.nf = ratio * nc;
+    P.blob = static_cast<const uint8_t *>(g->tc_blob);
+    P.nl = 2 * g->blocks + 1;
+    P.tanh_s = float(g->tanh_scale);
+    P.wfmt = f16 ? blob_layout(g->blocks).fmt_stride : 0;
+}
+
+int launch_sr_pass_tc_dbg(const mgsr_gen *g, const double *c, const double *c_shift, int nc, double log_lo,
+                          double span, double *fine, void *ws, size_t ws_bytes, float *dbg, int dbg_layer,
+                          cudaStream_t st, unsigned long long *prof = nullptr, int f16 = 0) {
+    using namespace tc;
+    if (!g->tc_blob) { set_error("tensor-core weights not packed"); return MGSR_E_UNSUPPORTED; }
+    if (ws_bytes < tc_workspace_bytes(nc)) { set_error("tensor-core workspace too small"); return MGSR_E_WORKSPACE; }
+    Params P{};
+    fill_params(P, g, c, c_shift, nc, log_lo, span, fine, 2, f16);
+    P.edge_u = static_cast<uint16_t *>(ws);
+    float *qgrid = reinterpret_cast<float *>(static_cast<char *>(ws) + tc_edge_bytes(nc));
+    P.qgrid = qgrid;
+    P.dbg = dbg;
+    P.dbg_layer = dbg_layer;
+    P.prof = prof;
+    int nsm = 0, dev = 0;
+    MGSR_CUDA_TRY(cudaGetDevice(&dev));
+    MGSR_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    k_normalize<<<grid_for((long long)nc * nc, 256), 256, 0, st>>>(c, c_shift, nc, log_lo, span, qgrid);
+    MGSR_LAUNCH_CHECK();
+    if (int r = launch_gen<0>(P, f16 != 0, dbg != nullptr || prof != nullptr, st)) return r;
     {
         const int ne = edge_count(P.npos);
         // per current device (function attributes are per device), like k_gen_tc's above
@@ -1393,6 +1715,40 @@ int launch_sr_pass_tc_dbg(const mgsr_gen *g, const double *c, const double *c_sh
 int launch_sr_pass_tc(const mgsr_gen *g, const double *c, const double *c_shift, int nc, double log_lo, double span,
                       double *fine, void *ws, size_t ws_bytes, cudaStream_t st, int f16) {
     return launch_sr_pass_tc_dbg(g, c, c_shift, nc, log_lo, span, fine, ws, ws_bytes, nullptr, -1, st, nullptr, f16);
+}
+
+// A ratio-4 windowed pass (two generator applications, srmodel.py:443-463 with applications = 2) on the tensor
+// cores: normalise -> k_gen_tc<V = 1> (6x6 windows -> full 12x12x3 X1) -> k_gen_tc<V = 2> (X1 -> kept 8x8
+// fine pixels of interior windows) -> k_tail_edge4 (edge windows' kept bands, exact fp32 tail).
+int launch_sr_pass4_tc(const mgsr_gen *g, const double *c, const double *c_shift, int nc, double log_lo, double span,
+                       double *fine, void *ws, size_t ws_bytes, cudaStream_t st, int f16) {
+    using namespace tc;
+    if (!g->tc_blob) { set_error("tensor-core weights not packed"); return MGSR_E_UNSUPPORTED; }
+    if (ws_bytes < tc4_workspace_bytes(nc)) { set_error("tensor-core workspace too small"); return MGSR_E_WORKSPACE; }
+    Params P{};
+    fill_params(P, g, c, c_shift, nc, log_lo, span, fine, 4, f16);
+    char *w = static_cast<char *>(ws);
+    P.edge_u = reinterpret_cast<uint16_t *>(w);
+    P.x1 = reinterpret_cast<uint16_t *>(w + tc4_edge_bytes(nc));
+    float *qgrid = reinterpret_cast<float *>(w + tc4_edge_bytes(nc) + tc4_x1_bytes(nc));
+    P.qgrid = qgrid;
+    int nsm = 0, dev = 0;
+    MGSR_CUDA_TRY(cudaGetDevice(&dev));
+    MGSR_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    k_normalize<<<grid_for((long long)nc * nc, 256), 256, 0, st>>>(c, c_shift, nc, log_lo, span, qgrid);
+    MGSR_LAUNCH_CHECK();
+    if (int r = launch_gen<1>(P, f16 != 0, false, st)) return r;
+    if (int r = launch_gen<2>(P, f16 != 0, false, st)) return r;
+    {
+        const int ne = edge_count(P.npos);
+        MGSR_CUDA_TRY(cudaFuncSetAttribute(f16 ? k_tail_edge4<true> : k_tail_edge4<false>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, int(TE4_SMEM)));
+        const int nb = ne < 4 * nsm ? ne : 4 * nsm;
+        if (f16) k_tail_edge4<true><<<nb, TE4_THREADS, TE4_SMEM, st>>>(P, ne);
+        else k_tail_edge4<false><<<nb, TE4_THREADS, TE4_SMEM, st>>>(P, ne);
+    }
+    MGSR_LAUNCH_CHECK();
+    return MGSR_OK;
 }
 
 }  // namespace mgsr

@@ -186,12 +186,63 @@ def test_tc_deterministic(cuda):
     assert np.array_equal(a, b)
 
 
-def test_tc_rejects_multi_pass_ratio(cuda):
+@pytest.mark.parametrize("weights", ["trained_b8", "trained_b4", "he_b1"])
+@pytest.mark.parametrize("nc", [12, 40])
+def test_tc_ratio4_pass_vs_oracle(cuda, orc, weights, nc):
+    """A ratio-4 SR pass on the tensor cores (first application on 6x6 windows with the full 12x12x3
+    output, second on 12x12 windows of 3 distinct channels, kept 8x8 fine pixels; srmodel.py:443-487)
+    against the fp64 CPU oracle, full field, at the north-star 1e-2 relL2 bar.  nc = 12 is the paper
+    ladder's 12 -> 48 first pass (16 windows, 12 of them edge windows).  Measured 1.7e-3 .. 4.3e-3
+    (tests/precision_r4.py; the oracle with fp16-rounded conv operands lands within 10% of the same)."""
     from paper_2403_07936_b200 import srmodel
     from paper_2403_07936_b200.grid import Grid, NormBounds
-    w = _trained(4)
-    with pytest.raises(ValueError, match="ratio-2"):
-        srmodel.sr_prolong(Grid(np.ones((16, 16)) * 1e-5), w, NormBounds(), 4, precision="fp16")
+    w = {"trained_b8": lambda: _trained(8), "trained_b4": lambda: _trained(4),
+         "he_b1": lambda: srmodel.random_weights(1, 3)}[weights]()
+    c = _fields(max(nc, 16))["smooth"][:nc, :nc]
+    c = c - c.mean()
+    exp = orc.sr_prolong(c, orc.quantize_f32(_oracle_weights(orc, w)), orc.Bounds(), 4)
+    got = srmodel.sr_prolong(Grid(c), w, NormBounds(), 4, precision="fp16").data
+    assert got.shape == exp.shape
+    assert rel_l2(got, exp) < 1e-2, rel_l2(got, exp)
+
+
+@pytest.mark.parametrize("s,nc", [(8, 16), (16, 12)])
+def test_tc_two_pass_ratios_per_pass_vs_oracle(cuda, orc, s, nc):
+    """Ratios 8 (x4 then x2) and 16 (x4 then x4) on the tensor cores: the composed prolongation equals
+    the two passes run one after the other through the public API (bitwise), and each pass matches the
+    fp64 oracle's pass on the same input at the 1e-2 bar.  The end-to-end fp16 error of the composition
+    is the reference algorithm's own sensitivity to operand rounding (the second pass re-normalises the
+    first pass's output logarithmically): the oracle run with fp16-rounded conv operands shows 7e-3 ..
+    6e-2 on these fields (tests/precision_r4.py), so the composition is
+    pinned per pass, not end to end."""
+    from paper_2403_07936_b200 import srmodel
+    from paper_2403_07936_b200.grid import Grid, NormBounds
+    w = _trained(8)
+    ow = orc.quantize_f32(_oracle_weights(orc, w))
+    c = _fields(16)["smooth"][:nc, :nc]
+    c = c - c.mean()
+    full = srmodel.sr_prolong(Grid(c), w, NormBounds(), s, precision="fp16").data
+    mid = srmodel.sr_prolong(Grid(c), w, NormBounds(), 4, precision="fp16").data
+    last = srmodel.sr_prolong(Grid(mid), w, NormBounds(), s // 4, precision="fp16").data
+    assert np.allclose(full, last, rtol=1e-12, atol=0.0), float(np.abs(full - last).max())
+    e1 = rel_l2(mid, orc.sr_prolong(c, ow, orc.Bounds(), 4))
+    e2 = rel_l2(last, orc.sr_prolong(mid, ow, orc.Bounds(), s // 4))
+    assert e1 < 1e-2 and e2 < 1e-2, (e1, e2)
+
+
+def test_tc_ratio4_pass_vs_fp32_generator_larger(cuda):
+    """A ratio-4 pass at n_c = 128 (3844 windows: many groups per CTA pair, interior and edge windows):
+    fp16 tensor cores against the fp32 CUDA-core generator (itself pinned to the oracle by
+    test_sr_prolong_fp32_golden) at the 1e-2 bar, and bitwise repeatable."""
+    from paper_2403_07936_b200 import srmodel
+    from paper_2403_07936_b200.grid import Grid, NormBounds
+    w = _trained(8)
+    c = _fields(128)["smooth"]
+    ref = srmodel.sr_prolong(Grid(c), w, NormBounds(), 4, precision="fp32").data
+    got = srmodel.sr_prolong(Grid(c), w, NormBounds(), 4, precision="fp16").data
+    assert rel_l2(got, ref) < 1e-2, rel_l2(got, ref)
+    again = srmodel.sr_prolong(Grid(c), w, NormBounds(), 4, precision="fp16").data
+    assert np.array_equal(got, again)
 
 
 @pytest.mark.parametrize("weights", ["trained", "he_init"])
