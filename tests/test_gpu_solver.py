@@ -361,3 +361,27 @@ def test_config3_hybrid_1024_matches_reference_fixture(cuda, orc, golden_dir, pr
     assert relh.max() < bar
     sub = p.data[::16, ::16]
     assert rel_l2(sub, fx["p_sub"]) < 1e-8
+
+
+@pytest.mark.parametrize("precision,bar", [("fp32", 1e-4), ("fp16", 1e-2)])
+def test_default_config_sr_vcycle_vs_oracle(cuda, orc, precision, bar):
+    """The reference's default RunConfig (N_step=4, r_min=12, N_smooth=20) with SR prolongation at
+    192^2: ladder [192, 12], one ratio-16 SR prolongation (two ratio-4 passes) of the 12^2 correction,
+    on the tensor cores for fp16.  One V-cycle against the CPU oracle (trained B=8 weights)."""
+    import os
+    from paper_2403_07936_b200 import datagen, solver, srmodel
+    from paper_2403_07936_b200.grid import Grid
+    from paper_2403_07936_b200.smoother import PoissonProblem
+    from conftest import ROOT
+    w = srmodel.load_weights(os.path.join(ROOT, "artifacts", "trained_b8.mgsr"))
+    n = 192
+    f = datagen.scale_to_p_rms(datagen.grf_blobs_rhs(n, seed=2, kmax=24.0), 1e-4)
+    p = orc.initial_iterate(n, orc.Config()) * 0.1
+    ocfg = orc.Config(N_step=4, r_min=12, N_smooth=20)
+    ow = orc.Weights({k: v for k, v in w.tensors.items()}, w.num_residual_blocks, w.tanh_scale)
+    exp = orc.v_cycle(p, f, ocfg, "sr", orc.quantize_f32(ow))
+    cfg = cfg_(N_step=4, r_min=12, N_smooth=20)
+    got = solver.v_cycle(Grid(p), PoissonProblem(Grid(f)), cfg, "sr", w, precision=precision).data
+    err = rel_l2(got - got.mean(), exp - exp.mean())
+    print(f"default-config SR V-cycle {precision}: relL2 {err:.3e}")
+    assert err < bar, err
