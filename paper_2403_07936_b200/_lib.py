@@ -28,6 +28,16 @@ MGSR_OK = 0
 MGSR_E_CUDA = -8
 PREC = {"fp32": 0, "bf16": 1, "fp16": 2}
 
+
+def precision(p: str | None) -> str:
+    """Generator precision of an operator call: an explicit argument wins, else ``MGSR_PRECISION``
+    (default "fp16": the tcgen05 tensor-core generator; "fp32" is the exact CUDA-core mode)."""
+    import os
+    p = p if p is not None else os.environ.get("MGSR_PRECISION", "fp16")
+    if p not in PREC:
+        raise ValueError(f"precision must be one of {sorted(PREC)}, got {p!r}")
+    return p
+
 _lock = threading.Lock()
 _lib = None
 

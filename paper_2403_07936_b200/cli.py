@@ -268,8 +268,9 @@ def cmd_datagen(a) -> int:
 
 
 def _common_solver_flags(sp):
-    sp.add_argument("--precision", choices=PRECISIONS, default="fp32",
-                    help="generator path for SR prolongations (fp32 CUDA cores, or tcgen05 fp16/bf16 operands)")
+    sp.add_argument("--precision", choices=PRECISIONS, default=None,
+                    help="generator path for SR prolongations (default MGSR_PRECISION or fp16: tcgen05 tensor cores; "
+                         "fp32: the exact CUDA-core mode)")
     sp.add_argument("--sr-levels", type=int, default=None,
                     help="SR only at the N finest prolongations (spline below); default: every level")
 

@@ -4,10 +4,13 @@ Mirrors ``mgsr.srmodel`` (srmodel.py:25-487).  Weights are host tensors in
 the MGSR1 format (same names, shapes, validation and typed errors); inference
 runs on the GPU:
 
-* ``precision="fp32"`` -- CUDA-core fp32 generator (reference precision, any
-  window side; used for the x4/x8/x16 passes too);
-* ``precision="bf16"`` -- the tcgen05 tensor-core megakernel (bf16 operands,
-  fp32 accumulation in TMEM), ratio-2 passes on 6x6 windows.
+* ``precision="fp16"`` (the default; ``MGSR_PRECISION`` overrides it) -- the tcgen05 tensor-core
+  megakernel (fp16 operands, fp32 accumulation in TMEM): ratio-2 passes on 6x6 windows and
+  ratio-4 passes (x4, x8 = x4 + x2, x16 = x4 + x4) as two applications (full 12x12x3 first
+  output, 12x12 windows of 3 channels second);
+* ``precision="bf16"`` -- the same kernels with bf16 operands;
+* ``precision="fp32"`` -- CUDA-core fp32 generator (the exact mode: <= 1e-5 of the reference's
+  fp64; any window side).
 """
 
 from __future__ import annotations
@@ -287,8 +290,9 @@ def stitch_plan(n_coarse: int) -> list[tuple[int, int, slice, slice]]:
 _PASS_PLAN = {2: (1,), 4: (2,), 8: (2, 1), 16: (2, 2)}
 
 
-def sr_prolong(coarse: Grid, w: GeneratorWeights, b: NormBounds, s: int, precision: str = "fp32") -> Grid:
+def sr_prolong(coarse: Grid, w: GeneratorWeights, b: NormBounds, s: int, precision: str | None = None) -> Grid:
     """SR prolongation by s in {2, 4, 8, 16} (srmodel.py:470-487), on the GPU."""
+    precision = _lib.precision(precision)
     if s not in _PASS_PLAN:
         raise ValueError(f"unsupported SR ratio {s}; expected one of {sorted(_PASS_PLAN)}")
     window_positions(coarse.n)

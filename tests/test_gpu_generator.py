@@ -37,11 +37,11 @@ def test_sr_prolong_fp32_golden(cuda, golden):
     from paper_2403_07936_b200 import srmodel
     from paper_2403_07936_b200.grid import Grid, NormBounds
     w2 = srmodel.random_weights(2, 0)
-    out = srmodel.sr_prolong(Grid(golden["sr_c16"]), w2, NormBounds(), 2)
+    out = srmodel.sr_prolong(Grid(golden["sr_c16"]), w2, NormBounds(), 2, precision="fp32")
     assert rel_l2(out.data, golden["sr2_out"]) < 1e-4
-    out = srmodel.sr_prolong(Grid(golden["sr_c12"]), w2, NormBounds(), 4)
+    out = srmodel.sr_prolong(Grid(golden["sr_c12"]), w2, NormBounds(), 4, precision="fp32")
     assert rel_l2(out.data, golden["sr4_out"]) < 1e-4
-    out = srmodel.sr_prolong(Grid(golden["sr_c16"]), srmodel.make_nearest_neighbor_weights(), NormBounds(), 2)
+    out = srmodel.sr_prolong(Grid(golden["sr_c16"]), srmodel.make_nearest_neighbor_weights(), NormBounds(), 2, precision="fp32")
     assert rel(out.data, golden["srnn2_out"]) < 1e-5
 
 
@@ -53,7 +53,7 @@ def test_sr_prolong_two_pass_ratios(cuda, orc, s):
     c = orc.scale_to_p_rms(orc.sine_modes_rhs(12, 4), 1e-4)[:12, :12]
     c = c - c.mean()
     w = srmodel.random_weights(1, 2)
-    got = srmodel.sr_prolong(Grid(c), w, NormBounds(), s).data
+    got = srmodel.sr_prolong(Grid(c), w, NormBounds(), s, precision="fp32").data
     exp = orc.sr_prolong(c, orc.random_weights(1, 2), orc.Bounds(), s)
     assert rel_l2(got, exp) < 1e-3
 
@@ -64,7 +64,7 @@ def test_sr_prolong_fp32_vs_oracle_256(cuda, orc):
     from paper_2403_07936_b200.grid import Grid, NormBounds
     c = orc.scale_to_p_rms(orc.sine_modes_rhs(128, 5), 1e-4)
     w = srmodel.random_weights(8, 0)
-    got = srmodel.sr_prolong(Grid(c), w, NormBounds(), 2).data
+    got = srmodel.sr_prolong(Grid(c), w, NormBounds(), 2, precision="fp32").data
     exp = orc.sr_prolong(c, orc.quantize_f32(orc.random_weights(8, 0)), orc.Bounds(), 2)
     assert rel_l2(got, exp) < 1e-3
 

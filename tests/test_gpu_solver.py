@@ -98,7 +98,7 @@ def test_solve_hybrid_schedule_golden(cuda, golden, golden_meta):
     from paper_2403_07936_b200.grid import Grid
     from paper_2403_07936_b200.smoother import PoissonProblem
     cfg = cfg_(mode="hybrid", N_GAN=1.0, S_thres=2.27e-4)
-    p, log = solver.solve(PoissonProblem(Grid(golden["hyb64_f"])), cfg, srmodel.random_weights(1, 0))
+    p, log = solver.solve(PoissonProblem(Grid(golden["hyb64_f"])), cfg, srmodel.random_weights(1, 0), precision="fp32")
     assert [r.operator for r in log.records] == golden_meta["hyb64_ops"]
     assert [r.switch_latched for r in log.records] == golden_meta["hyb64_latched"]
     got = np.array([[r.diff_norm, r.residual_norm] for r in log.records])
@@ -110,7 +110,7 @@ def test_v_cycle_sr_golden(cuda, golden):
     from paper_2403_07936_b200.grid import Grid
     from paper_2403_07936_b200.smoother import PoissonProblem
     out = solver.v_cycle(Grid(golden["vc_sr_p"]), PoissonProblem(Grid(golden["vc_sr_f"])), cfg_(N_smooth_pre=2),
-                         "sr", srmodel.random_weights(2, 0))
+                         "sr", srmodel.random_weights(2, 0), precision="fp32")
     assert rel_l2(out.data, golden["vc_sr_out"]) < 1e-4
 
 
@@ -175,8 +175,8 @@ def test_resident_solve_matches_host_loop(cuda, orc, mode, n):
     w = srmodel.load_weights(os.path.join(ROOT, "artifacts", "trained_b8.mgsr")) if mode == "hybrid" else None
     f = orc.scale_to_p_rms(orc.sine_modes_rhs(n, 0), 1e-4)
     cfg = cfg_(mode=mode, N_GAN=1.0, S_thres=5e-4)
-    p_a, la = solver.solve(PoissonProblem(Grid(f)), cfg, w, resident=True)
-    p_b, lb = solver.solve(PoissonProblem(Grid(f)), cfg, w, resident=False)
+    p_a, la = solver.solve(PoissonProblem(Grid(f)), cfg, w, resident=True, precision="fp32")
+    p_b, lb = solver.solve(PoissonProblem(Grid(f)), cfg, w, resident=False, precision="fp32")
     assert la.iterations == lb.iterations
     assert [r.operator for r in la.records] == [r.operator for r in lb.records]
     assert [r.switch_latched for r in la.records] == [r.switch_latched for r in lb.records]
@@ -196,9 +196,9 @@ def test_solve_batch_matches_single_solves(cuda, orc):
     w = srmodel.load_weights(os.path.join(ROOT, "artifacts", "trained_b8.mgsr"))
     fs = [orc.scale_to_p_rms(orc.sine_modes_rhs(128, s), 1e-4) for s in range(3)]
     cfg = cfg_(mode="hybrid", N_GAN=1.0, S_thres=5e-4)
-    batch = solver.solve_batch([PoissonProblem(Grid(f)) for f in fs], cfg, w)
+    batch = solver.solve_batch([PoissonProblem(Grid(f)) for f in fs], cfg, w, precision="fp32")
     for f, (pb, lb) in zip(fs, batch):
-        ps, ls = solver.solve(PoissonProblem(Grid(f)), cfg, w)
+        ps, ls = solver.solve(PoissonProblem(Grid(f)), cfg, w, precision="fp32")
         assert lb.iterations == ls.iterations and lb.converged(1e-10)
         assert [r.operator for r in lb.records] == [r.operator for r in ls.records]
         assert np.array_equal(pb.data, ps.data)
