@@ -157,6 +157,20 @@ int mgsr_plan_solve(mgsr_plan *plan, double *p, const double *f, int32_t mode, i
                     double s_thres, int32_t cadence, int32_t first_sr, int32_t ngan_one,
                     double *records_dev, int32_t *iterations_dev, void *stream);
 
+/* Batched device-resident solves (BASELINE config 5; the reference fans independent
+ * solves out over processes, cli.py:202-250): B plans of one configuration and
+ * generator (plans[b] with its iterate p[b] and RHS f[b]) run their solve loops in
+ * lockstep inside ONE graph launch, each with its own operator schedule, latch and
+ * stopping rule, and every SR level's generator runs as ONE persistent launch over
+ * the windows of all grids that prolong by SR in that iteration.  Each grid sees
+ * its mgsr_plan_solve kernel sequence, so p[b] and its records are bitwise those
+ * of mgsr_plan_solve.  records_dev: B x n_iter x 4 doubles; iterations_dev: B
+ * int32.  1 <= B <= 1024. */
+int mgsr_plan_solve_batch(mgsr_plan *const *plans, int32_t B, double *const *p, const double *const *f,
+                          int32_t mode, int32_t n_iter, double tol, double s_thres, int32_t cadence,
+                          int32_t first_sr, int32_t ngan_one, double *records_dev, int32_t *iterations_dev,
+                          void *stream);
+
 /* Instrumentation for bench.py.  mgsr_plan_timing_enable(plan, k): the next k
  * V-cycle launches record CUDA events (event-record nodes inside the graph,
  * re-targeted per launch) around (0) the finest-level generator kernel,

@@ -73,6 +73,7 @@ SIGNATURES = {
     "mgsr_plan_levels": (i32, [vp, ctypes.POINTER(i64)]),
     "mgsr_plan_vcycle": (ctypes.c_int, [vp, vp, vp, i32, vp, vp]),
     "mgsr_plan_solve": (ctypes.c_int, [vp, vp, vp, i32, i32, f64, f64, i32, i32, i32, vp, vp, vp]),
+    "mgsr_plan_solve_batch": (ctypes.c_int, [vp, i32, vp, vp, i32, i32, f64, f64, i32, i32, i32, vp, vp, vp]),
     "mgsr_plan_timing_enable": (ctypes.c_int, [vp, i32]),
     "mgsr_plan_timing_read": (ctypes.c_int, [vp, c_double_p, ctypes.POINTER(i32)]),
     "mgsr_plan_kernel_nodes": (i32, [vp, i32]),

@@ -42,6 +42,11 @@ size_t tc_workspace_bytes(int64_t nc);
 size_t tc4_workspace_bytes(int64_t nc);
 int launch_sr_pass_tc(const mgsr_gen *g, const double *c, const double *c_shift, int nc, double log_lo,
                       double span, double *fine, void *ws, size_t ws_bytes, cudaStream_t st, int f16);
+size_t tc_batch_workspace_bytes(int64_t nc, int B);
+int launch_sr_pass_tc_batch(const mgsr_gen *g, const double *const *cs, int B, const int *list, const int *count,
+                            int nc, double log_lo, double span, double *fine_base, void *ws, size_t ws_bytes,
+                            cudaStream_t st, int f16);
+int launch_mean_f64(const double *a, int64_t count, void *red_slot, double *result, cudaStream_t st);
 int launch_sr_pass4_tc(const mgsr_gen *g, const double *c, const double *c_shift, int nc, double log_lo,
                        double span, double *fine, void *ws, size_t ws_bytes, cudaStream_t st, int f16);
 

@@ -386,6 +386,12 @@ __global__ void k_mean_f64(const double *__restrict__ a, int64_t count, RedSlot 
     grid_reduce<1>(v, slot, result, 1.0 / double(count));
 }
 
+int launch_mean_f64(const double *a, int64_t count, void *red_slot, double *result, cudaStream_t st) {
+    k_mean_f64<<<grid_for(count, 256), 256, 0, st>>>(a, count, red_slot_at(red_slot), result);
+    MGSR_LAUNCH_CHECK();
+    return MGSR_OK;
+}
+
 __global__ void k_f64_to_f32(const double *__restrict__ a, float *__restrict__ b, int64_t count) {
     for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < count;
          t += int64_t(gridDim.x) * blockDim.x)

@@ -397,6 +397,12 @@ struct Params {
     int dbg_layer;
     unsigned long long *prof;   // optional event trace (bring-up instrumentation, tests/tc_trace.py)
     uint16_t *x1;               // ratio-4 passes: [nwin][3][12][12] fp16 first-application output (V = 1 -> V = 2)
+    // batched ratio-2 passes (V = 0, mgsr_plan_solve_batch): the windows of the *rhs_count grids listed in
+    // rhs_list, nwin1 windows each; grid r's q at qgrid + r q_stride, its output at fine + r fine_stride, its
+    // edge spill at edge_u + r edge_count(npos) windows.  rhs_list == nullptr: one grid.
+    const int *rhs_list;
+    const int *rhs_count;
+    long long nwin1, q_stride, fine_stride;
 };
 
 // Event trace of one steady-state group of CTA 0: role r (0 producer, 1 MMA, 2 epilogue warp 2,
@@ -417,13 +423,20 @@ struct Tracer {
 
 // window geometry of a global window index (srmodel.py:414-440)
 struct Win {
-    int iw, jw, wi, wj;
+    int iw, jw, wi, wj, rhs;
     bool valid, edge;
 };
-__device__ __forceinline__ Win window_of(const Params &P, long long k) {
+__device__ __forceinline__ Win window_of(const Params &P, long long k, long long nwin) {
     Win w;
-    w.valid = k < P.nwin;
-    const int kk = int(w.valid ? k : P.nwin - 1);
+    w.valid = k < nwin;
+    long long kg = w.valid ? k : nwin - 1;
+    w.rhs = 0;
+    if (P.rhs_list) {
+        const long long slot = kg / P.nwin1;
+        w.rhs = P.rhs_list[slot];
+        kg -= slot * P.nwin1;
+    }
+    const int kk = int(kg);
     w.wi = kk / P.npos;
     w.wj = kk - w.wi * P.npos;
     w.iw = 2 * w.wi;
@@ -488,7 +501,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
     const uint32_t rank = cluster_rank();
     const bool leader = rank == 0;
     const int pair = int(blockIdx.x >> 1), npairs = int(gridDim.x >> 1);
-    const int ngp = (P.ngroups + 1) >> 1;   // the pair processes groups 2 gp (leader) and 2 gp + 1 (peer)
+    long long nwin = P.nwin;   // batched passes: the device-side count of grids in this launch
+    int ngroups = P.ngroups;
+    if (P.rhs_count) {
+        nwin = (long long)(*P.rhs_count) * P.nwin1;
+        ngroups = int((nwin + GWPG - 1) / GWPG);
+    }
+    const int ngp = (ngroups + 1) >> 1;   // the pair processes groups 2 gp (leader) and 2 gp + 1 (peer)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int NL = P.nl, NLAYERS = P.nl;
@@ -841,12 +860,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
             const long long kq = (long long)(2 * gq + int(rank)) * GWPG;
             for (int i = et; i < GWPG * G::QN; i += 32 * NEPI) {
                 const int wk = i / G::QN, pp = i - wk * G::QN;
-                const Win W = window_of(P, kq + wk);
+                const Win W = window_of(P, kq + wk, nwin);
                 if constexpr (V == 2) {
-                    const long long kk = W.valid ? kq + wk : P.nwin - 1;
+                    const long long kk = W.valid ? kq + wk : nwin - 1;
                     misc[i] = __half2float(__ushort_as_half(P.x1[kk * 432 + pp]));
                 } else {
-                    misc[i] = __ldg(P.qgrid + (long long)(W.iw + pp / 6) * P.nc + W.jw + pp % 6);
+                    misc[i] = __ldg(P.qgrid + W.rhs * P.q_stride + (long long)(W.iw + pp / 6) * P.nc + W.jw + pp % 6);
                 }
             }
             epi_bar();
@@ -926,7 +945,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
             tr.buf = (P.prof && blockIdx.x == 0 && gp == TRACE_GROUP * npairs && lane == 0 &&
                       (warp == 2 || warp == 10)) ? P.prof + (warp == 2 ? 2 : 3) * 4096 : nullptr;
             tr(11, 0, 0);
-            const Win Wd = window_of(P, k0 + wrow);   // this thread's window in the up drains
+            const Win Wd = window_of(P, k0 + wrow, nwin);   // this thread's window in the up drains
             // ---- head + body + post epilogues: layer L (head = -1) writes buffer (L + 1) & 1 ----
             for (int L = -1; L < NL; ++L) {
                 uint8_t *obuf = act + ((L + 1) & 1) * ACT_BYTES;
@@ -1014,7 +1033,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
                     if constexpr (INSTR && V == 0) {
                         if (P.dbg && P.dbg_layer == L + 1 && interior) {
                             const long long k = k0 + wrow;
-                            if (k < P.nwin) {
+                            if (k < nwin) {
                                 const int pp = (2 * t + pyl) * 6 + (px - 1);
 #pragma unroll
                                 for (int j = 0; j < 16; ++j) P.dbg[(k * 36 + pp) * 64 + cb + j] = y[j];
@@ -1085,7 +1104,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
                                 const int pp = (py - 1) * G::WS + (px - 1);
                                 if (W.valid && W.edge) {   // spill in the up conv's channel order (edge-tail kernels)
                                     uint32_t *dst = reinterpret_cast<uint32_t *>(
-                                        P.edge_u + (size_t(edge_index(W.wi, W.wj, P.npos)) * (G::WS * G::WS) + pp) * 256 +
+                                        P.edge_u + (size_t(W.rhs) * edge_count(P.npos) + edge_index(W.wi, W.wj, P.npos)) * (G::WS * G::WS) * 256 + pp * 256 +
                                         64 * u + 32 * (cq >> 1) + 2 * ii);
 #pragma unroll
                                     for (int m = 0; m < 8; ++m) dst[2 * m] = pack_op<F16>(y[2 * m], y[2 * m + 1]);
@@ -1142,7 +1161,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
 #pragma unroll
                             for (int o = 0; o < 3; ++o) pre[o] += zr[o];
                         }
-                        const Win W = window_of(P, k0 + w);
+                        const Win W = window_of(P, k0 + w, nwin);
                         if (W.valid && !W.edge) {
                             double m = 0.0;
 #pragma unroll
@@ -1152,7 +1171,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
                             // operands' error), off the critical path's fp64 pow
                             const float e = (float(P.log_lo) + float(fabs(m)) * float(P.span)) * 3.32192809488736f;
                             const double mag = double(exp2f(e));
-                            P.fine[(long long)(2 * W.iw + 4 + j) * P.nf + 2 * W.jw + X] = m > 0.0 ? mag : (m < 0.0 ? -mag : 0.0);
+                            P.fine[W.rhs * P.fine_stride + (long long)(2 * W.iw + 4 + j) * P.nf + 2 * W.jw + X] = m > 0.0 ? mag : (m < 0.0 ? -mag : 0.0);
                         }
                     }
                     tr(14, 0, j);
@@ -1185,7 +1204,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
                                     for (int o = 0; o < 3; ++o) pre[o] += zr[o];
                                 }
                                 const long long k = k0 + w;
-                                if (k < P.nwin) {
+                                if (k < nwin) {
 #pragma unroll
                                     for (int o = 0; o < 3; ++o)
                                         P.x1[(k * 3 + o) * 144 + Y * 12 + X] =
@@ -1219,7 +1238,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
                             }
                         }
                         if (Xp >= 4 && Xp < 12) {
-                            const Win W = window_of(P, k0 + (lane >> 4));
+                            const Win W = window_of(P, k0 + (lane >> 4), nwin);
                             if (W.valid && !W.edge) {
                                 double m = 0.0;
 #pragma unroll
@@ -1258,6 +1277,16 @@ __global__ void k_normalize(const double *__restrict__ c, const double *shift, i
         q[i] = float(normalize_q(c[i] - sh, log_lo, span));
 }
 
+// batched normalise: grids cs[0..B) (device pointer array) -> q[r][nc][nc]
+__global__ void k_normalize_batch(const double *const *cs, int B, int nc, double log_lo, double span,
+                                  float *__restrict__ q) {
+    const long long per = (long long)nc * nc, total = per * B;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+        const long long r = i / per;
+        q[i] = float(normalize_q(cs[r][i - r * per], log_lo, span));
+    }
+}
+
 // Tail of the edge windows (kept band touching the grid edge), exact fp32 with
 // the reference's replicate clamping (srmodel.py:285-289) on the 12x12 field.
 // Register-blocked and persistent: the fp32 tail weights are staged once per CTA as [c][dy][o][dx (12)], each
@@ -1285,14 +1314,18 @@ __global__ void __launch_bounds__(TE_THREADS) k_tail_edge(Params P, int nedge) {
     }
     const int g = tid >> 3, slot = tid & 7;   // channels 2g, 2g + 1; strip slot
     const int n = P.npos, last = n - 1;
-    for (int e = blockIdx.x; e < nedge; e += gridDim.x) {
+    const int ne1 = edge_count(n);
+    if (P.rhs_count) nedge = *P.rhs_count * ne1;   // batched: the listed grids' edge windows
+    for (int eg = blockIdx.x; eg < nedge; eg += gridDim.x) {
+        const int gs = eg / ne1, e = eg - gs * ne1, rhs = P.rhs_list ? P.rhs_list[gs] : 0;
+        double *fine = P.fine + rhs * P.fine_stride;
         int wi, wj;
         if (n == 1) { wi = 0; wj = 0; }
         else if (e < n) { wi = 0; wj = e; }
         else if (e < 2 * n) { wi = n - 1; wj = e - n; }
         else { wi = 1 + (e - 2 * n) / 2; wj = ((e - 2 * n) & 1) ? n - 1 : 0; }
         __syncthreads();   // previous window's U / partials consumed (and the weights staged)
-        const uint16_t *src = P.edge_u + size_t(e) * 36 * 256;
+        const uint16_t *src = P.edge_u + (size_t(rhs) * ne1 + e) * 36 * 256;
         for (int i = tid; i < 36 * 256; i += TE_THREADS) {
             const int pp = i >> 8, oc = i & 255, c = oc >> 2, ii = (oc >> 1) & 1, jj = oc & 1;
             const int Y = 2 * (pp / 6) + ii, X = 2 * (pp % 6) + jj;
@@ -1376,7 +1409,7 @@ __global__ void __launch_bounds__(TE_THREADS) k_tail_edge(Params P, int nedge) {
                         m += double(P.tanh_s * tanhf(pre / P.tanh_s));
                     }
                     m = m / 3.0;
-                    P.fine[(long long)(2 * (2 * wi) + fy) * P.nf + 2 * (2 * wj) + fx] = denormalize_q(m, P.log_lo, P.span);
+                    fine[(long long)(2 * (2 * wi) + fy) * P.nf + 2 * (2 * wj) + fx] = denormalize_q(m, P.log_lo, P.span);
                 }
             }
             __syncthreads();
@@ -1722,6 +1755,47 @@ int launch_sr_pass_tc_dbg(const mgsr_gen *g, const double *c, const double *c_sh
 int launch_sr_pass_tc(const mgsr_gen *g, const double *c, const double *c_shift, int nc, double log_lo, double span,
                       double *fine, void *ws, size_t ws_bytes, cudaStream_t st, int f16) {
     return launch_sr_pass_tc_dbg(g, c, c_shift, nc, log_lo, span, fine, ws, ws_bytes, nullptr, -1, st, nullptr, f16);
+}
+
+// Batched ratio-2 passes (config 5, mgsr_plan_solve_batch): the windows of the *count grids listed in `list`
+// (device-side, written by the solve loop's controller) in ONE persistent k_gen_tc launch and one edge-tail
+// launch; grid r's coarse correction is cs[r] (device pointer array), its output fine_base + r nf^2.  Each
+// window's arithmetic is the single-grid launch's, so the outputs are bitwise those of launch_sr_pass_tc.
+size_t tc_batch_workspace_bytes(int64_t nc, int B) {
+    return size_t(B) * tc_edge_bytes(nc) + sizeof(float) * size_t(B) * nc * nc + 256;
+}
+int launch_sr_pass_tc_batch(const mgsr_gen *g, const double *const *cs, int B, const int *list, const int *count,
+                            int nc, double log_lo, double span, double *fine_base, void *ws, size_t ws_bytes,
+                            cudaStream_t st, int f16) {
+    using namespace tc;
+    if (!g->tc_blob) { set_error("tensor-core weights not packed"); return MGSR_E_UNSUPPORTED; }
+    if (ws_bytes < tc_batch_workspace_bytes(nc, B)) { set_error("tensor-core workspace too small"); return MGSR_E_WORKSPACE; }
+    Params P{};
+    fill_params(P, g, nullptr, nullptr, nc, log_lo, span, fine_base, 2, f16);
+    P.nwin1 = P.nwin;
+    P.nwin = P.nwin1 * B;   // the launch's capacity; the kernels read *count
+    P.rhs_list = list;
+    P.rhs_count = count;
+    P.q_stride = (long long)nc * nc;
+    P.fine_stride = 4LL * nc * nc;
+    char *w = static_cast<char *>(ws);
+    P.edge_u = reinterpret_cast<uint16_t *>(w);
+    float *qgrid = reinterpret_cast<float *>(w + size_t(B) * tc_edge_bytes(nc));
+    P.qgrid = qgrid;
+    int nsm = 0, dev = 0;
+    MGSR_CUDA_TRY(cudaGetDevice(&dev));
+    MGSR_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    k_normalize_batch<<<grid_for((long long)B * nc * nc, 256), 256, 0, st>>>(cs, B, nc, log_lo, span, qgrid);
+    MGSR_LAUNCH_CHECK();
+    if (int r = launch_gen<0>(P, f16 != 0, false, st)) return r;
+    const int ne = edge_count(P.npos) * B;
+    MGSR_CUDA_TRY(cudaFuncSetAttribute(f16 ? k_tail_edge<true> : k_tail_edge<false>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, int(TE_SMEM)));
+    const int nb = ne < nsm ? ne : nsm;
+    if (f16) k_tail_edge<true><<<nb, TE_THREADS, TE_SMEM, st>>>(P, ne);
+    else k_tail_edge<false><<<nb, TE_THREADS, TE_SMEM, st>>>(P, ne);
+    MGSR_LAUNCH_CHECK();
+    return MGSR_OK;
 }
 
 // A ratio-4 windowed pass (two generator applications, srmodel.py:443-463 with applications = 2) on the tensor

@@ -12,6 +12,8 @@
 
 #include <cmath>
 #include <cstdlib>
+#include <algorithm>
+#include <functional>
 #include <map>
 #include <string>
 #include <tuple>
@@ -135,8 +137,9 @@ int prolong_into(mgsr_plan *pl, int l, int use_sr, const double *base, const dou
     return launch_add2(base, bshift, pl->srbuf, sr_mean(pl, l), out, nf * nf, mean_out, slot(pl, 3), st);
 }
 
-// correction(rhs_l, l) of solver.py:181-190; leaves the gauge-fixed result in d[l].
-int correction(mgsr_plan *pl, int l, int use_sr, cudaStream_t st) {
+// correction(rhs_l, l) of solver.py:181-190; leaves the gauge-fixed result in d[l].  stop > 0 (batched
+// solves): the prolongations from levels <= stop are left to the caller (prolong_level, level-major).
+int correction(mgsr_plan *pl, int l, int use_sr, cudaStream_t st, int stop = 0) {
     const int L = int(pl->sides.size());
     const int n = pl->sides[l];
     const double h = 2.0 * M_PI / n;
@@ -167,7 +170,8 @@ int correction(mgsr_plan *pl, int l, int use_sr, cudaStream_t st) {
     if (r) return r;
     if (!fuse_rc && (r = launch_res_restrict(pl->d[l], fs, n, s, pl->rc[l + 1], rc_mean(pl, l + 1), slot(pl, 1), st)))
         return r;
-    if ((r = correction(pl, l + 1, use_sr, st))) return r;
+    if ((r = correction(pl, l + 1, use_sr, st, stop))) return r;
+    if (l + 1 <= stop) return MGSR_OK;
     // d[l] = (d[l] - d_mean) + up  (in place: elementwise)
     const double *bshift = n <= kSmallN ? nullptr : d_mean(pl, l);
     return prolong_into(pl, l + 1, use_sr, pl->d[l], bshift, pl->d[l], nullptr, st);
@@ -206,6 +210,49 @@ int record_vcycle(mgsr_plan *pl, double *p, const double *f, int use_sr, cudaStr
     if (r) return r;
     if (mk) MGSR_CUDA_TRY(cudaEventRecordWithFlags(pl->cap_ev[5], st, cudaEventRecordExternal));
     return MGSR_OK;
+}
+
+// The batched solve's pieces of record_vcycle (same kernels, same order per grid): everything before the
+// prolongation from level `stop` (record_down), one prolongation (prolong_level / sr_add_level), the
+// logging pass (record_finalize).
+int prolong_level(mgsr_plan *pl, int l, int use_sr, cudaStream_t st) {
+    if (l == 1) {
+        const double *bshift = pl->sides[0] <= kSmallN ? nullptr : sc(pl, SC_S_MEAN);
+        return prolong_into(pl, 1, use_sr, pl->S, bshift, pl->S, sc(pl, SC_OUT_MEAN), st);
+    }
+    const double *bshift = pl->sides[l - 1] <= kSmallN ? nullptr : d_mean(pl, l - 1);
+    return prolong_into(pl, l, use_sr, pl->d[l - 1], bshift, pl->d[l - 1], nullptr, st);
+}
+
+int record_down(mgsr_plan *pl, double *p, const double *f, int use_sr, cudaStream_t st, int stop) {
+    const int n = pl->sides[0];
+    const double h = 2.0 * M_PI / n;
+    const int s0 = n / pl->sides[1];
+    FSrc fs{f, nullptr, 1.0};
+    int r = launch_gs(p, pl->S, pl->tmp, fs, n, h * h, pl->cfg.n_smooth, 0, s0 == 2 ? pl->rc[1] : nullptr,
+                      s0 == 2 ? rc_mean(pl, 1) : nullptr, sc(pl, SC_S_MEAN), pl->red, st);
+    if (r) return r;
+    if (s0 != 2 && (r = launch_res_restrict(pl->S, fs, n, s0, pl->rc[1], rc_mean(pl, 1), slot(pl, 1), st))) return r;
+    if ((r = correction(pl, 1, use_sr, st, stop))) return r;
+    return stop == 0 ? prolong_level(pl, 1, use_sr, st) : MGSR_OK;
+}
+
+// the SR branch of prolong_into after the (batched) generator wrote this grid's raw output to srbuf
+int sr_add_level(mgsr_plan *pl, int l, const double *srbuf, cudaStream_t st) {
+    const int64_t nf = pl->sides[l - 1];
+    int r = launch_mean_f64(srbuf, nf * nf, slot(pl, 2), sr_mean(pl, l), st);
+    if (r) return r;
+    double *base = l == 1 ? pl->S : pl->d[l - 1];
+    const double *bshift = l == 1 ? (pl->sides[0] <= kSmallN ? nullptr : sc(pl, SC_S_MEAN))
+                                  : (pl->sides[l - 1] <= kSmallN ? nullptr : d_mean(pl, l - 1));
+    return launch_add2(base, bshift, srbuf, sr_mean(pl, l), base, nf * nf, l == 1 ? sc(pl, SC_OUT_MEAN) : nullptr,
+                       slot(pl, 3), st);
+}
+
+int record_finalize(mgsr_plan *pl, double *p, const double *f, cudaStream_t st) {
+    FSrc fs{f, nullptr, 1.0};
+    return launch_finalize(pl->S, sc(pl, SC_OUT_MEAN), p, fs, pl->sides[0], sc(pl, SC_ACC), sc(pl, SC_STATS),
+                           slot(pl, 0), st);
 }
 
 }  // namespace
@@ -274,8 +321,11 @@ extern "C" int mgsr_plan_create(const mgsr_plan_config *cfg, const mgsr_gen *gen
     return MGSR_OK;
 }
 
+void batch_forget(const mgsr_plan *pl);
+
 extern "C" int mgsr_plan_destroy(mgsr_plan *pl) {
     if (!pl) return MGSR_OK;
+    batch_forget(pl);   // batched solve graphs that captured this plan's buffers
     for (auto &kv : pl->graphs) {
         cudaGraphExecDestroy(kv.second.exec);
         cudaGraphDestroy(kv.second.graph);
@@ -602,4 +652,371 @@ extern "C" int mgsr_plan_solve(mgsr_plan *pl, double *p, const double *f, int32_
                                   cudaMemcpyDeviceToDevice, st));
     MGSR_CUDA_TRY(cudaMemcpyAsync(iterations_dev, pl->solve_state + 3, sizeof(int), cudaMemcpyDeviceToDevice, st));
     return MGSR_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Batched device-resident solves (BASELINE config 5: independent right-hand sides of one size solved
+// concurrently with batch-N generator inference).  B plans of one configuration run their solve loops
+// in lockstep inside ONE graph launch: a WHILE node whose body is
+//   k_batch_pre   -> per grid: operator of its own iteration (its own N_GAN cadence and latch), the
+//                    IF handles (active / spline this iteration / SR this iteration) and the device list
+//                    of the grids that prolong by SR;
+//   per grid, in parallel branches: IF(active) the cycle down to the SR levels (record_down);
+//   per SR level, finest last: IF(spline) that grid's spline prolongation, and ONE batched generator
+//                    launch over the listed grids' windows followed by IF(SR) that grid's mean + add;
+//   per grid: IF(active) the logging pass;
+//   k_batch_post  -> per grid: record, latch, deactivate on tol / N_iter; loop while any grid is active.
+// Every grid sees exactly its single-solve kernel sequence, so results are bitwise those of
+// mgsr_plan_solve on each grid.
+
+namespace {
+
+__global__ void k_batch_init(int *state, int *active, int B) {
+    const int r = threadIdx.x;
+    if (r < B) {
+        state[4 * r] = state[4 * r + 1] = state[4 * r + 2] = state[4 * r + 3] = 0;
+        active[r] = 1;
+    }
+}
+
+// handles: [kind 3][grid B][nh] -- every IF node owns its handle; kind 0 = active, 1 = spline this
+// iteration, 2 = SR this iteration
+__global__ void k_batch_pre(int *state, const int *active, int B, int mode, int cadence, int first_sr, int ngan_one,
+                            const cudaGraphConditionalHandle *hdl, int nh, int n0, int n1, int n2, int *list,
+                            int *count) {
+    __shared__ int flag[1024];
+    const int r = threadIdx.x;
+    int act = 0, sr = 0;
+    if (r < B) {
+        int *st = state + 4 * r;
+        act = active[r];
+        if (act) {   // k_solve_pre's schedule (solver.py:122-144)
+            const int it = st[0] + 1, latched = st[1];
+            if (mode == 0) sr = 0;
+            else if (mode == 1) sr = 1;
+            else if (latched) sr = !first_sr;
+            else if (ngan_one) sr = it & 1;
+            else sr = (it % cadence != 0) ? first_sr : !first_sr;
+            st[2] = sr;
+        }
+        const unsigned v[3] = {act ? 1u : 0u, (act && !sr) ? 1u : 0u, (act && sr) ? 1u : 0u};
+        const int used[3] = {n0, n1, n2};   // IF nodes of each kind per grid
+        for (int k = 0; k < 3; ++k)
+            for (int j = 0; j < used[k]; ++j) cudaGraphSetConditional(hdl[(size_t(k) * B + r) * nh + j], v[k]);
+    }
+    flag[r] = act && sr;
+    __syncthreads();
+    if (r == 0) {
+        int c = 0;
+        for (int k = 0; k < B; ++k)
+            if (flag[k]) list[c++] = k;
+        *count = c;
+    }
+}
+
+__global__ void k_batch_post(int *state, int *active, int B, const double *const *stats, double *rec, int n_iter,
+                             double tol, double s_thres, cudaGraphConditionalHandle h_while) {
+    const int r = threadIdx.x;
+    int more = 0;
+    if (r < B && active[r]) {   // k_solve_post per grid
+        int *st = state + 4 * r;
+        const int it = st[0] + 1;
+        const double d = stats[r][0];
+        double *rr = rec + (size_t(r) * n_iter + (it - 1)) * 4;
+        rr[0] = d;
+        rr[1] = stats[r][1];
+        rr[2] = double(st[2]);
+        rr[3] = double(st[1]);
+        if (!st[1] && d <= s_thres) st[1] = 1;
+        st[0] = it;
+        st[3] = it;
+        more = (!(d < tol) && it < n_iter) ? 1 : 0;
+        active[r] = more;
+    }
+    more = __syncthreads_or(more);
+    if (r == 0) cudaGraphSetConditional(h_while, more ? 1u : 0u);
+}
+
+struct BatchGraph {
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    void *mem = nullptr;   // device: state, active, records, list, count, handles, pointer arrays, SR buffers
+    int *state = nullptr, *active = nullptr, *list = nullptr, *count = nullptr;
+    double *rec = nullptr;
+    int n_iter = 0;
+    cudaStream_t cap = nullptr;
+};
+using BatchKey = std::tuple<std::vector<const void *>, int, int, double, double, int, int, int>;
+std::map<BatchKey, BatchGraph> g_batches;
+
+void batch_free(BatchGraph &G) {
+    if (G.exec) cudaGraphExecDestroy(G.exec);
+    if (G.graph) cudaGraphDestroy(G.graph);
+    if (G.mem) cudaFree(G.mem);
+    if (G.cap) cudaStreamDestroy(G.cap);
+    G = BatchGraph{};
+}
+
+int capture_into(cudaGraph_t body, cudaStream_t cap, const std::function<int(cudaStream_t)> &fn) {
+    MGSR_CUDA_TRY(cudaStreamBeginCaptureToGraph(cap, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+    int r = fn(cap);
+    cudaGraph_t out = nullptr;
+    cudaError_t e = cudaStreamEndCapture(cap, &out);
+    if (r) return r;
+    if (e != cudaSuccess) { set_error(std::string("batch capture: ") + cudaGetErrorString(e)); return MGSR_E_CUDA; }
+    return MGSR_OK;
+}
+
+int build_batch(BatchGraph &G, mgsr_plan *const *pls, int B, double *const *p, const double *const *f, int mode,
+                int n_iter, double tol, double s_thres, int cadence, int first_sr, int ngan_one) {
+    mgsr_plan *p0 = pls[0];
+    const int L = int(p0->sides.size());
+    const bool tc = tensor_core_precision(p0->cfg.precision) && p0->gen && p0->gen->tc_blob;
+    // the SR prolongations: from level l into l - 1 where the mask bit l - 1 is set (and the grid allows SR)
+    std::vector<int> sr_lev(L, 0);
+    int stop = 0;
+    if (mode != 0 && p0->gen)
+        for (int l = 1; l < L; ++l) {
+            const int nc = p0->sides[l];
+            if (((p0->cfg.sr_level_mask >> (l - 1)) & 1u) && nc >= 6 && nc % 2 == 0) {
+                sr_lev[l] = 1;
+                stop = std::max(stop, l);
+            }
+        }
+    // device memory
+    size_t off = 0;
+    auto take = [&](size_t bytes) { size_t o = off; off = (off + bytes + 255) & ~size_t(255); return o; };
+    const size_t o_state = take(sizeof(int) * 4 * B), o_active = take(sizeof(int) * B), o_list = take(sizeof(int) * B),
+                 o_count = take(sizeof(int)), o_rec = take(sizeof(double) * 4 * size_t(B) * n_iter),
+                 o_h = take(sizeof(cudaGraphConditionalHandle) * 3 * B * (L + 2)), o_stats = take(sizeof(double *) * B),
+                 o_cs = take(sizeof(double *) * B * L);
+    size_t o_srbuf = 0, o_srws = 0, srws_bytes = 0;
+    int64_t nf_max = 0;
+    for (int l = 1; l < L; ++l)
+        if (sr_lev[l] && tc && p0->sides[l - 1] == 2 * p0->sides[l]) {
+            nf_max = std::max<int64_t>(nf_max, p0->sides[l - 1]);
+            if (tc_batch_workspace_bytes(p0->sides[l], B) > srws_bytes) {
+                srws_bytes = tc_batch_workspace_bytes(p0->sides[l], B);
+            }
+        }
+    if (nf_max) {
+        o_srbuf = take(sizeof(double) * size_t(B) * nf_max * nf_max);
+        o_srws = take(srws_bytes);
+    }
+    MGSR_CUDA_TRY(cudaMalloc(&G.mem, off));
+    char *m = static_cast<char *>(G.mem);
+    G.state = reinterpret_cast<int *>(m + o_state);
+    G.active = reinterpret_cast<int *>(m + o_active);
+    G.list = reinterpret_cast<int *>(m + o_list);
+    G.count = reinterpret_cast<int *>(m + o_count);
+    G.rec = reinterpret_cast<double *>(m + o_rec);
+    G.n_iter = n_iter;
+    auto *hdev = reinterpret_cast<cudaGraphConditionalHandle *>(m + o_h);
+    auto *stats_dev = reinterpret_cast<const double **>(m + o_stats);
+    auto *cs_dev = reinterpret_cast<const double **>(m + o_cs);
+    double *srbuf = nf_max ? reinterpret_cast<double *>(m + o_srbuf) : nullptr;
+    void *srws = nf_max ? m + o_srws : nullptr;
+    MGSR_CUDA_TRY(cudaStreamCreateWithFlags(&G.cap, cudaStreamNonBlocking));
+
+    cudaGraph_t g = nullptr;
+    MGSR_CUDA_TRY(cudaGraphCreate(&g, 0));
+    G.graph = g;
+    cudaGraphConditionalHandle hw;
+    MGSR_CUDA_TRY(cudaGraphConditionalHandleCreate(&hw, g, 1, cudaGraphCondAssignDefault));
+    // every IF node owns a handle: [kind][grid][j], j < nh = L + 2 (kinds: 0 active, 1 spline, 2 SR)
+    const int nh = L + 2;
+    std::vector<cudaGraphConditionalHandle> hh(size_t(3) * B * nh, 0);
+    std::vector<int> hused(3 * B, 0);
+    auto new_handle = [&](int kind, int b, cudaGraphConditionalHandle *out) -> int {
+        int &u = hused[kind * B + b];
+        if (u >= nh) { set_error("batch: too many conditional nodes"); return MGSR_E_UNSUPPORTED; }
+        MGSR_CUDA_TRY(cudaGraphConditionalHandleCreate(out, g, 0, cudaGraphCondAssignDefault));
+        hh[(size_t(kind) * B + b) * nh + u++] = *out;
+        return MGSR_OK;
+    };
+    std::vector<const double *> stats_h(B), cs_h(size_t(B) * L, nullptr);
+    for (int b = 0; b < B; ++b) {
+        stats_h[b] = sc(pls[b], SC_STATS);
+        for (int l = 1; l < L; ++l) cs_h[size_t(l) * B + b] = pls[b]->d[l];
+    }
+    MGSR_CUDA_TRY(cudaMemcpy(stats_dev, stats_h.data(), sizeof(double *) * B, cudaMemcpyHostToDevice));
+    MGSR_CUDA_TRY(cudaMemcpy(cs_dev, cs_h.data(), sizeof(double *) * B * L, cudaMemcpyHostToDevice));
+
+    cudaGraphNode_t n_init, n_while, n_pre, n_post;
+    int *state = G.state, *active = G.active, *list = G.list, *count = G.count;
+    double *rec = G.rec;
+    int B_ = B, mode_ = mode, cad = cadence, fs_ = first_sr, g1 = ngan_one, nit = n_iter;
+    double tol_ = tol, sth = s_thres;
+    void *a_init[] = {&state, &active, &B_};
+    cudaKernelNodeParams kpi{};
+    kpi.func = reinterpret_cast<void *>(k_batch_init);
+    kpi.gridDim = dim3(1);
+    kpi.blockDim = dim3(1024);
+    kpi.kernelParams = a_init;
+    int r = MGSR_OK;
+    MGSR_CUDA_TRY(cudaGraphAddKernelNode(&n_init, g, nullptr, 0, &kpi));
+    cudaGraph_t body = nullptr;
+    if (!r) r = add_if(g, &n_while, &n_init, hw, cudaGraphCondTypeWhile, &body);
+    const cudaGraphConditionalHandle *hdl = hdev;
+    int nh_ = nh, nu[3] = {0, 0, 0};   // the per-kind counts are filled in once the body is built
+    void *a_pre[] = {&state, &active, &B_, &mode_, &cad, &fs_, &g1, &hdl, &nh_, &nu[0], &nu[1], &nu[2], &list, &count};
+    cudaKernelNodeParams kp{};
+    kp.func = reinterpret_cast<void *>(k_batch_pre);
+    kp.gridDim = dim3(1);
+    kp.blockDim = dim3(1024);
+    kp.kernelParams = a_pre;
+    if (!r) MGSR_CUDA_TRY(cudaGraphAddKernelNode(&n_pre, body, nullptr, 0, &kp));
+    cudaKernelNodeParams kp_pre = kp;
+    cudaGraphNode_t join = n_pre;
+    // one IF node per grid after `join`, each capturing fn(b, stream); returns the join of them all (plus extra)
+    auto per_grid = [&](int kind, const std::function<int(int, cudaStream_t)> &fn,
+                        std::vector<cudaGraphNode_t> extra) -> int {
+        std::vector<cudaGraphNode_t> ends = std::move(extra);
+        for (int b = 0; b < B; ++b) {
+            cudaGraphNode_t nd;
+            cudaGraph_t bd = nullptr;
+            cudaGraphConditionalHandle h;
+            if (int e = new_handle(kind, b, &h)) return e;
+            if (int e = add_if(body, &nd, &join, h, cudaGraphCondTypeIf, &bd)) return e;
+            if (int e = capture_into(bd, G.cap, [&](cudaStream_t cs) { return fn(b, cs); })) return e;
+            ends.push_back(nd);
+        }
+        cudaGraphNode_t j;
+        MGSR_CUDA_TRY(cudaGraphAddEmptyNode(&j, body, ends.data(), ends.size()));
+        join = j;
+        return MGSR_OK;
+    };
+    // spline iterations: the whole cycle (its small-grid fusions included) up to the logging pass; SR iterations:
+    // the cycle down to the finest SR level, then level-major below
+    {
+        std::vector<cudaGraphNode_t> sp;
+        const cudaGraphNode_t j0 = join;
+        for (int b = 0; b < B && !r; ++b) {
+            cudaGraphNode_t nd;
+            cudaGraph_t bd = nullptr;
+            cudaGraphConditionalHandle h;
+            r = new_handle(1, b, &h);
+            if (!r) r = add_if(body, &nd, &j0, h, cudaGraphCondTypeIf, &bd);
+            if (!r) r = capture_into(bd, G.cap, [&](cudaStream_t cs) { return record_down(pls[b], p[b], f[b], 0, cs, 0); });
+            sp.push_back(nd);
+        }
+        if (!r) r = per_grid(2, [&](int b, cudaStream_t cs) { return record_down(pls[b], p[b], f[b], 1, cs, stop); }, sp);
+    }
+    for (int l = stop; !r && l >= 1; --l) {
+        const bool batched = sr_lev[l] && tc && p0->sides[l - 1] == 2 * p0->sides[l];
+        if (!batched) {   // spline level between SR levels, fp32 generator, or a multi-pass ratio: per grid
+            r = per_grid(2, [&](int b, cudaStream_t cs) { return prolong_level(pls[b], l, 1, cs); }, {});
+            continue;
+        }
+        // one generator launch over the SR grids' windows -> srbuf + b nf^2, then per grid mean + add
+        const int nc = p0->sides[l];
+        const double log_lo = std::log10(p0->cfg.p_min), span = std::log10(p0->cfg.p_max) - log_lo;
+        cudaGraph_t sg = nullptr;
+        MGSR_CUDA_TRY(cudaGraphCreate(&sg, 0));
+        const double *const *csl = cs_dev + size_t(l) * B;
+        r = capture_into(sg, G.cap, [&](cudaStream_t cs) {
+            return launch_sr_pass_tc_batch(p0->gen, csl, B, list, count, nc, log_lo, span, srbuf, srws, srws_bytes, cs,
+                                           p0->cfg.precision == MGSR_PREC_FP16);
+        });
+        cudaGraphNode_t n_sr;
+        if (!r) MGSR_CUDA_TRY(cudaGraphAddChildGraphNode(&n_sr, body, &join, 1, sg));
+        cudaGraphDestroy(sg);
+        if (r) break;
+        const int64_t nf = 2LL * nc;
+        join = n_sr;
+        r = per_grid(2, [&](int b, cudaStream_t cs) { return sr_add_level(pls[b], l, srbuf + size_t(b) * nf * nf, cs); }, {});
+    }
+    if (!r) r = per_grid(0, [&](int b, cudaStream_t cs) { return record_finalize(pls[b], p[b], f[b], cs); }, {});
+    // the handle table, and the per-kind node counts into the controller's parameters (uniform across grids)
+    if (!r) MGSR_CUDA_TRY(cudaMemcpy(hdev, hh.data(), sizeof(cudaGraphConditionalHandle) * hh.size(), cudaMemcpyHostToDevice));
+    for (int k = 0; k < 3 && !r; ++k) {
+        nu[k] = hused[k * B];
+        for (int b = 1; b < B; ++b)
+            if (hused[k * B + b] != nu[k]) { set_error("batch: uneven conditional nodes"); r = MGSR_E_UNSUPPORTED; }
+    }
+    if (!r) MGSR_CUDA_TRY(cudaGraphKernelNodeSetParams(n_pre, &kp_pre));
+    const double *const *stats_c = stats_dev;
+    void *a_post[] = {&state, &active, &B_, &stats_c, &rec, &nit, &tol_, &sth, &hw};
+    kp.func = reinterpret_cast<void *>(k_batch_post);
+    kp.kernelParams = a_post;
+    if (!r) MGSR_CUDA_TRY(cudaGraphAddKernelNode(&n_post, body, &join, 1, &kp));
+    if (!r) {
+        cudaError_t e = cudaGraphInstantiate(&G.exec, g, 0);
+        if (e != cudaSuccess) { set_error(std::string("batch graph instantiate: ") + cudaGetErrorString(e)); r = MGSR_E_CUDA; }
+    }
+    return r;
+}
+
+}  // namespace
+
+extern "C" int mgsr_plan_solve_batch(mgsr_plan *const *plans, int32_t B, double *const *p, const double *const *f,
+                                     int32_t mode, int32_t n_iter, double tol, double s_thres, int32_t cadence,
+                                     int32_t first_sr, int32_t ngan_one, double *records_dev, int32_t *iterations_dev,
+                                     void *stream) {
+    if (!plans || !p || !f || !records_dev || !iterations_dev || B < 1 || B > 1024 || n_iter < 1 || mode < 0 ||
+        mode > 2 || cadence < 1) {
+        set_error("bad argument");
+        return MGSR_E_BAD_ARG;
+    }
+    for (int b = 0; b < B; ++b) {
+        if (!plans[b] || !p[b] || !f[b]) { set_error("bad argument"); return MGSR_E_BAD_ARG; }
+        const mgsr_plan *a = plans[0], *c = plans[b];
+        if (c->sides != a->sides || c->gen != a->gen || c->cfg.precision != a->cfg.precision ||
+            c->cfg.sr_level_mask != a->cfg.sr_level_mask || c->cfg.n_smooth != a->cfg.n_smooth ||
+            c->cfg.coarse_sweeps != a->cfg.coarse_sweeps || c->cfg.p_min != a->cfg.p_min || c->cfg.p_max != a->cfg.p_max) {
+            set_error("solve_batch: the plans must share one configuration and generator");
+            return MGSR_E_BAD_ARG;
+        }
+        for (int k = 0; k < b; ++k)
+            if (plans[k] == plans[b]) { set_error("solve_batch: a plan appears twice"); return MGSR_E_BAD_ARG; }
+    }
+    if (mode != 0 && !plans[0]->gen) { set_error("SR prolongation requires generator weights"); return MGSR_E_BAD_ARG; }
+    if (plans[0]->sides[0] <= kSmallN) { set_error("solve_batch: grids of side <= 64 run per grid"); return MGSR_E_UNSUPPORTED; }
+    if (graphs_disabled()) {
+        set_error("the batched solve loop needs CUDA graphs (disabled by MGSR_NO_GRAPH or an attached profiler)");
+        return MGSR_E_UNSUPPORTED;
+    }
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    std::vector<const void *> ids;
+    for (int b = 0; b < B; ++b) { ids.push_back(plans[b]); ids.push_back(p[b]); ids.push_back(f[b]); }
+    BatchKey key{ids, int(mode), int(n_iter), tol, s_thres, int(cadence), int(first_sr), int(ngan_one)};
+    auto it = g_batches.find(key);
+    if (it == g_batches.end()) {
+        MGSR_CUDA_TRY(cudaStreamSynchronize(st));
+        if (g_batches.size() >= 4) {   // bounded cache
+            MGSR_CUDA_TRY(cudaDeviceSynchronize());
+            for (auto &kv : g_batches) batch_free(kv.second);
+            g_batches.clear();
+        }
+        BatchGraph G;
+        std::vector<bool> mk(B);   // no event-record markers inside conditional bodies
+        for (int b = 0; b < B; ++b) { mk[b] = plans[b]->capturing_markers; plans[b]->capturing_markers = false; }
+        int r = build_batch(G, plans, B, p, f, mode, n_iter, tol, s_thres, cadence, first_sr, ngan_one);
+        for (int b = 0; b < B; ++b) plans[b]->capturing_markers = mk[b];
+        if (r) { batch_free(G); return r; }
+        it = g_batches.emplace(key, G).first;
+    }
+    BatchGraph &G = it->second;
+    MGSR_CUDA_TRY(cudaGraphLaunch(G.exec, st));
+    MGSR_CUDA_TRY(cudaMemcpyAsync(records_dev, G.rec, 4 * sizeof(double) * size_t(B) * n_iter, cudaMemcpyDeviceToDevice, st));
+    for (int b = 0; b < B; ++b)
+        MGSR_CUDA_TRY(cudaMemcpyAsync(iterations_dev + b, G.state + 4 * b + 3, sizeof(int), cudaMemcpyDeviceToDevice, st));
+    return MGSR_OK;
+}
+
+// drop the batched graphs that captured a plan's buffers (called by mgsr_plan_destroy)
+void batch_forget(const mgsr_plan *pl) {
+    bool any = false;
+    for (auto &kv : g_batches)
+        for (size_t i = 0; i < std::get<0>(kv.first).size(); i += 3)
+            if (std::get<0>(kv.first)[i] == pl) any = true;
+    if (!any) return;
+    cudaDeviceSynchronize();
+    for (auto it = g_batches.begin(); it != g_batches.end();) {
+        bool hit = false;
+        for (size_t i = 0; i < std::get<0>(it->first).size(); i += 3)
+            if (std::get<0>(it->first)[i] == pl) hit = true;
+        if (hit) { batch_free(it->second); it = g_batches.erase(it); }
+        else ++it;
+    }
 }

@@ -2,7 +2,10 @@
 random fields, config-3 generator), latched hybrid solves run concurrently with
 solver.solve_batch, for smoothing sweeps nu in {1, 2, 4} and SR at the {1, 2, 3}
 finest prolongations (per-level GAN mask).  Reports V-cycles to diff < 1e-10 per RHS
-and wall time per solve.  Not collected by pytest.
+and wall time per solve, for the batched solve (all loops in lockstep in one graph
+launch, one generator launch per SR level across the batch) next to one resident
+solve per RHS on its own stream, and checks that both give identical results.
+Not collected by pytest.
 
     python tests/config5_timing.py [out.json] [batch] [n]
     python -m torch.distributed.run --nproc-per-node 8 --master-addr 127.0.0.1 tests/config5_timing.py ...
@@ -44,11 +47,16 @@ def main():
         for gl in (1, 2, 3):
             cfg = solver.RunConfig(N_step=1, r_min=8, N_smooth=nu, mode="hybrid", N_GAN=1.0, S_thres=5e-4,
                                    N_iter=100)
-            run(probs, cfg, w, precision="fp16", sr_levels=gl)   # plans, graphs (not timed)
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            res = run(probs, cfg, w, precision="fp16", sr_levels=gl)
-            wall = time.perf_counter() - t0   # includes the gather: every rank holds all results
+            walls, outs = {}, {}
+            for batched in (True, False):
+                run(probs, cfg, w, precision="fp16", sr_levels=gl, batched=batched)   # plans, graphs (not timed)
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                outs[batched] = run(probs, cfg, w, precision="fp16", sr_levels=gl, batched=batched)
+                walls[batched] = time.perf_counter() - t0   # includes the gather: every rank holds all results
+            res, wall = outs[True], walls[True]
+            same = all(np.array_equal(a[0].data, b[0].data) and a[1].iterations == b[1].iterations
+                       for a, b in zip(outs[True], outs[False]))
             its = [log.iterations for _, log in res]
             conv = [log.converged(1e-10) for _, log in res]
             sr_cycles = [sum(r.operator == "sr" for r in log.records) for _, log in res]
@@ -56,7 +64,8 @@ def main():
                    "iterations_mean": float(np.mean(its)), "iterations_min": int(min(its)),
                    "iterations_max": int(max(its)), "all_converged": bool(all(conv)),
                    "sr_cycles_mean": float(np.mean(sr_cycles)),
-                   "wall_s_batch": wall, "wall_ms_per_solve": 1e3 * wall / batch}
+                   "wall_s_batch": wall, "wall_ms_per_solve": 1e3 * wall / batch,
+                   "wall_ms_per_solve_streams": 1e3 * walls[False] / batch, "batched_equals_streams": bool(same)}
             row["ranks"] = world
             rows.append(row)
             if rank == 0:
@@ -64,7 +73,9 @@ def main():
     if out and rank == 0:
         json.dump({"note": "fp16 tensor-core generator (trained B=8 fixture), latched hybrid N_GAN=1, S_thres=5e-4, "
                            "tol 1e-10; wall clock of the whole batch incl. host->device RHS copies and result "
-                           "readback; solves run concurrently (one plan + stream each, one graph launch per solve)",
+                           "readback; wall_ms_per_solve: the batched solve (solve_batch(batched=True): one graph launch for the "
+                           "whole batch, one generator launch per SR level across the RHS); wall_ms_per_solve_streams: one "
+                           "resident solve per RHS, each on its own stream",
                    "rows": rows}, open(out, "w"), indent=1)
 
 

@@ -186,22 +186,34 @@ def test_resident_solve_matches_host_loop(cuda, orc, mode, n):
     assert np.array_equal(p_a.data, p_b.data)
 
 
-def test_solve_batch_matches_single_solves(cuda, orc):
-    """Concurrent multi-RHS solves (one plan + stream each) give exactly the single-solve results."""
+@pytest.mark.parametrize("batched,precision,n,sr_levels", [(False, "fp32", 128, None), (True, "fp32", 128, None),
+                                                         (True, "fp16", 128, None), (True, "fp16", 256, 3)])
+def test_solve_batch_matches_single_solves(cuda, orc, batched, precision, n, sr_levels):
+    """Multi-RHS solves give exactly the single-solve results: one plan + stream each (batched=False),
+    or all solve loops in lockstep in one graph launch with one generator launch per SR level across
+    the RHS that prolong by SR in that iteration (batched=True; fp16 = the batched tensor-core launch).
+    The right-hand sides differ in scale and spectrum, so their latches and stopping iterations differ."""
     import os
     from paper_2403_07936_b200 import solver, srmodel
     from paper_2403_07936_b200.grid import Grid
     from paper_2403_07936_b200.smoother import PoissonProblem
     from conftest import ROOT
     w = srmodel.load_weights(os.path.join(ROOT, "artifacts", "trained_b8.mgsr"))
-    fs = [orc.scale_to_p_rms(orc.sine_modes_rhs(128, s), 1e-4) for s in range(3)]
+    fs = [orc.scale_to_p_rms(orc.sine_modes_rhs(n, 0), 1e-4), orc.scale_to_p_rms(orc.grf_blobs_rhs(n, seed=1, kmax=n / 8), 3e-4),
+          orc.scale_to_p_rms(orc.sine_modes_rhs(n, 2), 3e-2)]
     cfg = cfg_(mode="hybrid", N_GAN=1.0, S_thres=5e-4)
-    batch = solver.solve_batch([PoissonProblem(Grid(f)) for f in fs], cfg, w, precision="fp32")
+    batch = solver.solve_batch([PoissonProblem(Grid(f)) for f in fs], cfg, w, precision=precision, sr_levels=sr_levels,
+                               batched=batched)
+    iters = []
     for f, (pb, lb) in zip(fs, batch):
-        ps, ls = solver.solve(PoissonProblem(Grid(f)), cfg, w, precision="fp32")
+        ps, ls = solver.solve(PoissonProblem(Grid(f)), cfg, w, precision=precision, sr_levels=sr_levels)
         assert lb.iterations == ls.iterations and lb.converged(1e-10)
         assert [r.operator for r in lb.records] == [r.operator for r in ls.records]
+        assert [r.switch_latched for r in lb.records] == [r.switch_latched for r in ls.records]
+        assert [r.diff_norm for r in lb.records] == [r.diff_norm for r in ls.records]
         assert np.array_equal(pb.data, ps.data)
+        iters.append(ls.iterations)
+    print(f"\nsolve_batch batched={batched} {precision} n={n}: iterations {iters}")
 
 
 @pytest.mark.parametrize("n,seed,pmax", [(16, 0, 1e-3), (64, 3, 1e-3), (256, 0, 2.5e-2), (2048, 11, 1e-3)])
