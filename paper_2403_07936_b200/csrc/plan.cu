@@ -112,6 +112,14 @@ int ladder(int64_t n, int n_step, int r_min, std::vector<int> &sides) {
     return MGSR_OK;
 }
 
+// The finest prolongation of a spline (or non-SR-at-level-1) cycle fused with the logging pass
+// (k_prolong_finalize_rows): the mean of out is the mean of d[1], which the level-2 prolongation emits.
+bool fused_top(const mgsr_plan *pl, int use_sr) {
+    return pl->sides.size() >= 3 && pl->sides[0] == 2 * pl->sides[1] && prolong_finalize_applies(pl->sides[0]) &&
+           !(use_sr && (pl->cfg.sr_level_mask & 1u));
+}
+double *d1_out_mean(mgsr_plan *pl) { return pl->scal + SC_LEVEL0 + 4 * 1 + 3; }
+
 // Prolong the correction of level l (buffer d[l], or the coarsest GS result)
 // into level l-1 and add to `base` (level l-1 GS result with mean *bshift):
 // out = (base - *bshift) + P(corr).  mean_out (optional) = mean(out).
@@ -174,8 +182,11 @@ int correction(mgsr_plan *pl, int l, int use_sr, cudaStream_t st, int stop = 0) 
     if (l + 1 <= stop) return MGSR_OK;
     // d[l] = (d[l] - d_mean) + up  (in place: elementwise)
     const double *bshift = n <= kSmallN ? nullptr : d_mean(pl, l);
-    return prolong_into(pl, l + 1, use_sr, pl->d[l], bshift, pl->d[l], nullptr, st);
+    return prolong_into(pl, l + 1, use_sr, pl->d[l], bshift, pl->d[l],
+                        (l == 1 && fused_top(pl, use_sr)) ? d1_out_mean(pl) : nullptr, st);
 }
+
+int record_top(mgsr_plan *pl, double *p, const double *f, int use_sr, cudaStream_t st);
 
 int record_vcycle(mgsr_plan *pl, double *p, const double *f, int use_sr, cudaStream_t st) {
     const int n = pl->sides[0];
@@ -204,10 +215,7 @@ int record_vcycle(mgsr_plan *pl, double *p, const double *f, int use_sr, cudaStr
     if (mk) MGSR_CUDA_TRY(cudaEventRecordWithFlags(pl->cap_ev[3], st, cudaEventRecordExternal));
     if (s0 != 2 && (r = launch_res_restrict(pl->S, fs, n, s0, pl->rc[1], rc_mean(pl, 1), slot(pl, 1), st))) return r;
     if ((r = correction(pl, 1, use_sr, st))) return r;
-    const double *bshift = n <= kSmallN ? nullptr : sc(pl, SC_S_MEAN);
-    if ((r = prolong_into(pl, 1, use_sr, pl->S, bshift, pl->S, sc(pl, SC_OUT_MEAN), st))) return r;
-    r = launch_finalize(pl->S, sc(pl, SC_OUT_MEAN), p, fs, n, sc(pl, SC_ACC), sc(pl, SC_STATS), slot(pl, 0), st);
-    if (r) return r;
+    if ((r = record_top(pl, p, f, use_sr, st))) return r;
     if (mk) MGSR_CUDA_TRY(cudaEventRecordWithFlags(pl->cap_ev[5], st, cudaEventRecordExternal));
     return MGSR_OK;
 }
@@ -221,7 +229,8 @@ int prolong_level(mgsr_plan *pl, int l, int use_sr, cudaStream_t st) {
         return prolong_into(pl, 1, use_sr, pl->S, bshift, pl->S, sc(pl, SC_OUT_MEAN), st);
     }
     const double *bshift = pl->sides[l - 1] <= kSmallN ? nullptr : d_mean(pl, l - 1);
-    return prolong_into(pl, l, use_sr, pl->d[l - 1], bshift, pl->d[l - 1], nullptr, st);
+    return prolong_into(pl, l, use_sr, pl->d[l - 1], bshift, pl->d[l - 1],
+                        (l == 2 && fused_top(pl, use_sr)) ? d1_out_mean(pl) : nullptr, st);
 }
 
 int record_down(mgsr_plan *pl, double *p, const double *f, int use_sr, cudaStream_t st, int stop) {
@@ -233,8 +242,7 @@ int record_down(mgsr_plan *pl, double *p, const double *f, int use_sr, cudaStrea
                       s0 == 2 ? rc_mean(pl, 1) : nullptr, sc(pl, SC_S_MEAN), pl->red, st);
     if (r) return r;
     if (s0 != 2 && (r = launch_res_restrict(pl->S, fs, n, s0, pl->rc[1], rc_mean(pl, 1), slot(pl, 1), st))) return r;
-    if ((r = correction(pl, 1, use_sr, st, stop))) return r;
-    return stop == 0 ? prolong_level(pl, 1, use_sr, st) : MGSR_OK;
+    return correction(pl, 1, use_sr, st, stop);
 }
 
 // the SR branch of prolong_into after the (batched) generator wrote this grid's raw output to srbuf
@@ -245,14 +253,25 @@ int sr_add_level(mgsr_plan *pl, int l, const double *srbuf, cudaStream_t st) {
     double *base = l == 1 ? pl->S : pl->d[l - 1];
     const double *bshift = l == 1 ? (pl->sides[0] <= kSmallN ? nullptr : sc(pl, SC_S_MEAN))
                                   : (pl->sides[l - 1] <= kSmallN ? nullptr : d_mean(pl, l - 1));
-    return launch_add2(base, bshift, srbuf, sr_mean(pl, l), base, nf * nf, l == 1 ? sc(pl, SC_OUT_MEAN) : nullptr,
-                       slot(pl, 3), st);
+    double *mean_out = l == 1 ? sc(pl, SC_OUT_MEAN) : ((l == 2 && fused_top(pl, 1)) ? d1_out_mean(pl) : nullptr);
+    return launch_add2(base, bshift, srbuf, sr_mean(pl, l), base, nf * nf, mean_out, slot(pl, 3), st);
 }
 
 int record_finalize(mgsr_plan *pl, double *p, const double *f, cudaStream_t st) {
     FSrc fs{f, nullptr, 1.0};
     return launch_finalize(pl->S, sc(pl, SC_OUT_MEAN), p, fs, pl->sides[0], sc(pl, SC_ACC), sc(pl, SC_STATS),
                            slot(pl, 0), st);
+}
+
+// the finest prolongation and the logging pass of a cycle (record_vcycle's tail)
+int record_top(mgsr_plan *pl, double *p, const double *f, int use_sr, cudaStream_t st) {
+    if (fused_top(pl, use_sr)) {
+        FSrc fs{f, nullptr, 1.0};
+        return launch_prolong_finalize(pl->S, sc(pl, SC_S_MEAN), pl->d[1], pl->sides[1], d1_out_mean(pl), p, fs,
+                                       sc(pl, SC_ACC), sc(pl, SC_STATS), slot(pl, 0), st);
+    }
+    int r = prolong_level(pl, 1, use_sr, st);
+    return r ? r : record_finalize(pl, p, f, st);
 }
 
 }  // namespace
@@ -897,13 +916,19 @@ int build_batch(BatchGraph &G, mgsr_plan *const *pls, int B, double *const *p, c
             cudaGraphConditionalHandle h;
             r = new_handle(1, b, &h);
             if (!r) r = add_if(body, &nd, &j0, h, cudaGraphCondTypeIf, &bd);
-            if (!r) r = capture_into(bd, G.cap, [&](cudaStream_t cs) { return record_down(pls[b], p[b], f[b], 0, cs, 0); });
+            if (!r) r = capture_into(bd, G.cap, [&](cudaStream_t cs) { return record_vcycle(pls[b], p[b], f[b], 0, cs); });
             sp.push_back(nd);
         }
-        if (!r) r = per_grid(2, [&](int b, cudaStream_t cs) { return record_down(pls[b], p[b], f[b], 1, cs, stop); }, sp);
+        if (!r) r = per_grid(2, [&](int b, cudaStream_t cs) {
+            return stop > 0 ? record_down(pls[b], p[b], f[b], 1, cs, stop) : record_vcycle(pls[b], p[b], f[b], 1, cs);
+        }, sp);
     }
     for (int l = stop; !r && l >= 1; --l) {
         const bool batched = sr_lev[l] && tc && p0->sides[l - 1] == 2 * p0->sides[l];
+        if (l == 1 && !sr_lev[1]) {   // the cycle's spline top prolongation and its logging pass (maybe fused)
+            r = per_grid(2, [&](int b, cudaStream_t cs) { return record_top(pls[b], p[b], f[b], 1, cs); }, {});
+            continue;
+        }
         if (!batched) {   // spline level between SR levels, fp32 generator, or a multi-pass ratio: per grid
             r = per_grid(2, [&](int b, cudaStream_t cs) { return prolong_level(pls[b], l, 1, cs); }, {});
             continue;
@@ -926,7 +951,8 @@ int build_batch(BatchGraph &G, mgsr_plan *const *pls, int B, double *const *p, c
         join = n_sr;
         r = per_grid(2, [&](int b, cudaStream_t cs) { return sr_add_level(pls[b], l, srbuf + size_t(b) * nf * nf, cs); }, {});
     }
-    if (!r) r = per_grid(0, [&](int b, cudaStream_t cs) { return record_finalize(pls[b], p[b], f[b], cs); }, {});
+    if (!r && stop > 0 && sr_lev[1])   // after an SR top prolongation: the logging pass
+        r = per_grid(2, [&](int b, cudaStream_t cs) { return record_finalize(pls[b], p[b], f[b], cs); }, {});
     // the handle table, and the per-kind node counts into the controller's parameters (uniform across grids)
     if (!r) MGSR_CUDA_TRY(cudaMemcpy(hdev, hh.data(), sizeof(cudaGraphConditionalHandle) * hh.size(), cudaMemcpyHostToDevice));
     for (int k = 0; k < 3 && !r; ++k) {

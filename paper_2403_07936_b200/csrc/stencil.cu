@@ -1018,6 +1018,187 @@ __global__ void __launch_bounds__(256, 4) k_finalize_rows(const double *__restri
     }
 }
 
+
+// Keys ratio-2 weights applied in k_prolong2_rows' order (vertical: rows a-1..a+2; horizontal: columns)
+__device__ __forceinline__ double pf_vert(double c0, double c1, double c2, double c3) {
+    const double w0 = -0.0625, w1 = 0.5625;
+    double row = 0.0;
+    row += w0 * c0;
+    row += w1 * c1;
+    row += w1 * c2;
+    row += w0 * c3;
+    return row;
+}
+__device__ __forceinline__ double pf_hint(double q0, double q1, double q2, double q3) {
+    const double w0 = -0.0625, w1 = 0.5625;
+    double a = 0.0;
+    a += w0 * q0; a += w1 * q1; a += w1 * q2; a += w0 * q3;
+    return a;
+}
+
+// The finest spline prolongation fused with the solve-loop logging pass (k_prolong2_rows + k_finalize_rows
+// without the out field in HBM): out = (S - *bshift) + P(c) is evaluated row by row from S and the coarse
+// correction c (Keys ratio 2, the k_prolong2_rows arithmetic), and immediately consumed by the logging
+// pass: p <- out - m, diff and residual accumulators, stats.  m = *out_mean, the mean of out, is taken as
+// the mean of c (the Keys weights of every coarse value sum to 4 fine cells, so mean(P(c)) = mean(c), and
+// mean(S - *bshift) = 0): a grid-wide reduction of out before the pass is not needed.  34 B per fine cell
+// (S, p, f read, p written, c read once per 4 cells) instead of 18 + 32.
+// Thread = coarse column bj (fine columns 2 bj, 2 bj + 1), marching down a strip of fine rows; the own
+// column's coarse rows a - 1 .. a + 2 stay in registers (one new coarse row per two fine rows), the
+// neighbouring columns' values come by shuffle; lanes 0 / 31 also carry the two coarse columns beyond the
+// warp and evaluate the out values left / right of the warp for the Laplacian.  nc % 32 == 0.
+__global__ void __launch_bounds__(256, 2) k_prolong_finalize_rows(
+    const double *__restrict__ S, const double *bshift, const double *__restrict__ c, int nc,
+    const double *out_mean, double *__restrict__ p, FSrc fs, double inv_h2, RedSlot slot, double *acc_out,
+    double *stats, int rows) {
+    const int n = 2 * nc;
+    const int lane = threadIdx.x & 31;
+    const int bj = blockIdx.x * blockDim.x + threadIdx.x;
+    const bool active = bj < nc;   // whole warps
+    const int c0 = 2 * bj;
+    const double bsh = *bshift, m = *out_mean;
+    const double sh = fs.load_shift();
+    const bool shifted = fs.shift != nullptr;
+    const int r0 = blockIdx.y * rows, r1 = min(r0 + rows, n);
+    double v[3] = {0.0, 0.0, 0.0};
+    if (active && r0 < r1) {
+        // extra coarse columns: lane 0 -> bj - 2, bj - 1; lane 31 -> bj + 1, bj + 2
+        const int xa = lane == 0 ? wrap(bj - 2, nc) : wrap(bj + 1, nc), xb = lane == 0 ? wrap(bj - 1, nc) : wrap(bj + 2, nc);
+        const bool edge = lane == 0 || lane == 31;
+        // coarse rows a - 1 .. a + 2 of the own column (w*) and the extra columns (a*, b*)
+        double w_0, w_1, w_2, w_3, a_0 = 0.0, a_1 = 0.0, a_2 = 0.0, a_3 = 0.0, b_0 = 0.0, b_1 = 0.0, b_2 = 0.0, b_3 = 0.0;
+#define PF_LOAD(K, ROW)                                               \
+    {                                                                 \
+        const double *cr_ = c + int64_t(wrap((ROW), nc)) * nc;        \
+        w_##K = __ldg(cr_ + bj);                                      \
+        if (edge) {                                                   \
+            a_##K = __ldg(cr_ + xa);                                  \
+            b_##K = __ldg(cr_ + xb);                                  \
+        }                                                             \
+    }
+        int i = r0 == 0 ? n - 1 : r0 - 1;
+        int a = i >> 1;
+        PF_LOAD(0, a - 1) PF_LOAD(1, a) PF_LOAD(2, a + 1) PF_LOAD(3, a + 2)
+        // out row ii from the window and its S values (s2 = the own pair, sl / sr_ = the halo S of lanes 0 / 31):
+        // the own pair (x = 2 bj, y = 2 bj + 1) and the values left of 2 bj / right of 2 bj + 1
+        auto out_row = [&](bool odd, double2 s2, double sl, double sr_, double2 &o, double &hl, double &hr) {
+            const double Ro = odd ? pf_vert(w_0, w_1, w_2, w_3) : w_1;
+            double Ra = 0.0, Rb = 0.0;
+            if (edge) {
+                Ra = odd ? pf_vert(a_0, a_1, a_2, a_3) : a_1;
+                Rb = odd ? pf_vert(b_0, b_1, b_2, b_3) : b_1;
+            }
+            const double up1 = __shfl_up_sync(0xffffffffu, Ro, 1);
+            const double dn1 = __shfl_down_sync(0xffffffffu, Ro, 1);
+            const double dn2 = __shfl_down_sync(0xffffffffu, Ro, 2);
+            const double l31a = __shfl_sync(0xffffffffu, Ra, 31);   // lane 31's R at bj + 1 (= bj + 2 of lane 30)
+            const double Rm1 = lane == 0 ? Rb : up1;                  // coarse column bj - 1
+            const double Rp1 = lane == 31 ? Ra : dn1;                 // bj + 1
+            const double Rp2 = lane == 31 ? Rb : (lane == 30 ? l31a : dn2);   // bj + 2
+            o.x = (s2.x - bsh) + Ro;
+            o.y = (s2.y - bsh) + pf_hint(Rm1, Ro, Rp1, Rp2);
+            hl = __shfl_up_sync(0xffffffffu, o.y, 1);
+            hr = __shfl_down_sync(0xffffffffu, o.x, 1);
+            if (lane == 0) hl = (sl - bsh) + pf_hint(Ra, Rb, Ro, Rp1);
+            if (lane == 31) hr = (sr_ - bsh) + Rp1;
+        };
+        const int cl = c0 == 0 ? n - 1 : c0 - 1, crr = c0 + 2 >= n ? c0 + 2 - n : c0 + 2;
+        auto load_s = [&](int ii, double2 &s2, double &sl, double &sr_) {
+            const double *srow = S + int64_t(ii) * n;
+            s2 = __ldg(reinterpret_cast<const double2 *>(srow + c0));
+            if (lane == 0) sl = __ldg(srow + cl);
+            if (lane == 31) sr_ = __ldg(srow + crr);
+        };
+        double2 up, cur, dn, s2;
+        double sl = 0.0, srr = 0.0, hl_c, hr_c, hl_d, hr_d, tl, tr;
+        load_s(i, s2, sl, srr);
+        out_row(i & 1, s2, sl, srr, up, tl, tr);
+        // one fine row down: the window moves by one coarse row when the coarse row index changes
+        {
+            const int an = r0 >> 1;
+            if (an != a) {
+                a = an;
+                w_0 = w_1; w_1 = w_2; w_2 = w_3;
+                a_0 = a_1; a_1 = a_2; a_2 = a_3;
+                b_0 = b_1; b_1 = b_2; b_2 = b_3;
+                PF_LOAD(3, a + 2)
+            }
+        }
+        i = r0;
+        load_s(i, s2, sl, srr);
+        out_row(i & 1, s2, sl, srr, cur, hl_c, hr_c);
+        // prefetched operands of the next iteration: S of row i + 1, p / f of row i, the coarse row the window
+        // needs at row i + 1
+        int i1 = i + 1 >= n ? i + 1 - n : i + 1;
+        double2 sN, pN, fN;
+        double slN = 0.0, srN = 0.0, cwN = 0.0, caN = 0.0, cbN = 0.0;
+        load_s(i1, sN, slN, srN);
+        pN = *reinterpret_cast<const double2 *>(p + int64_t(i) * n + c0);
+        fN = __ldg(reinterpret_cast<const double2 *>(fs.f + int64_t(i) * n + c0));
+        bool shiftN = (i1 >> 1) != a;
+        if (shiftN) {
+            const double *cr_ = c + int64_t(wrap((i1 >> 1) + 2, nc)) * nc;
+            cwN = __ldg(cr_ + bj);
+            if (edge) { caN = __ldg(cr_ + xa); cbN = __ldg(cr_ + xb); }
+        }
+#pragma unroll 1
+        for (; i < r1; ++i) {
+            const double2 pp = pN, ff = fN, sc2 = sN;
+            const double scl = slN, scr = srN;
+            if (shiftN) {
+                a = i1 >> 1;
+                w_0 = w_1; w_1 = w_2; w_2 = w_3; w_3 = cwN;
+                a_0 = a_1; a_1 = a_2; a_2 = a_3; a_3 = caN;
+                b_0 = b_1; b_1 = b_2; b_2 = b_3; b_3 = cbN;
+            }
+            const bool odd1 = i1 & 1;
+            // next iteration's loads first
+            if (i + 1 < r1) {
+                const int i2 = i1 + 1 >= n ? i1 + 1 - n : i1 + 1;
+                load_s(i2, sN, slN, srN);
+                pN = *reinterpret_cast<const double2 *>(p + int64_t(i1) * n + c0);
+                fN = __ldg(reinterpret_cast<const double2 *>(fs.f + int64_t(i1) * n + c0));
+                shiftN = (i2 >> 1) != a;
+                if (shiftN) {
+                    const double *cr_ = c + int64_t(wrap((i2 >> 1) + 2, nc)) * nc;
+                    cwN = __ldg(cr_ + bj);
+                    if (edge) { caN = __ldg(cr_ + xa); cbN = __ldg(cr_ + xb); }
+                }
+                i1 = i2;
+            }
+            out_row(odd1, sc2, scl, scr, dn, hl_d, hr_d);
+            const double nb0 = ((up.x + dn.x) + hl_c) + cur.y;
+            const double nb1 = ((up.y + dn.y) + cur.x) + hr_c;
+            const double f0 = shifted ? (ff.x - sh) * fs.scale : ff.x;
+            const double f1 = shifted ? (ff.y - sh) * fs.scale : ff.y;
+            const double np0 = cur.x - m, np1 = cur.y - m;
+            const double d0 = np0 - pp.x, d1 = np1 - pp.y;
+            const double q0 = f0 - ((nb0 - 4.0 * cur.x) * inv_h2);
+            const double q1 = f1 - ((nb1 - 4.0 * cur.y) * inv_h2);
+            *reinterpret_cast<double2 *>(p + int64_t(i) * n + c0) = make_double2(np0, np1);
+            v[0] += d0 * d0;
+            v[0] += d1 * d1;
+            v[1] += q0;
+            v[1] += q1;
+            v[2] += q0 * q0;
+            v[2] += q1 * q1;
+            up = cur;
+            cur = dn;
+            hl_c = hl_d;
+            hr_c = hr_d;
+        }
+    }
+#undef PF_LOAD
+    double *const outs[3] = {acc_out, acc_out + 1, acc_out + 2};
+    const double inv = 1.0 / (double(n) * double(n));
+    const double scales[3] = {inv, inv, inv};
+    if (grid_reduce_to<3>(v, slot, outs, scales)) {
+        stats[0] = sqrt(acc_out[0]);
+        const double var = acc_out[2] - acc_out[1] * acc_out[1];
+        stats[1] = sqrt(var > 0.0 ? var : 0.0);
+    }
+}
+
 __global__ void k_stats_sqrt(const double *acc, double *stats) {
     stats[0] = sqrt(acc[0]);
     double var = acc[2] - acc[1] * acc[1];
@@ -1262,6 +1443,24 @@ int launch_res_restrict(const double *p, FSrc fs, int n, int s, double *rc, doub
     RedSlot sl = red_slot_at(red_slot);
     k_res_restrict<<<grid_2d(nc, nc), 256, 0, st>>>(p, fs, n, s, 1.0 / ((2.0 * M_PI / n) * (2.0 * M_PI / n)),
                                                                        rc, sl, rc_mean);
+    MGSR_LAUNCH_CHECK();
+    return MGSR_OK;
+}
+
+// the fused finest spline prolongation + logging pass (k_prolong_finalize_rows); false when it does not apply
+bool prolong_finalize_applies(int n) { return n >= 1024 && (n / 2) % 256 == 0 && !std::getenv("MGSR_NO_FUSED_TOP"); }
+int launch_prolong_finalize(const double *S, const double *bshift, const double *c, int nc, const double *out_mean,
+                            double *p, FSrc fs, double *acc3, double *stats2, void *red_slot, cudaStream_t st) {
+    RedSlot sl = red_slot_at(red_slot);
+    const int n = 2 * nc;
+    const double h = 2.0 * M_PI / n;
+    const int gx = nc / 256;
+    int strips = (2 * num_sms()) / gx;   // one wave at 2 CTAs per SM
+    strips = strips < 1 ? 1 : (strips > n ? n : strips);
+    const int rows = (n + strips - 1) / strips;
+    const dim3 g(gx, (n + rows - 1) / rows);
+    if (int64_t(g.x) * g.y > kRedMaxBlocks) { set_error("prolong_finalize grid too large"); return MGSR_E_UNSUPPORTED; }
+    k_prolong_finalize_rows<<<g, 256, 0, st>>>(S, bshift, c, nc, out_mean, p, fs, 1.0 / (h * h), sl, acc3, stats2, rows);
     MGSR_LAUNCH_CHECK();
     return MGSR_OK;
 }

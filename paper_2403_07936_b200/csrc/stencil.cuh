@@ -18,6 +18,9 @@ int launch_res_restrict(const double *p, FSrc fs, int n, int s, double *rc, doub
                         cudaStream_t st);
 int launch_finalize(const double *out, const double *mean_ptr, double *p, FSrc fs, int n, double *acc3,
                     double *stats2, void *red_slot, cudaStream_t st);
+bool prolong_finalize_applies(int n);
+int launch_prolong_finalize(const double *S, const double *bshift, const double *c, int nc, const double *out_mean,
+                            double *p, FSrc fs, double *acc3, double *stats2, void *red_slot, cudaStream_t st);
 int launch_affine(const double *a, double *out, int64_t count, const double *shift, double scale, cudaStream_t st);
 // correction of a whole ratio-2 sub-ladder with sides[0] <= kSmallN in one CTA (spline prolongation)
 // a whole spline V-cycle + logging pass of a ratio-2 ladder with sides[0] <= kSmallN in one CTA
