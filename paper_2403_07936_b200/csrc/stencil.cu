@@ -131,6 +131,34 @@ __device__ void small_gs(double *sp, const double *sf, int n, double h2, int swe
     }
 }
 
+// The same sweeps with the mean subtracted once at the end: Gauss-Seidel is shift-equivariant (every update
+// (sum of neighbours - h^2 f) / 4 moves by c when all values move by c), so the per-sweep subtractions add up
+// to subtracting the final mean (the deferred-mean identity, as k_gs_rb uses it).  Saves four
+// barriers and two passes per sweep on the latency-bound bottom of the ladder.
+__device__ void small_gs_deferred(double *sp, const double *sf, int n, double h2, int sweeps, double *sred) {
+    const int tid = threadIdx.x, nt = blockDim.x, nn = n * n, half = nn >> 1;
+    const int hn = n >> 1, hsh = pow2_shift(hn);
+    for (int s = 0; s < sweeps; ++s) {
+        for (int color = 0; color < 2; ++color) {
+            for (int t = tid; t < half; t += nt) {
+                int i, k;
+                split_idx(t, hn, hsh, i, k);
+                int jj = 2 * k + ((i + color) & 1);
+                int im1 = i > 0 ? i - 1 : n - 1, ip1 = i < n - 1 ? i + 1 : 0;
+                int jm1 = jj > 0 ? jj - 1 : n - 1, jp1 = jj < n - 1 ? jj + 1 : 0;
+                double nb = ((sp[im1 * n + jj] + sp[ip1 * n + jj]) + sp[i * n + jm1]) + sp[i * n + jp1];
+                sp[i * n + jj] = (nb - h2 * sf[i * n + jj]) * 0.25;
+            }
+            __syncthreads();
+        }
+    }
+    double acc = 0.0;
+    for (int c = tid; c < nn; c += nt) acc += sp[c];
+    const double mean = block_sum_1024(acc, sred) * (1.0 / double(nn));
+    for (int c = tid; c < nn; c += nt) sp[c] -= mean;
+    __syncthreads();
+}
+
 // Raw residual f - L p at the injected (even, even) points of an n-grid -> fr (n/2 x n/2); returns
 // the mean (block sum).  Arithmetic of k_res_restrict / the fused residual of k_gs_rb.
 __device__ double small_residual_inject(const double *sp, const double *sf, int n, double *fr, double *sred) {
@@ -204,7 +232,11 @@ __device__ void small_ladder(double *const *D, double *const *F, const SmallLadd
         for (int c = tid; c < nn; c += nt) D[j][c] = 0.0;
         __syncthreads();
         const double h = 2.0 * M_PI / n;
+#ifdef MGSR_EXACT_SMALL_MEANS
         small_gs(D[j], F[j], n, h * h, j == L.nlev - 1 ? coarse_sweeps : n_smooth, sred);
+#else
+        small_gs_deferred(D[j], F[j], n, h * h, j == L.nlev - 1 ? coarse_sweeps : n_smooth, sred);
+#endif
         if (j < L.nlev - 1) {   // residual at the injected points -> next RHS 0.5 (r - mean(r))
             const int ncc = (n >> 1) * (n >> 1);
             const double mean = small_residual_inject(D[j], F[j], n, F[j + 1], sred);
@@ -1198,6 +1230,7 @@ __global__ void __launch_bounds__(256, 2) k_prolong_finalize_rows(
         stats[1] = sqrt(var > 0.0 ? var : 0.0);
     }
 }
+
 
 __global__ void k_stats_sqrt(const double *acc, double *stats) {
     stats[0] = sqrt(acc[0]);
