@@ -119,3 +119,46 @@ def vcycle_(p: torch.Tensor, f: torch.Tensor, plan: int, use_sr: int, stats: tor
     """One graph-launched V-cycle + logging pass (solver.v_cycle + solver.py:312-313)."""
     _check_t(p, "p"); _check_t(f, "f"); _check_t(stats, "stats")
     _lib.check(_lib.load().mgsr_plan_vcycle(plan, p.data_ptr(), f.data_ptr(), int(use_sr), stats.data_ptr(), _st()))
+
+
+# Fake (meta) kernels: output shapes and dtypes for tracing / FakeTensor propagation (no compute, no library).
+@gs_sweeps_.register_fake
+def _(p, f, h2, sweeps):
+    return None
+
+
+@laplacian.register_fake
+def _(p, inv_h2):
+    return torch.empty_like(p)
+
+
+@residual.register_fake
+def _(p, f):
+    return torch.empty_like(p)
+
+
+@restrict.register_fake
+def _(fine, s, subtract_mean):
+    n = fine.shape[0]
+    nc = n // s if s > 0 and n % s == 0 else 1
+    return fine.new_empty((nc, nc))
+
+
+@spline_prolong.register_fake
+def _(c, s):
+    return c.new_empty((c.shape[0] * max(s, 1), c.shape[0] * max(s, 1)))
+
+
+@sr_prolong.register_fake
+def _(c, gen, s, p_min, p_max, precision):
+    return c.new_empty((c.shape[0] * s, c.shape[0] * s))
+
+
+@generator_forward.register_fake
+def _(x, gen):
+    return x.new_empty((x.shape[0], 3, 2 * x.shape[2], 2 * x.shape[3]))
+
+
+@vcycle_.register_fake
+def _(p, f, plan, use_sr, stats):
+    return None

@@ -315,3 +315,20 @@ def test_bench_gpus2_self_launch_gloo():
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["config"]["parallelism"] == "replicas x2"
     assert abs(d["value"] - 2 * 4 / 0.110) < 1e-9
+
+
+def test_custom_op_fake_kernels():
+    """The torch.library ops carry fake (meta) kernels: shapes propagate under FakeTensorMode without the
+    CUDA library or a GPU."""
+    import torch
+    from torch._subclasses.fake_tensor import FakeTensorMode
+    from paper_2403_07936_b200 import ops  # noqa: F401
+    with FakeTensorMode():
+        p = torch.empty(64, 64, dtype=torch.float64)
+        assert torch.ops.mgsr.laplacian(p, 1.0).shape == (64, 64)
+        assert torch.ops.mgsr.residual(p, p).shape == (64, 64)
+        assert torch.ops.mgsr.restrict(p, 4, True).shape == (16, 16)
+        assert torch.ops.mgsr.spline_prolong(p, 4).shape == (256, 256)
+        assert torch.ops.mgsr.sr_prolong(p, 0, 16, 1e-10, 1e-3, 2).shape == (1024, 1024)
+        x = torch.empty(5, 3, 6, 6, dtype=torch.float64)
+        assert torch.ops.mgsr.generator_forward(x, 0).shape == (5, 3, 12, 12)
