@@ -1,5 +1,9 @@
+# Round-end measurement (GPU): the GPU test suite, smoke, the bench lines (GAN trained / He-init, spline,
+# reference arm), the ncu launch lists of both bench modes and one --set full capture of the generator.
 set -x
 mkdir -p gpurun_out/final
+python -m pytest tests -m gpu -q > gpurun_out/final/gputests.log 2>&1; echo rc=$? >> gpurun_out/final/gputests.log
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/final/smoke.log 2>&1
 python bench.py > gpurun_out/final/bench_gan.json 2> gpurun_out/final/bench_gan.err
 python bench.py --mode spline > gpurun_out/final/bench_spline.json 2> gpurun_out/final/bench_spline.err
 python bench.py --weights he --no-cpu-baseline > gpurun_out/final/bench_he.json 2> gpurun_out/final/bench_he.err
