@@ -397,3 +397,25 @@ def test_default_config_sr_vcycle_vs_oracle(cuda, orc, precision, bar):
     err = rel_l2(got - got.mean(), exp - exp.mean())
     print(f"default-config SR V-cycle {precision}: relL2 {err:.3e}")
     assert err < bar, err
+
+
+def test_solve_batch_default_config_ratio16_matches_single(cuda, orc):
+    """Batched solves with the reference's default ladder (N_step=4, r_min=12: [192, 12], one ratio-16 SR
+    prolongation = two ratio-4 tensor-core passes, run per grid inside the batched graph) equal the single
+    solves bitwise."""
+    import os
+    from paper_2403_07936_b200 import solver, srmodel
+    from paper_2403_07936_b200.grid import Grid
+    from paper_2403_07936_b200.smoother import PoissonProblem
+    from conftest import ROOT
+    w = srmodel.load_weights(os.path.join(ROOT, "artifacts", "trained_b8.mgsr"))
+    n = 192
+    fs = [orc.scale_to_p_rms(orc.grf_blobs_rhs(n, seed=s, kmax=24.0), 1e-4) for s in range(2)]
+    cfg = cfg_(N_step=4, r_min=12, N_smooth=20, mode="hybrid", N_GAN=1.0, S_thres=5e-4, N_iter=40)
+    batch = solver.solve_batch([PoissonProblem(Grid(f)) for f in fs], cfg, w, precision="fp16", batched=True)
+    for f, (pb, lb) in zip(fs, batch):
+        ps, ls = solver.solve(PoissonProblem(Grid(f)), cfg, w, precision="fp16")
+        assert lb.iterations == ls.iterations
+        assert [r.operator for r in lb.records] == [r.operator for r in ls.records]
+        assert [r.diff_norm for r in lb.records] == [r.diff_norm for r in ls.records]
+        assert np.array_equal(pb.data, ps.data)
