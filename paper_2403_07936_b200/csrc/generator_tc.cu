@@ -980,6 +980,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
                         lds16(sc + 64 + cb, kb);
                         float a[16];
                         load_dx3(a);
+                        tr(17, L + 1, t);
                         if (conv1) {
                             float al[16];
                             lds16(sc + 128 + cb, al);

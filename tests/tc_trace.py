@@ -18,7 +18,7 @@ from paper_2403_07936_b200 import _lib, srmodel  # noqa: E402
 NAMES = {1: "P.fill", 2: "M.act_ready", 3: "M.issued", 4: "M.weights", 5: "M.i2c_full",
          6: "E.acc_full", 7: "E.arrive", 8: "D.acc_full", 9: "D.ubuf_free", 10: "D.ubuf_full",
          11: "E.group_start/q", 12: "E.i2c_built", 13: "Z.full", 14: "Z.stored", 15: "E.end",
-         16: "M.tail_issue"}
+         16: "M.tail_issue", 17: "E.acc_loaded"}
 ROLES = ["producer", "mma", "epi_w2", "epi_w10"]
 
 
