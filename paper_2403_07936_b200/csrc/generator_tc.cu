@@ -147,6 +147,13 @@ static_assert(Geo<2>::WPG * 432 * 4 <= MISC_BYTES, "misc (V = 2)");
 // this CTA's 16 N rows, [dy 9][k 2][16 n][8].
 constexpr int UQ = 16;
 constexpr int UP_QUARTERS_C = 4;
+// Up-conv column order: epilogue thread cq's 16 columns j of a quarter are 8 shuffled channels (m = j / 2 of
+// the quarter's channel group cq / 2) x the two sub-pixels jj = j % 2 of sub-row ii = cq % 2, so a thread
+// writes two adjacent 16-byte U pixel rows (32 B contiguous, lanes contiguous).  Column 16 cq + j holds the
+// up conv's output channel 64 u + up_col_channel(16 cq + j) = 4 c + 2 ii + jj (pixel shuffle, srmodel.py:321).
+__host__ __device__ constexpr int up_col_channel(int col) {
+    return 32 * ((col >> 4) >> 1) + 4 * ((col & 15) >> 1) + 2 * ((col >> 4) & 1) + (col & 1);
+}
 constexpr int U_BYTES_MAX = 2 * Geo<0>::U_PLANE;       // 49152
 constexpr int TW_HALF = 9 * 512;                       // 4608: this CTA's half of a quarter's tail weights
 constexpr int TW_QBYTES = 2 * TW_HALF;                 // a quarter in the blob (both halves)
@@ -1048,9 +1055,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
                 // tail MMAs (V = 0, 2: edge windows also spill it for the edge-tail kernel).  U is rewritten
                 // for quarter u once the tail MMAs of quarter u - 1 released it. ----
                 for (int u = 0; u < UP_QUARTERS; ++u) {
-                    float ua[4];
+                    float ua[8];   // PReLU alpha of this thread's 8 shuffled channels
 #pragma unroll
-                    for (int m = 0; m < 4; ++m) ua[m] = up_a[UQ * u + 4 * cq + m];
+                    for (int m = 0; m < 8; ++m) ua[m] = up_a[UQ * u + 8 * (cq >> 1) + m];
 #pragma unroll
                     for (int t = 0; t < T; ++t) {
                         tr(8, u, t);
@@ -1059,51 +1066,51 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
                         if (u > 0 && t == 0) mbar_wait(b_ubuf_free, uint32_t(u - 1) & 1u);
                         tr(9, u, t);
                         if (interior) {
-                            // column 16 cq + j -> shuffled channel 16 u + 4 cq + j / 4, sub-pixel ((j >> 1) & 1, j & 1)
-                            const int py = TPY * t + 1 + pyl;
+                            // column j -> shuffled channel 16 u + 8 (cq >> 1) + j / 2, sub-pixel (cq & 1, j & 1)
+                            const int py = TPY * t + 1 + pyl, ii = cq & 1;
                             float y[16];
 #pragma unroll
                             for (int j = 0; j < 16; ++j) {
                                 const float x = a[j];
-                                y[j] = x > 0.f ? x : ua[j >> 2] * x;
+                                y[j] = x > 0.f ? x : ua[j >> 1] * x;
                             }
-                            uint8_t *Ub = ubuf + (cq >> 1) * G::U_PLANE + 8 * (cq & 1);
+                            uint8_t *Ub = ubuf + (cq >> 1) * G::U_PLANE;
+                            const int Y = 2 * (py - 1) + ii, X0 = 2 * (px - 1);
+                            uint4 val[2];
 #pragma unroll
-                            for (int sub = 0; sub < 4; ++sub) {
-                                const int Y = 2 * (py - 1) + (sub >> 1), X = 2 * (px - 1) + (sub & 1);
-                                const uint2 val = make_uint2(pack_op<F16>(y[sub], y[4 + sub]), pack_op<F16>(y[8 + sub], y[12 + sub]));
-                                if constexpr (V == 0) {
-                                    *reinterpret_cast<uint2 *>(Ub + (Y * G::UROWS_Y + 12 * wrow + X) * 16) = val;
-                                } else if constexpr (V == 1) {
-                                    // chunk rows 4 zc - 4 .. 4 zc + 7, replicate-clamped at the window edge
-                                    const int Yu = Y - 4 * zc + 4;
-                                    if (Yu >= 0 && Yu < 12)
-                                        *reinterpret_cast<uint2 *>(Ub + (Yu * G::UROWS_Y + 12 * wrow + X) * 16) = val;
-                                    if (zc == 0 && Y == 0)
+                            for (int jj = 0; jj < 2; ++jj)
+                                val[jj] = make_uint4(pack_op<F16>(y[jj], y[2 + jj]), pack_op<F16>(y[4 + jj], y[6 + jj]),
+                                                     pack_op<F16>(y[8 + jj], y[10 + jj]), pack_op<F16>(y[12 + jj], y[14 + jj]));
+                            auto put = [&](int urow) {   // pixels (Y, X0), (Y, X0 + 1) of U rows urow, urow + 1
+                                uint4 *d = reinterpret_cast<uint4 *>(Ub + urow * 16);
+                                d[0] = val[0];
+                                d[1] = val[1];
+                            };
+                            if constexpr (V == 0) {
+                                put(Y * G::UROWS_Y + 12 * wrow + X0);
+                            } else if constexpr (V == 1) {
+                                // chunk rows 4 zc - 4 .. 4 zc + 7, replicate-clamped at the window edge
+                                const int Yu = Y - 4 * zc + 4;
+                                if (Yu >= 0 && Yu < 12) put(Yu * G::UROWS_Y + 12 * wrow + X0);
+                                if (zc == 0 && Y == 0)
 #pragma unroll
-                                        for (int e = 0; e < 4; ++e)
-                                            *reinterpret_cast<uint2 *>(Ub + (e * G::UROWS_Y + 12 * wrow + X) * 16) = val;
-                                    if (zc == 2 && Y == 11)
+                                    for (int e = 0; e < 4; ++e) put(e * G::UROWS_Y + 12 * wrow + X0);
+                                if (zc == 2 && Y == 11)
 #pragma unroll
-                                        for (int e = 8; e < 12; ++e)
-                                            *reinterpret_cast<uint2 *>(Ub + (e * G::UROWS_Y + 12 * wrow + X) * 16) = val;
-                                } else {
-                                    if (Y >= 4 && Y < 20 && X >= 4 && X < 20)
-                                        *reinterpret_cast<uint2 *>(Ub + ((Y - 4) * G::UROWS_Y + 16 * wrow + X - 4) * 16) = val;
-                                }
+                                    for (int e = 8; e < 12; ++e) put(e * G::UROWS_Y + 12 * wrow + X0);
+                            } else {
+                                if (Y >= 4 && Y < 20 && X0 >= 4 && X0 < 20) put((Y - 4) * G::UROWS_Y + 16 * wrow + X0 - 4);
                             }
                             if constexpr (V != 1) {
                                 const Win &W = Wd;
                                 const int pp = (py - 1) * G::WS + (px - 1);
-                                if (W.valid && W.edge) {
-                                    uint32_t pk[8];
-#pragma unroll
-                                    for (int j = 0; j < 8; ++j) pk[j] = pack_op<F16>(y[2 * j], y[2 * j + 1]);
+                                if (W.valid && W.edge) {   // spill in the up conv's channel order (edge-tail kernels)
                                     const size_t ei = BATCH ? size_t(W.rhs) * edge_count(P.npos) + edge_index(W.wi, W.wj, P.npos)
                                                             : size_t(edge_index(W.wi, W.wj, P.npos));
-                                    uint4 *dst = reinterpret_cast<uint4 *>(P.edge_u + (ei * (G::WS * G::WS) + pp) * 256 + 64 * u + cb);
-                                    dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-                                    dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+                                    uint32_t *dst = reinterpret_cast<uint32_t *>(
+                                        P.edge_u + (ei * (G::WS * G::WS) + pp) * 256 + 64 * u + 32 * (cq >> 1) + 2 * ii);
+#pragma unroll
+                                    for (int m = 0; m < 8; ++m) dst[2 * m] = pack_op<F16>(y[2 * m], y[2 * m + 1]);
                                 }
                             }
                             if constexpr (INSTR && V == 0) {
@@ -1111,8 +1118,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
                                 if (P.dbg && P.dbg_layer == NL + 1 && Wd.valid) {
 #pragma unroll
                                     for (int j = 0; j < 16; ++j) {
-                                        const int c = UQ * u + 4 * cq + (j >> 2), Y = 2 * (py - 1) + ((j >> 1) & 1),
-                                                  X = 2 * (px - 1) + (j & 1);
+                                        const int c = UQ * u + 8 * (cq >> 1) + (j >> 1), X = X0 + (j & 1);
                                         P.dbg[(k * 144 + Y * 12 + X) * 64 + c] = y[j];
                                     }
                                 }
@@ -1553,15 +1559,17 @@ int tc_pack_weights(mgsr_gen *g, const float *const *t) {
     // kernel row dy of a 3x3 64 -> 64 conv (output channels oc0..oc0 + 63): [half][ng 12][kc 8][8 rows][8 ic], so
     // a CTA's unit is one K-major B operand of N = 96 rows with 8-row groups 1 KB apart; row n' = 48 (oc' / 16)
     // + 16 dx + oc' % 16 (oc' = oc % 32), so an epilogue thread's 16 channels x 3 dx are adjacent columns
-    auto pack_row = [&](uint16_t *dst, const float *w, int oc0, int dy, int bn_gi) {
+    // perm: the up conv's column order (up_col_channel); identity for the body layers
+    auto pack_row = [&](uint16_t *dst, const float *w, int oc0, int dy, int bn_gi, bool perm) {
         uint16_t *dst16 = reinterpret_cast<uint16_t *>(reinterpret_cast<uint8_t *>(dst) + BL.fmt_stride);
         for (int dx = 0; dx < 3; ++dx)
             for (int kc = 0; kc < 8; ++kc)
                 for (int oc = 0; oc < 64; ++oc) {
-                    const double k = bn_gi >= 0 ? bn_scale(bn_gi, oc0 + oc) : 1.0;
+                    const int wc = oc0 + (perm ? up_col_channel(oc) : oc);
+                    const double k = bn_gi >= 0 ? bn_scale(bn_gi, wc) : 1.0;
                     for (int e = 0; e < 8; ++e) {
                         int ic = 8 * kc + e;
-                        const float v = float(double(w[(((oc0 + oc) * 64 + ic) * 3 + dy) * 3 + dx]) * k);
+                        const float v = float(double(w[((wc * 64 + ic) * 3 + dy) * 3 + dx]) * k);
                         const int nr = 48 * ((oc & 31) >> 4) + 16 * dx + (oc & 15);
                         const int o = ((((oc >> 5) * 12 + (nr >> 3)) * 8 + kc) * 8 + (nr & 7)) * 8 + e;
                         dst[o] = f2bf(v);
@@ -1577,11 +1585,11 @@ int tc_pack_weights(mgsr_gen *g, const float *const *t) {
     for (int L = 0; L < BL.nl; ++L)
         for (int dy = 0; dy < 3; ++dy)
             pack_row(reinterpret_cast<uint16_t *>(blob.data() + BL.body + (size_t(L) * 3 + dy) * ROW_BYTES),
-                     t[conv_index(L)], 0, dy, bn_index(L));
+                     t[conv_index(L)], 0, dy, bn_index(L), false);
     for (int u = 0; u < UP_QUARTERS; ++u)
         for (int dy = 0; dy < 3; ++dy)
             pack_row(reinterpret_cast<uint16_t *>(blob.data() + BL.up + (size_t(u) * 3 + dy) * ROW_BYTES),
-                     t[ip + 5], 64 * u, dy, -1);
+                     t[ip + 5], 64 * u, dy, -1, true);
     {
         // tail B operand: per quarter u and CTA half h, [dy 9][k 2][16 n][8] with n = 16 h + n' = 3 dx + o
         // (27 of 32 used) and k = shuffled channel 16 u + 8 k + e
