@@ -1443,49 +1443,53 @@ __global__ void __launch_bounds__(TE4_THREADS) k_tail_edge4(Params P, int nedge)
         else if (e < 2 * n) { wi = n - 1; wj = e - n; }
         else { wi = 1 + (e - 2 * n) / 2; wj = ((e - 2 * n) & 1) ? n - 1 : 0; }
         const int lo_i = wi == 0 ? 0 : 8, hi_i = wi == last ? 24 : 16, lo_j = wj == 0 ? 0 : 8, hi_j = wj == last ? 24 : 16;
-        const int wk = hi_j - lo_j, npx = (hi_i - lo_i) * wk;
-        const int fy = tid < npx ? lo_i + tid / wk : lo_i, fx = tid < npx ? lo_j + tid % wk : lo_j;
-        float acc[3] = {0.f, 0.f, 0.f};
+        const int wk = hi_j - lo_j, npx = (hi_i - lo_i) * wk;   // <= 16 x 16, or 24 x 24 for a single window
         const uint16_t *src = P.edge_u + size_t(e) * 144 * 256;
 #pragma unroll 1
-        for (int c0 = 0; c0 < 64; c0 += TE4_CH) {
-            __syncthreads();   // the previous chunk / window is consumed
-            for (int i = tid; i < TE4_CH * TE4_PAD * TE4_PAD; i += TE4_THREADS) {
-                const int c = i / (TE4_PAD * TE4_PAD), yp = (i / TE4_PAD) % TE4_PAD, xp = i % TE4_PAD;
-                const int Y = min(max(yp - 4, 0), 23), X = min(max(xp - 4, 0), 23);
-                const int oc = 4 * (c0 + c) + 2 * (Y & 1) + (X & 1);
-                U[i] = op_lo<F16>(uint32_t(src[((Y >> 1) * 12 + (X >> 1)) * 256 + oc]));
-            }
-            for (int i = tid; i < TE4_CH * 3 * 81; i += TE4_THREADS) {
-                const int c = i / 243, o = (i / 81) % 3, tap = i % 81;
-                Wc[i] = __ldg(w + (o * 64 + c0 + c) * 81 + tap);
-            }
-            __syncthreads();
-            if (tid < npx) {
+        for (int p0 = 0; p0 < npx; p0 += TE4_THREADS) {
+            const int pix = p0 + tid;
+            const int fy = pix < npx ? lo_i + pix / wk : lo_i, fx = pix < npx ? lo_j + pix % wk : lo_j;
+            float acc[3] = {0.f, 0.f, 0.f};
 #pragma unroll 1
-                for (int c = 0; c < TE4_CH; ++c)
+            for (int c0 = 0; c0 < 64; c0 += TE4_CH) {
+                __syncthreads();   // the previous chunk / window is consumed
+                for (int i = tid; i < TE4_CH * TE4_PAD * TE4_PAD; i += TE4_THREADS) {
+                    const int c = i / (TE4_PAD * TE4_PAD), yp = (i / TE4_PAD) % TE4_PAD, xp = i % TE4_PAD;
+                    const int Y = min(max(yp - 4, 0), 23), X = min(max(xp - 4, 0), 23);
+                    const int oc = 4 * (c0 + c) + 2 * (Y & 1) + (X & 1);
+                    U[i] = op_lo<F16>(uint32_t(src[((Y >> 1) * 12 + (X >> 1)) * 256 + oc]));
+                }
+                for (int i = tid; i < TE4_CH * 3 * 81; i += TE4_THREADS) {
+                    const int c = i / 243, o = (i / 81) % 3, tap = i % 81;
+                    Wc[i] = __ldg(w + (o * 64 + c0 + c) * 81 + tap);
+                }
+                __syncthreads();
+                if (pix < npx) {
 #pragma unroll 1
-                    for (int dy = 0; dy < 9; ++dy) {
-                        const float *ur = U + (c * TE4_PAD + fy + dy) * TE4_PAD + fx;
-                        const float *wr = Wc + c * 243 + dy * 9;
+                    for (int c = 0; c < TE4_CH; ++c)
+#pragma unroll 1
+                        for (int dy = 0; dy < 9; ++dy) {
+                            const float *ur = U + (c * TE4_PAD + fy + dy) * TE4_PAD + fx;
+                            const float *wr = Wc + c * 243 + dy * 9;
 #pragma unroll
-                        for (int dx = 0; dx < 9; ++dx) {
-                            const float u = ur[dx];
+                            for (int dx = 0; dx < 9; ++dx) {
+                                const float u = ur[dx];
 #pragma unroll
-                            for (int o = 0; o < 3; ++o) acc[o] = fmaf(u, wr[o * 81 + dx], acc[o]);
+                                for (int o = 0; o < 3; ++o) acc[o] = fmaf(u, wr[o * 81 + dx], acc[o]);
+                            }
                         }
-                    }
+                }
             }
-        }
-        if (tid < npx) {
-            double m = 0.0;
+            if (pix < npx) {
+                double m = 0.0;
 #pragma unroll
-            for (int o = 0; o < 3; ++o) {
-                const float pre = acc[o] + __ldg(bias + o);
-                m += double(P.tanh_s * tanhf(pre / P.tanh_s));
+                for (int o = 0; o < 3; ++o) {
+                    const float pre = acc[o] + __ldg(bias + o);
+                    m += double(P.tanh_s * tanhf(pre / P.tanh_s));
+                }
+                m = m / 3.0;
+                P.fine[(long long)(4 * (2 * wi) + fy) * P.nf + 4 * (2 * wj) + fx] = denormalize_q(m, P.log_lo, P.span);
             }
-            m = m / 3.0;
-            P.fine[(long long)(4 * (2 * wi) + fy) * P.nf + 4 * (2 * wj) + fx] = denormalize_q(m, P.log_lo, P.span);
         }
     }
 }

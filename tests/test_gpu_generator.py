@@ -335,3 +335,18 @@ def test_generator_forward_matches_reference_trainer_fixtures(cuda, blocks):
     for x, y in zip(fx[f"b{blocks}_inputs"], fx[f"b{blocks}_outputs"]):
         got = srmodel.generator_forward(w, x.astype(np.float64))
         assert np.abs(got - y).max() < 1e-4
+
+
+@pytest.mark.parametrize("nc", [6, 8, 10, 14, 26])
+def test_tc_ratio4_pass_tiny_and_ragged_grids(cuda, orc, nc):
+    """Ratio-4 passes where every window is an edge window (nc = 6: one window; 8: 2 x 2) and where the
+    window count leaves the last 2-window group of the second application half full (nc = 10, 14, 26):
+    fp16 tensor cores against the fp64 oracle at the 1e-2 bar (trained B=8)."""
+    from paper_2403_07936_b200 import srmodel
+    from paper_2403_07936_b200.grid import Grid, NormBounds
+    w = _trained(8)
+    c = _fields(32)["smooth"][:nc, :nc]
+    c = c - c.mean()
+    exp = orc.sr_prolong(c, orc.quantize_f32(_oracle_weights(orc, w)), orc.Bounds(), 4)
+    got = srmodel.sr_prolong(Grid(c), w, NormBounds(), 4, precision="fp16").data
+    assert rel_l2(got, exp) < 1e-2, rel_l2(got, exp)
