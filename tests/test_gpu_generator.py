@@ -350,3 +350,19 @@ def test_tc_ratio4_pass_tiny_and_ragged_grids(cuda, orc, nc):
     exp = orc.sr_prolong(c, orc.quantize_f32(_oracle_weights(orc, w)), orc.Bounds(), 4)
     got = srmodel.sr_prolong(Grid(c), w, NormBounds(), 4, precision="fp16").data
     assert rel_l2(got, exp) < 1e-2, rel_l2(got, exp)
+
+
+def test_tc_ratio4_pass_bf16_operands(cuda, orc):
+    """The bf16-operand instantiations of the ratio-4 kernels (V = 1, 2 with F16 = false) run and stay within
+    their operand format's error (bf16 has 8x coarser mantissas than fp16: DESIGN.md "Operand precision"),
+    and fp16 is the more accurate of the two."""
+    from paper_2403_07936_b200 import srmodel
+    from paper_2403_07936_b200.grid import Grid, NormBounds
+    w = _trained(8)
+    c = _fields(40)["smooth"][:40, :40]
+    c = c - c.mean()
+    exp = orc.sr_prolong(c, orc.quantize_f32(_oracle_weights(orc, w)), orc.Bounds(), 4)
+    eb = rel_l2(srmodel.sr_prolong(Grid(c), w, NormBounds(), 4, precision="bf16").data, exp)
+    e16 = rel_l2(srmodel.sr_prolong(Grid(c), w, NormBounds(), 4, precision="fp16").data, exp)
+    print(f"\nratio-4 pass relL2: bf16 {eb:.2e}, fp16 {e16:.2e}")
+    assert e16 < eb < 5e-2
