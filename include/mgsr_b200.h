@@ -85,7 +85,7 @@ int mgsr_rms_diff(const double *a, const double *b, int64_t count, double *out_h
 
 typedef struct mgsr_gen mgsr_gen;
 
-enum { MGSR_PREC_FP32 = 0, MGSR_PREC_BF16 = 1, MGSR_PREC_FP16 = 2 };
+enum { MGSR_PREC_FP32 = 0, MGSR_PREC_BF16 = 1, MGSR_PREC_FP16 = 2, MGSR_PREC_MIXED = 3 };
 
 /* Build an immutable generator from the MGSR1 tensor set (host float32 arrays in
  * the canonical order of expected_tensor_shapes(B), srmodel.py:90-114), i.e.
@@ -107,7 +107,10 @@ int mgsr_generator_forward(const mgsr_gen *g, const double *x, int64_t batch, in
  * stride 2, generator, channel mean, stitch, denormalise with output signs,
  * mean-subtract (per pass).  precision: MGSR_PREC_FP32 (CUDA-core fp32),
  * MGSR_PREC_BF16 / MGSR_PREC_FP16 (tcgen05 megakernel with bf16 / fp16 operands,
- * fp32 accumulation, tf32 head; ratio-2 passes only).
+ * fp32 accumulation; ratio-2 passes and ratio-4 passes), MGSR_PREC_MIXED (fp16
+ * tensor cores, except the first pass of a two-pass ratio x8 / x16, which runs in
+ * fp32: the second pass re-normalises its output logarithmically and amplifies its
+ * operand rounding ~25x).
  * Replaces srmodel.sr_prolong (srmodel.py:470-487). */
 size_t mgsr_sr_workspace_bytes(int64_t nc, int32_t s);
 int mgsr_sr_prolong(const mgsr_gen *g, const double *c, int64_t nc, int32_t s,

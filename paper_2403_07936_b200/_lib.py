@@ -26,14 +26,16 @@ def graphs_disabled() -> bool:
 
 MGSR_OK = 0
 MGSR_E_CUDA = -8
-PREC = {"fp32": 0, "bf16": 1, "fp16": 2}
+PREC = {"fp32": 0, "bf16": 1, "fp16": 2, "mixed": 3}
 
 
 def precision(p: str | None) -> str:
-    """Generator precision of an operator call: an explicit argument wins, else ``MGSR_PRECISION``
-    (default "fp16": the tcgen05 tensor-core generator; "fp32" is the exact CUDA-core mode)."""
+    """Generator precision of an operator call: an explicit argument wins, else ``MGSR_PRECISION``, else
+    "mixed": the tcgen05 tensor-core generator with fp16 operands, except the first pass of a two-pass
+    ratio (x8, x16), which runs on the fp32 CUDA cores because the second pass amplifies its rounding
+    ~25x.  "fp16" / "bf16": tensor cores for every pass; "fp32": the exact CUDA-core mode."""
     import os
-    p = p if p is not None else os.environ.get("MGSR_PRECISION", "fp16")
+    p = p if p is not None else os.environ.get("MGSR_PRECISION", "mixed")
     if p not in PREC:
         raise ValueError(f"precision must be one of {sorted(PREC)}, got {p!r}")
     return p

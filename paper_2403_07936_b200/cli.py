@@ -37,7 +37,7 @@ from .solver import RunConfig, solve, solve_batch
 
 SWEEP_COLUMNS = ("param", "value", "replicate", "rhs_id", "iters_to_converge", "converged", "final_diff")
 SWEEP_PARAMS = ("N_smooth", "N_GAN", "S_thres", "N_grid", "k_peak")
-PRECISIONS = ("fp32", "bf16", "fp16")
+PRECISIONS = ("fp32", "bf16", "fp16", "mixed")
 
 
 class CliError(Exception):
@@ -269,8 +269,9 @@ def cmd_datagen(a) -> int:
 
 def _common_solver_flags(sp):
     sp.add_argument("--precision", choices=PRECISIONS, default=None,
-                    help="generator path for SR prolongations (default MGSR_PRECISION or fp16: tcgen05 tensor cores; "
-                         "fp32: the exact CUDA-core mode)")
+                    help="generator path for SR prolongations (default MGSR_PRECISION or mixed: tcgen05 tensor cores "
+                         "with an exact first pass for x8/x16; fp16/bf16: tensor cores throughout; fp32: the exact "
+                         "CUDA-core mode)")
     sp.add_argument("--sr-levels", type=int, default=None,
                     help="SR only at the N finest prolongations (spline below); default: every level")
 

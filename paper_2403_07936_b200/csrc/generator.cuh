@@ -24,8 +24,17 @@ struct mgsr_gen {
 namespace mgsr {
 
 // One predicate decides both the workspace size and the kernel of a precision mode.
-inline bool valid_precision(int p) { return p == MGSR_PREC_FP32 || p == MGSR_PREC_BF16 || p == MGSR_PREC_FP16; }
-inline bool tensor_core_precision(int p) { return p == MGSR_PREC_BF16 || p == MGSR_PREC_FP16; }
+inline bool valid_precision(int p) {
+    return p == MGSR_PREC_FP32 || p == MGSR_PREC_BF16 || p == MGSR_PREC_FP16 || p == MGSR_PREC_MIXED;
+}
+// the tensor-core path for ratio-2 / single-pass work (MIXED = fp16 there)
+inline bool tensor_core_precision(int p) { return p == MGSR_PREC_BF16 || p == MGSR_PREC_FP16 || p == MGSR_PREC_MIXED; }
+// the precision of pass `ip` of `npass` under a precision mode: MIXED runs the first pass of a two-pass
+// ratio in fp32 and everything else as fp16
+inline int pass_precision(int p, int ip, int npass) {
+    if (p != MGSR_PREC_MIXED) return p;
+    return (npass == 2 && ip == 0) ? MGSR_PREC_FP32 : MGSR_PREC_FP16;
+}
 
 // Windowed SR prolongation (one full sr_prolong, all passes).
 // c_shift: optional device scalar subtracted from c before normalising.

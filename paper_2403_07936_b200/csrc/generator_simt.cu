@@ -416,8 +416,10 @@ static size_t pass_ws_floats(int apps) {
 size_t sr_workspace_bytes(int64_t nc, int s, int precision) {
     // intermediate fine grid for two-pass ratios + fp32 chunk buffers + scalars
     size_t inter = (s == 8 || s == 16) ? sizeof(double) * size_t(nc * 4) * size_t(nc * 4) : 0;
-    // the fp32 CUDA-core chunk buffers only for fp32 (the tensor-core precisions never fall back to them)
-    size_t simt = tensor_core_precision(precision) ? 0 : sizeof(float) * pass_ws_floats(s == 2 ? 1 : 2) + 4096;
+    // the fp32 CUDA-core chunk buffers only for the passes that run in fp32 (the tensor-core passes never fall
+    // back to them): fp32 everywhere, or MIXED's first pass of a two-pass ratio (two applications)
+    const bool simt_pass = !tensor_core_precision(precision) || (precision == MGSR_PREC_MIXED && (s == 8 || s == 16));
+    size_t simt = simt_pass ? sizeof(float) * pass_ws_floats(s == 2 ? 1 : 2) + 4096 : 0;
     size_t tc = 0;
     if (tensor_core_precision(precision)) {   // the largest pass of the plan: (ratio, coarse side) per pass
         tc = s == 2 ? tc_workspace_bytes(nc) : tc4_workspace_bytes(nc);
@@ -473,7 +475,7 @@ static int sr_pass_simt(const mgsr_gen *g, const double *c, const double *c_shif
 int launch_sr_prolong(const mgsr_gen *g, const double *c, const double *c_shift, int nc, int s, double p_min,
                       double p_max, int precision, double *out, double *out_mean, void *ws, size_t ws_bytes,
                       void *red_slot, cudaStream_t st, cudaEvent_t *gen_markers) {
-    if (!valid_precision(precision)) { set_error("precision must be one of fp32, bf16, fp16"); return MGSR_E_BAD_ARG; }
+    if (!valid_precision(precision)) { set_error("precision must be one of fp32, bf16, fp16, mixed"); return MGSR_E_BAD_ARG; }
     int npass = 0;
     const int *plan = pass_plan(s, &npass);
     if (!plan) { set_error("unsupported SR ratio " + std::to_string(s) + "; expected one of [2, 4, 8, 16]"); return MGSR_E_SR_RATIO; }
@@ -499,14 +501,15 @@ int launch_sr_prolong(const mgsr_gen *g, const double *c, const double *c_shift,
         int r;
         const bool mark = gen_markers && ip == npass - 1;
         if (mark) MGSR_CUDA_TRY(cudaEventRecordWithFlags(gen_markers[0], st, cudaEventRecordExternal));
-        if (tensor_core_precision(precision)) {
+        const int pprec = pass_precision(precision, ip, npass);
+        if (tensor_core_precision(pprec)) {
             // tensor-core path only; no silent fallback to the fp32 CUDA-core path
             if (!g->tc_blob) { set_error("tensor-core weights not packed"); return MGSR_E_UNSUPPORTED; }
             const size_t left = ws_bytes - size_t(w - static_cast<char *>(ws));
             r = apps == 1 ? launch_sr_pass_tc(g, src, src_shift, n_in, log_lo, span, dst, w, left, st,
-                                              precision == MGSR_PREC_FP16)
+                                              pprec != MGSR_PREC_BF16)
                           : launch_sr_pass4_tc(g, src, src_shift, n_in, log_lo, span, dst, w, left, st,
-                                               precision == MGSR_PREC_FP16);
+                                               pprec != MGSR_PREC_BF16);
         } else {
             r = sr_pass_simt(g, src, src_shift, n_in, apps, log_lo, span, dst, reinterpret_cast<float *>(w), st);
         }
@@ -631,7 +634,7 @@ extern "C" int mgsr_sr_prolong(const mgsr_gen *g, const double *c, int64_t nc, i
                                double p_max, int32_t precision, double *out, void *ws, size_t ws_bytes,
                                void *stream) {
     if (!g || !c || !out) { set_error("SR prolongation requires generator weights"); return MGSR_E_BAD_ARG; }
-    if (!valid_precision(precision)) { set_error("precision must be one of fp32, bf16, fp16"); return MGSR_E_BAD_ARG; }
+    if (!valid_precision(precision)) { set_error("precision must be one of fp32, bf16, fp16, mixed"); return MGSR_E_BAD_ARG; }
     if (ws_bytes < mgsr_sr_workspace_bytes(nc, s)) { set_error("workspace too small"); return MGSR_E_WORKSPACE; }
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     char *w = static_cast<char *>(ws);

@@ -280,7 +280,7 @@ extern "C" int mgsr_plan_create(const mgsr_plan_config *cfg, const mgsr_gen *gen
     if (!cfg || !out) { set_error("bad argument"); return MGSR_E_BAD_ARG; }
     if (cfg->n_smooth < 1 || cfg->coarse_sweeps < 1) { set_error("sweep counts must be positive"); return MGSR_E_BAD_ARG; }
     if (cfg->r_min < 2 || cfg->r_min % 2) { set_error("r_min must be an even integer >= 2"); return MGSR_E_BAD_ARG; }
-    if (!valid_precision(cfg->precision)) { set_error("precision must be one of fp32, bf16, fp16"); return MGSR_E_BAD_ARG; }
+    if (!valid_precision(cfg->precision)) { set_error("precision must be one of fp32, bf16, fp16, mixed"); return MGSR_E_BAD_ARG; }
     mgsr_plan *pl = new mgsr_plan();
     pl->cfg = *cfg;
     pl->gen = gen;
@@ -941,7 +941,7 @@ int build_batch(BatchGraph &G, mgsr_plan *const *pls, int B, double *const *p, c
         const double *const *csl = cs_dev + size_t(l) * B;
         r = capture_into(sg, G.cap, [&](cudaStream_t cs) {
             return launch_sr_pass_tc_batch(p0->gen, csl, B, list, count, nc, log_lo, span, srbuf, srws, srws_bytes, cs,
-                                           p0->cfg.precision == MGSR_PREC_FP16);
+                                           p0->cfg.precision != MGSR_PREC_BF16);
         });
         cudaGraphNode_t n_sr;
         if (!r) MGSR_CUDA_TRY(cudaGraphAddChildGraphNode(&n_sr, body, &join, 1, sg));

@@ -4,11 +4,13 @@ Mirrors ``mgsr.srmodel`` (srmodel.py:25-487).  Weights are host tensors in
 the MGSR1 format (same names, shapes, validation and typed errors); inference
 runs on the GPU:
 
-* ``precision="fp16"`` (the default; ``MGSR_PRECISION`` overrides it) -- the tcgen05 tensor-core
-  megakernel (fp16 operands, fp32 accumulation in TMEM): ratio-2 passes on 6x6 windows and
-  ratio-4 passes (x4, x8 = x4 + x2, x16 = x4 + x4) as two applications (full 12x12x3 first
-  output, 12x12 windows of 3 channels second);
-* ``precision="bf16"`` -- the same kernels with bf16 operands;
+* ``precision="mixed"`` (the default; ``MGSR_PRECISION`` overrides it) -- the tcgen05 tensor-core
+  megakernel (fp16 operands, fp32 accumulation in TMEM) for ratio-2 passes on 6x6 windows and
+  ratio-4 passes (two applications: full 12x12x3 first output, 12x12 windows of 3 channels
+  second), except the first pass of a two-pass ratio (x8 = x4 + x2, x16 = x4 + x4), which runs on
+  the fp32 CUDA cores: the second pass re-normalises it logarithmically and amplifies its operand
+  rounding ~25x (fp16 throughout: ~5e-2 relL2 at x16; mixed: ~2e-3);
+* ``precision="fp16"`` / ``"bf16"`` -- the tensor cores for every pass;
 * ``precision="fp32"`` -- CUDA-core fp32 generator (the exact mode: <= 1e-5 of the reference's
   fp64; any window side).
 """

@@ -35,7 +35,7 @@ def main():
     w = tg._trained(8)
     rows = []
     for s, nc, precs in [(2, 2048, ("fp16",)), (4, 768, ("fp16", "fp32")), (4, 1024, ("fp16",)),
-                         (16, 12, ("fp16", "fp32")), (16, 192, ("fp16", "fp32")), (8, 384, ("fp16",))]:
+                         (16, 12, ("fp16", "mixed", "fp32")), (16, 192, ("fp16", "mixed", "fp32")), (8, 384, ("fp16", "mixed"))]:
         f = datagen.scale_to_p_rms(datagen.grf_blobs_rhs(nc, seed=5, kmax=nc / 8), 1e-4)
         c = torch.from_numpy(datagen.spectral_solution(f)).cuda()
         for pr in precs:

@@ -366,3 +366,22 @@ def test_tc_ratio4_pass_bf16_operands(cuda, orc):
     e16 = rel_l2(srmodel.sr_prolong(Grid(c), w, NormBounds(), 4, precision="fp16").data, exp)
     print(f"\nratio-4 pass relL2: bf16 {eb:.2e}, fp16 {e16:.2e}")
     assert e16 < eb < 5e-2
+
+
+@pytest.mark.parametrize("weights", ["trained_b8", "trained_b4", "he_b1"])
+@pytest.mark.parametrize("s,nc", [(8, 16), (8, 40), (16, 12), (16, 24)])
+def test_mixed_two_pass_ratios_vs_oracle(cuda, orc, weights, s, nc):
+    """precision="mixed" (the default): x8 / x16 prolongations with the first ratio-4 pass on the fp32 CUDA
+    cores and the second pass (16x the windows) on the fp16 tensor cores, end to end against the fp64 oracle
+    at the north-star 1e-2 bar.  (fp16 throughout lands at 5e-2 on these fields: the second pass amplifies
+    the first pass's operand rounding; the reverse split -- first fp16, second exact -- shows the same
+    4.8e-2 in the CPU emulation, the forward one 1.8e-3.)"""
+    from paper_2403_07936_b200 import srmodel
+    from paper_2403_07936_b200.grid import Grid, NormBounds
+    w = {"trained_b8": lambda: _trained(8), "trained_b4": lambda: _trained(4),
+         "he_b1": lambda: srmodel.random_weights(1, 3)}[weights]()
+    c = _fields(max(nc, 16))["smooth"][:nc, :nc]
+    c = c - c.mean()
+    exp = orc.sr_prolong(c, orc.quantize_f32(_oracle_weights(orc, w)), orc.Bounds(), s)
+    got = srmodel.sr_prolong(Grid(c), w, NormBounds(), s).data     # default precision: mixed
+    assert rel_l2(got, exp) < 1e-2, rel_l2(got, exp)
