@@ -222,6 +222,107 @@ __device__ void small_prolong2_add(const double *c, int nc, double *out) {
     __syncthreads();
 }
 
+// The same three level operations with the side N a compile-time constant (the power-of-two sides of the
+// N_step = 1 ladders: 64, 32, 16, 8): index arithmetic folds to shifts and masks and each thread's cells are
+// an unrolled, fixed-count loop whose shared-memory loads issue together, instead of a runtime-bounded loop
+// of dependent address computations.  Per cell the arithmetic is the generic functions', and every
+// per-thread partial sum visits its cells in the same order, so results are bitwise identical.
+template <int N>
+__device__ __forceinline__ void small_level_down(double *sp, double *sf, int sweeps, double *fr, double *sred) {
+    constexpr int NT = kSmallThreads, NN = N * N, HALF = NN / 2, HN = N / 2, NC = N / 2, NCC = NC * NC;
+    const int tid = threadIdx.x;
+    for (int it = 0; it < (NN + NT - 1) / NT; ++it)
+        if (tid + it * NT < NN) sp[tid + it * NT] = 0.0;
+    __syncthreads();
+    const double h = 2.0 * M_PI / N, h2 = h * h;
+#pragma unroll 1
+    for (int s = 0; s < sweeps; ++s) {
+#pragma unroll
+        for (int color = 0; color < 2; ++color) {
+#pragma unroll
+            for (int it = 0; it < (HALF + NT - 1) / NT; ++it) {
+                const int t = tid + it * NT;
+                if (t < HALF) {
+                    const int i = t / HN, k = t % HN;
+                    const int jj = 2 * k + ((i + color) & 1);
+                    const int im1 = (i + N - 1) % N, ip1 = (i + 1) % N, jm1 = (jj + N - 1) % N, jp1 = (jj + 1) % N;
+                    double nb = ((sp[im1 * N + jj] + sp[ip1 * N + jj]) + sp[i * N + jm1]) + sp[i * N + jp1];
+                    sp[i * N + jj] = (nb - h2 * sf[i * N + jj]) * 0.25;
+                }
+            }
+            __syncthreads();
+        }
+    }
+    {
+        double acc = 0.0;
+#pragma unroll
+        for (int it = 0; it < (NN + NT - 1) / NT; ++it)
+            if (tid + it * NT < NN) acc += sp[tid + it * NT];
+        const double mean = block_sum_1024(acc, sred) * (1.0 / double(NN));
+#pragma unroll
+        for (int it = 0; it < (NN + NT - 1) / NT; ++it)
+            if (tid + it * NT < NN) sp[tid + it * NT] -= mean;
+        __syncthreads();
+    }
+    if (!fr) return;
+    const double inv_h2 = 1.0 / (h * h);
+    double acc = 0.0, res[(NCC + NT - 1) / NT];
+#pragma unroll
+    for (int it = 0; it < (NCC + NT - 1) / NT; ++it) {
+        const int t = tid + it * NT;
+        res[it] = 0.0;
+        if (t < NCC) {
+            const int i = 2 * (t / NC), jj = 2 * (t % NC);
+            const int im1 = (i + N - 1) % N, ip1 = (i + 1) % N, jm1 = (jj + N - 1) % N, jp1 = (jj + 1) % N;
+            const int c = i * N + jj;
+            double nb = ((sp[im1 * N + jj] + sp[ip1 * N + jj]) + sp[i * N + jm1]) + sp[i * N + jp1];
+            res[it] = sf[c] - ((nb - 4.0 * sp[c]) * inv_h2);
+            acc += res[it];
+        }
+    }
+    const double mean = block_sum_1024(acc, sred) * (1.0 / double(NCC));
+#pragma unroll
+    for (int it = 0; it < (NCC + NT - 1) / NT; ++it)
+        if (tid + it * NT < NCC) fr[tid + it * NT] = (res[it] - mean) * 0.5;
+    __syncthreads();
+}
+
+template <int NC>
+__device__ __forceinline__ void small_prolong2_add_t(const double *c, double *out) {
+    constexpr int NT = kSmallThreads, N = 2 * NC;
+    const double w0 = -0.0625, w1 = 0.5625;
+    const int tid = threadIdx.x;
+#pragma unroll
+    for (int it = 0; it < (NC * NC + NT - 1) / NT; ++it) {
+        const int t = tid + it * NT;
+        if (t >= NC * NC) continue;
+        const int bi = t / NC, bj = t % NC;
+        double R0[4], R1[4];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const int cb = (bj + b - 1 + NC) % NC;
+            const double c0 = c[((bi + NC - 1) % NC) * NC + cb], c1 = c[bi * NC + cb];
+            const double c2 = c[((bi + 1) % NC) * NC + cb], c3 = c[((bi + 2) % NC) * NC + cb];
+            R0[b] = c1;
+            double row = 0.0;
+            row += w0 * c0;
+            row += w1 * c1;
+            row += w1 * c2;
+            row += w0 * c3;
+            R1[b] = row;
+        }
+        double a01 = 0.0, a11 = 0.0;
+        a01 += w0 * R0[0]; a01 += w1 * R0[1]; a01 += w1 * R0[2]; a01 += w0 * R0[3];
+        a11 += w0 * R1[0]; a11 += w1 * R1[1]; a11 += w1 * R1[2]; a11 += w0 * R1[3];
+        const int t0 = (2 * bi) * N + 2 * bj, t1 = t0 + N;
+        out[t0] = (out[t0] - 0.0) + R0[1];
+        out[t0 + 1] = (out[t0 + 1] - 0.0) + a01;
+        out[t1] = (out[t1] - 0.0) + R1[1];
+        out[t1 + 1] = (out[t1 + 1] - 0.0) + a11;
+    }
+    __syncthreads();
+}
+
 // correction(rhs, l) of solver.py:181-190 for a ratio-2 sub-ladder in shared memory: D[j], F[j]
 // per level, F[0] filled by the caller; leaves the correction of level 0 in D[0].
 __device__ void small_ladder(double *const *D, double *const *F, const SmallLadder &L, int n_smooth,
@@ -229,22 +330,39 @@ __device__ void small_ladder(double *const *D, double *const *F, const SmallLadd
     const int tid = threadIdx.x, nt = blockDim.x;
     for (int j = 0; j < L.nlev; ++j) {
         const int n = L.side[j], nn = n * n;
+        const int sweeps = j == L.nlev - 1 ? coarse_sweeps : n_smooth;
+        double *const fr = j < L.nlev - 1 ? F[j + 1] : nullptr;
+#ifndef MGSR_EXACT_SMALL_MEANS
+        if (nt == kSmallThreads && (n == 64 || n == 32 || n == 16 || n == 8)) {
+            if (n == 64) small_level_down<64>(D[j], F[j], sweeps, fr, sred);
+            else if (n == 32) small_level_down<32>(D[j], F[j], sweeps, fr, sred);
+            else if (n == 16) small_level_down<16>(D[j], F[j], sweeps, fr, sred);
+            else small_level_down<8>(D[j], F[j], sweeps, fr, sred);
+            continue;
+        }
+#endif
         for (int c = tid; c < nn; c += nt) D[j][c] = 0.0;
         __syncthreads();
         const double h = 2.0 * M_PI / n;
 #ifdef MGSR_EXACT_SMALL_MEANS
-        small_gs(D[j], F[j], n, h * h, j == L.nlev - 1 ? coarse_sweeps : n_smooth, sred);
+        small_gs(D[j], F[j], n, h * h, sweeps, sred);
 #else
-        small_gs_deferred(D[j], F[j], n, h * h, j == L.nlev - 1 ? coarse_sweeps : n_smooth, sred);
+        small_gs_deferred(D[j], F[j], n, h * h, sweeps, sred);
 #endif
-        if (j < L.nlev - 1) {   // residual at the injected points -> next RHS 0.5 (r - mean(r))
+        if (fr) {   // residual at the injected points -> next RHS 0.5 (r - mean(r))
             const int ncc = (n >> 1) * (n >> 1);
-            const double mean = small_residual_inject(D[j], F[j], n, F[j + 1], sred);
-            for (int t = tid; t < ncc; t += nt) F[j + 1][t] = (F[j + 1][t] - mean) * 0.5;
+            const double mean = small_residual_inject(D[j], F[j], n, fr, sred);
+            for (int t = tid; t < ncc; t += nt) fr[t] = (fr[t] - mean) * 0.5;
             __syncthreads();
         }
     }
-    for (int j = L.nlev - 2; j >= 0; --j) small_prolong2_add(D[j + 1], L.side[j + 1], D[j]);   // ascend
+    for (int j = L.nlev - 2; j >= 0; --j) {   // ascend
+        const int nc = L.side[j + 1];
+        if (nt == kSmallThreads && nc == 32) small_prolong2_add_t<32>(D[j + 1], D[j]);
+        else if (nt == kSmallThreads && nc == 16) small_prolong2_add_t<16>(D[j + 1], D[j]);
+        else if (nt == kSmallThreads && nc == 8) small_prolong2_add_t<8>(D[j + 1], D[j]);
+        else small_prolong2_add(D[j + 1], nc, D[j]);
+    }
 }
 
 // Whole small grid in one CTA: all sweeps with the reference's per-sweep mean subtraction done
@@ -387,7 +505,12 @@ __global__ void __launch_bounds__(kSmallThreads) k_vcycle_small(double *__restri
 //   * interior written with 16-byte stores; tiles of the last row/column are
 //     shifted inwards (x0 = n - TX) rather than masked: they recompute cells
 //     of their neighbour bit for bit and only count their own cells in the sums.
-constexpr int kRbW = 64, kRbRows = 8, kRbWarps = 8, kRbThreads = 32 * kRbWarps, kRbMinN = 128, kRbMaxK = 4;
+#ifndef MGSR_RB_ROWS
+#define MGSR_RB_ROWS 8
+#endif
+constexpr int kRbW = 64, kRbRows = MGSR_RB_ROWS, kRbWarps = kRbW / kRbRows, kRbThreads = 32 * kRbWarps, kRbMinN = 128,
+              kRbMaxK = 4;
+static_assert(kRbRows % 2 == 0 && kRbW % kRbRows == 0, "even rows per warp");
 
 __device__ __forceinline__ void rb_mbar_wait(uint32_t bar, uint32_t parity) {
     asm volatile(
@@ -1231,6 +1354,194 @@ __global__ void __launch_bounds__(256, 2) k_prolong_finalize_rows(
     }
 }
 
+// k_prolong_finalize_rows with its operands staged by the bulk-copy engine (same per-cell arithmetic, same
+// launch geometry, so bitwise identical results).  The register-prefetch form keeps one fine row of S, p, f
+// and one coarse row in flight per thread: ~28 KB per SM against the ~35 KB the HBM latency-bandwidth
+// product asks for, so it ran latency-bound at ~4.6 TB/s.  Here a CTA (512 fine columns of a row strip)
+// streams its rows through a ring of kPfNst shared-memory stages; stage k holds fine row g = r0 - 1 + k:
+// S over columns c_blk - 2 .. c_blk + 513 (the halo the edge lanes read), p and f over the CTA's 512
+// columns (rows r0 .. r1 - 1 only), and, when g is even, the coarse row (g >> 1) + 2 that slides into the
+// Keys window, over coarse columns bj_blk - 2 .. bj_blk + 257.  Thread 0 issues the copies (1-D
+// cp.async.bulk, one or two pieces per periodic segment) on a full mbarrier per stage; each warp releases a
+// stage on its empty mbarrier once it read it, and thread 0 refills the slot two iterations later, so
+// ~4 rows (~100 KB per SM at 2 CTAs) are in flight.
+constexpr int kPfCols = 512;                                 // fine columns per CTA (256 threads x 2)
+constexpr int kPfSegS = kPfCols + 4;                         // S: c_blk - 2 .. c_blk + 513
+constexpr int kPfSegC = kPfCols / 2 + 4;                     // coarse: bj_blk - 2 .. bj_blk + 257
+constexpr int kPfOffP = kPfSegS, kPfOffF = kPfOffP + kPfCols, kPfOffC = kPfOffF + kPfCols;
+constexpr int kPfStage = kPfOffC + kPfSegC;                  // 1800 doubles = 14400 B (16-B multiple)
+constexpr int kPfNst = 7;
+constexpr size_t kPfSmem = size_t(kPfStage) * kPfNst * 8 + 2 * kPfNst * 8;
+
+// [x0, x0 + len) of a periodic row of length n (len < n) -> shared memory, in one or two 16-B aligned pieces
+__device__ __forceinline__ void pf_seg(uint32_t dst, const double *row, int x0, int len, int n, uint32_t bar) {
+    if (x0 < 0) {
+        rb_bulk(dst, row + x0 + n, uint32_t(-x0 * 8), bar);
+        rb_bulk(dst + uint32_t(-x0 * 8), row, uint32_t((len + x0) * 8), bar);
+    } else if (x0 + len > n) {
+        rb_bulk(dst, row + x0, uint32_t((n - x0) * 8), bar);
+        rb_bulk(dst + uint32_t((n - x0) * 8), row, uint32_t((len - (n - x0)) * 8), bar);
+    } else {
+        rb_bulk(dst, row + x0, uint32_t(len * 8), bar);
+    }
+}
+
+__global__ void __launch_bounds__(256, 2) k_prolong_finalize_tma(
+    const double *__restrict__ S, const double *bshift, const double *__restrict__ c, int nc,
+    const double *out_mean, double *__restrict__ p, FSrc fs, double inv_h2, RedSlot slot, double *acc_out,
+    double *stats, int rows) {
+    extern __shared__ __align__(128) double pf_sm[];
+    uint64_t *const bars = reinterpret_cast<uint64_t *>(pf_sm + size_t(kPfStage) * kPfNst);   // full[kPfNst], empty[kPfNst]
+    const uint32_t sm0 = uint32_t(__cvta_generic_to_shared(pf_sm));
+    const uint32_t full0 = uint32_t(__cvta_generic_to_shared(bars)), empty0 = full0 + 8 * kPfNst;
+    const int n = 2 * nc;
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int bj = blockIdx.x * blockDim.x + tid;
+    const int c_blk = blockIdx.x * kPfCols, bj_blk = blockIdx.x * (kPfCols / 2);
+    const double bsh = *bshift, m = *out_mean;
+    const double sh = fs.load_shift();
+    const bool shifted = fs.shift != nullptr;
+    const int r0 = blockIdx.y * rows, r1 = min(r0 + rows, n);
+    const int R = r1 - r0;   // >= 1 by the launch geometry
+    const int nstages = R + 2;
+    auto grow = [&](int k) { return wrap(r0 - 1 + k, n); };
+    auto issue = [&](int k) {   // thread 0: stage k -> slot k % kPfNst
+        const int g = grow(k);
+        const bool pf = k >= 1 && k <= R, cr = k >= 1 && !(g & 1);
+        const uint32_t bytes = uint32_t(kPfSegS * 8) + (pf ? uint32_t(2 * kPfCols * 8) : 0u) +
+                               (cr ? uint32_t(kPfSegC * 8) : 0u);
+        const uint32_t bar = full0 + 8u * uint32_t(k % kPfNst);
+        const uint32_t dst = sm0 + uint32_t((k % kPfNst) * kPfStage * 8);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+        const int64_t ro = int64_t(g) * n;
+        pf_seg(dst, S + ro, c_blk - 2, kPfSegS, n, bar);
+        if (pf) {
+            rb_bulk(dst + kPfOffP * 8, p + ro + c_blk, kPfCols * 8, bar);
+            rb_bulk(dst + kPfOffF * 8, fs.f + ro + c_blk, kPfCols * 8, bar);
+        }
+        if (cr) pf_seg(dst + kPfOffC * 8, c + int64_t(wrap((g >> 1) + 2, nc)) * nc, bj_blk - 2, kPfSegC, nc, bar);
+    };
+    if (tid == 0) {
+        for (int s = 0; s < kPfNst; ++s) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(full0 + 8u * s) : "memory");
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(empty0 + 8u * s), "r"(blockDim.x / 32) : "memory");
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (tid == 0)
+        for (int k = 0; k < kPfNst && k < nstages; ++k) issue(k);
+    auto wait_full = [&](int k) { rb_mbar_wait(full0 + 8u * uint32_t(k % kPfNst), uint32_t((k / kPfNst) & 1)); };
+    auto release = [&](int k) {
+        __syncwarp();
+        if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(empty0 + 8u * uint32_t(k % kPfNst)) : "memory");
+    };
+    auto stage = [&](int k) { return pf_sm + (k % kPfNst) * kPfStage; };
+    double v[3] = {0.0, 0.0, 0.0};
+    const int t2 = 2 * tid;   // the thread's fine pair in the CTA's columns; coarse column tid
+    const bool edge = lane == 0 || lane == 31;
+    // extra coarse columns: lane 0 -> bj - 2, bj - 1; lane 31 -> bj + 1, bj + 2 (segment offsets)
+    const int oxa = lane == 0 ? tid : tid + 3, oxb = lane == 0 ? tid + 1 : tid + 4;
+    double w_0, w_1, w_2, w_3, a_0 = 0.0, a_1 = 0.0, a_2 = 0.0, a_3 = 0.0, b_0 = 0.0, b_1 = 0.0, b_2 = 0.0, b_3 = 0.0;
+    {
+        const int xa = lane == 0 ? wrap(bj - 2, nc) : wrap(bj + 1, nc), xb = lane == 0 ? wrap(bj - 1, nc) : wrap(bj + 2, nc);
+        const int a = grow(0) >> 1;
+#define PF_GLOAD(K, ROW)                                              \
+    {                                                                 \
+        const double *cr_ = c + int64_t(wrap((ROW), nc)) * nc;        \
+        w_##K = __ldg(cr_ + bj);                                      \
+        if (edge) {                                                   \
+            a_##K = __ldg(cr_ + xa);                                  \
+            b_##K = __ldg(cr_ + xb);                                  \
+        }                                                             \
+    }
+        PF_GLOAD(0, a - 1) PF_GLOAD(1, a) PF_GLOAD(2, a + 1) PF_GLOAD(3, a + 2)
+#undef PF_GLOAD
+    }
+    // the window slides one coarse row when stage k's fine row is even (its coarse row is in the stage)
+    auto slide = [&](int k) {
+        if (grow(k) & 1) return;
+        const double *cs = stage(k) + kPfOffC;
+        w_0 = w_1; w_1 = w_2; w_2 = w_3; w_3 = cs[tid + 2];
+        a_0 = a_1; a_1 = a_2; a_2 = a_3;
+        b_0 = b_1; b_1 = b_2; b_2 = b_3;
+        if (edge) { a_3 = cs[oxa]; b_3 = cs[oxb]; }
+    };
+    auto out_row = [&](int k, double2 &o, double &hl, double &hr) {
+        const double *ss = stage(k);
+        const bool odd = grow(k) & 1;
+        const double2 s2 = *reinterpret_cast<const double2 *>(ss + 2 + t2);
+        const double Ro = odd ? pf_vert(w_0, w_1, w_2, w_3) : w_1;
+        double Ra = 0.0, Rb = 0.0;
+        if (edge) {
+            Ra = odd ? pf_vert(a_0, a_1, a_2, a_3) : a_1;
+            Rb = odd ? pf_vert(b_0, b_1, b_2, b_3) : b_1;
+        }
+        const double up1 = __shfl_up_sync(0xffffffffu, Ro, 1);
+        const double dn1 = __shfl_down_sync(0xffffffffu, Ro, 1);
+        const double dn2 = __shfl_down_sync(0xffffffffu, Ro, 2);
+        const double l31a = __shfl_sync(0xffffffffu, Ra, 31);
+        const double Rm1 = lane == 0 ? Rb : up1;
+        const double Rp1 = lane == 31 ? Ra : dn1;
+        const double Rp2 = lane == 31 ? Rb : (lane == 30 ? l31a : dn2);
+        o.x = (s2.x - bsh) + Ro;
+        o.y = (s2.y - bsh) + pf_hint(Rm1, Ro, Rp1, Rp2);
+        hl = __shfl_up_sync(0xffffffffu, o.y, 1);
+        hr = __shfl_down_sync(0xffffffffu, o.x, 1);
+        if (lane == 0) hl = (ss[1 + t2] - bsh) + pf_hint(Ra, Rb, Ro, Rp1);
+        if (lane == 31) hr = (ss[4 + t2] - bsh) + Rp1;
+    };
+    double2 up, cur, dn;
+    double hl_c, hr_c, hl_d, hr_d, tl, tr;
+    wait_full(0);
+    out_row(0, up, tl, tr);
+    release(0);
+    wait_full(1);
+    slide(1);
+    out_row(1, cur, hl_c, hr_c);
+#pragma unroll 1
+    for (int k = 1; k <= R; ++k) {
+        if (tid == 0 && k >= 2 && k - 2 + kPfNst < nstages) {
+            const int kr = k - 2;   // released by every warp at the end of iteration k - 2 (stage 0: before the loop)
+            rb_mbar_wait(empty0 + 8u * uint32_t(kr % kPfNst), uint32_t((kr / kPfNst) & 1));
+            issue(kr + kPfNst);
+        }
+        wait_full(k + 1);
+        slide(k + 1);
+        out_row(k + 1, dn, hl_d, hr_d);
+        const double *st = stage(k);
+        const double2 pp = *reinterpret_cast<const double2 *>(st + kPfOffP + t2);
+        const double2 ff = *reinterpret_cast<const double2 *>(st + kPfOffF + t2);
+        release(k);
+        const double nb0 = ((up.x + dn.x) + hl_c) + cur.y;
+        const double nb1 = ((up.y + dn.y) + cur.x) + hr_c;
+        const double f0 = shifted ? (ff.x - sh) * fs.scale : ff.x;
+        const double f1 = shifted ? (ff.y - sh) * fs.scale : ff.y;
+        const double np0 = cur.x - m, np1 = cur.y - m;
+        const double d0 = np0 - pp.x, d1 = np1 - pp.y;
+        const double q0 = f0 - ((nb0 - 4.0 * cur.x) * inv_h2);
+        const double q1 = f1 - ((nb1 - 4.0 * cur.y) * inv_h2);
+        *reinterpret_cast<double2 *>(p + int64_t(grow(k)) * n + c_blk + t2) = make_double2(np0, np1);
+        v[0] += d0 * d0;
+        v[0] += d1 * d1;
+        v[1] += q0;
+        v[1] += q1;
+        v[2] += q0 * q0;
+        v[2] += q1 * q1;
+        up = cur;
+        cur = dn;
+        hl_c = hl_d;
+        hr_c = hr_d;
+    }
+    double *const outs[3] = {acc_out, acc_out + 1, acc_out + 2};
+    const double inv = 1.0 / (double(n) * double(n));
+    const double scales[3] = {inv, inv, inv};
+    if (grid_reduce_to<3>(v, slot, outs, scales)) {
+        stats[0] = sqrt(acc_out[0]);
+        const double var = acc_out[2] - acc_out[1] * acc_out[1];
+        stats[1] = sqrt(var > 0.0 ? var : 0.0);
+    }
+}
 
 __global__ void k_stats_sqrt(const double *acc, double *stats) {
     stats[0] = sqrt(acc[0]);
@@ -1493,7 +1804,21 @@ int launch_prolong_finalize(const double *S, const double *bshift, const double 
     const int rows = (n + strips - 1) / strips;
     const dim3 g(gx, (n + rows - 1) / rows);
     if (int64_t(g.x) * g.y > kRedMaxBlocks) { set_error("prolong_finalize grid too large"); return MGSR_E_UNSUPPORTED; }
-    k_prolong_finalize_rows<<<g, 256, 0, st>>>(S, bshift, c, nc, out_mean, p, fs, 1.0 / (h * h), sl, acc3, stats2, rows);
+    static const bool tma = std::getenv("MGSR_FUSED_TOP_TMA") != nullptr;   // A/B: the bulk-copy staged form
+    if (!tma) {
+        k_prolong_finalize_rows<<<g, 256, 0, st>>>(S, bshift, c, nc, out_mean, p, fs, 1.0 / (h * h), sl, acc3, stats2,
+                                                   rows);
+        MGSR_LAUNCH_CHECK();
+        return MGSR_OK;
+    }
+    static bool attr = false;
+    if (!attr) {
+        MGSR_CUDA_TRY(cudaFuncSetAttribute(k_prolong_finalize_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           int(kPfSmem)));
+        attr = true;
+    }
+    k_prolong_finalize_tma<<<g, 256, kPfSmem, st>>>(S, bshift, c, nc, out_mean, p, fs, 1.0 / (h * h), sl, acc3, stats2,
+                                                    rows);
     MGSR_LAUNCH_CHECK();
     return MGSR_OK;
 }
