@@ -13,6 +13,7 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <string>
 
 #include "common.cuh"
@@ -1354,6 +1355,145 @@ __global__ void __launch_bounds__(256, 2) k_prolong_finalize_rows(
     }
 }
 
+// k_prolong_finalize_rows restated two fine rows per iteration (same per-cell arithmetic and thread -> column
+// mapping).  ncu showed the row-at-a-time form issue-bound, not bandwidth-bound: ~300 warp instructions per
+// 64-cell warp row (parity selects, divergent edge-lane blocks with two extra coarse columns each, window
+// slides behind branches, per-row index arithmetic) at 4 warps per scheduler.  Here an iteration handles the
+// coarse row a of a strip that starts on an even fine row: the odd fine row 2a + 1 (vertical Keys weights over
+// coarse rows a - 1 .. a + 2) and the even fine row 2a + 2 (coarse row a + 1 itself), so row parity is
+// compile-time; every lane carries ONE extra coarse column (lane 0: bj0 - 1, lane 1: bj0 - 2, lane 31:
+// bj0 + 32, lane 30: bj0 + 33; other lanes a dummy), so the columns beyond the warp cost one uniform
+// vertical evaluation and an xor-1 shuffle instead of two divergent ones; the operands of the next
+// iteration (two rows of S, p, f, one coarse row: ~100 B per thread) are requested before this one computes.
+__device__ __forceinline__ void pf2_out_row(int lane, double Ro, double E, double2 s2, double sx, double bsh,
+                                            double2 &o, double &hl, double &hr) {
+    const double up1 = __shfl_up_sync(0xffffffffu, Ro, 1);
+    const double dn1 = __shfl_down_sync(0xffffffffu, Ro, 1);
+    const double dn2 = __shfl_down_sync(0xffffffffu, Ro, 2);
+    const double xe = __shfl_xor_sync(0xffffffffu, E, 1);
+    const double Rm1 = lane == 0 ? E : up1;       // coarse column bj - 1
+    const double Rp1 = lane == 31 ? E : dn1;      // bj + 1
+    const double Rp2 = lane >= 30 ? xe : dn2;     // bj + 2
+    o.x = (s2.x - bsh) + Ro;
+    o.y = (s2.y - bsh) + pf_hint(Rm1, Ro, Rp1, Rp2);
+    // the out values left of the warp (odd fine column of bj0 - 1) / right of it (even fine column of bj0 + 32)
+    const double t = pf_hint(xe, E, Ro, Rp1);
+    const double X = (sx - bsh) + (lane == 0 ? t : Rp1);
+    const double l = __shfl_up_sync(0xffffffffu, o.y, 1);
+    const double r = __shfl_down_sync(0xffffffffu, o.x, 1);
+    hl = lane == 0 ? X : l;
+    hr = lane == 31 ? X : r;
+}
+
+__device__ __forceinline__ void pf2_finalize(double2 up, double2 cur, double2 dn, double hl, double hr, double2 pp,
+                                             double2 ff, double m, double inv_h2, double *__restrict__ prow,
+                                             double (&v)[3]) {
+    const double nb0 = ((up.x + dn.x) + hl) + cur.y;
+    const double nb1 = ((up.y + dn.y) + cur.x) + hr;
+    const double np0 = cur.x - m, np1 = cur.y - m;
+    const double d0 = np0 - pp.x, d1 = np1 - pp.y;
+    const double q0 = ff.x - ((nb0 - 4.0 * cur.x) * inv_h2);
+    const double q1 = ff.y - ((nb1 - 4.0 * cur.y) * inv_h2);
+    *reinterpret_cast<double2 *>(prow) = make_double2(np0, np1);
+    v[0] += d0 * d0;
+    v[0] += d1 * d1;
+    v[1] += q0;
+    v[1] += q1;
+    v[2] += q0 * q0;
+    v[2] += q1 * q1;
+}
+
+// rows even (strips start on even fine rows), nc % 256 == 0, f unshifted
+__global__ void __launch_bounds__(256, 2) k_prolong_finalize_pairs(
+    const double *__restrict__ S, const double *bshift, const double *__restrict__ c, int nc,
+    const double *out_mean, double *__restrict__ p, const double *__restrict__ f, double inv_h2, RedSlot slot,
+    double *acc_out, double *stats, int rows) {
+    const int n = 2 * nc;
+    const int lane = threadIdx.x & 31;
+    const int bj = blockIdx.x * blockDim.x + threadIdx.x;
+    const int c0 = 2 * bj;
+    const double bsh = *bshift, m = *out_mean;
+    const int r0 = blockIdx.y * rows, r1 = min(r0 + rows, n);
+    double v[3] = {0.0, 0.0, 0.0};
+    if (r0 < r1) {
+        const bool edge = lane <= 1 || lane >= 30;
+        const bool sedge = lane == 0 || lane == 31;
+        const int xcol = wrap(bj + (lane == 0 ? -1 : (lane == 1 ? -3 : (lane == 30 ? 3 : 1))), nc);
+        const int scol = lane == 0 ? (c0 == 0 ? n - 1 : c0 - 1) : (c0 + 2 >= n ? c0 + 2 - n : c0 + 2);
+        const int a0 = r0 >> 1, a1 = r1 >> 1;   // coarse rows of the strip: a0 .. a1 - 1
+        auto ld_c = [&](int row, double &w, double &e) {
+            const double *cr = c + int64_t(wrap(row, nc)) * nc;
+            w = __ldg(cr + bj);
+            e = 0.0;
+            if (edge) e = __ldg(cr + xcol);
+        };
+        auto ld_s = [&](int row, double2 &s2, double &sx) {   // row already in [0, n)
+            const double *sr = S + int64_t(row) * n;
+            s2 = __ldg(reinterpret_cast<const double2 *>(sr + c0));
+            sx = 0.0;
+            if (sedge) sx = __ldg(sr + scol);
+        };
+        double w0, w1, w2, w3, e0, e1, e2, e3;
+        double2 up, cur, dn, dn2;
+        double hl_c, hr_c, hl_d, hr_d, hl_e, hr_e;
+        {
+            // out rows r0 - 1 (odd row of coarse row a0 - 1: window a0 - 2 .. a0 + 1) and r0 (coarse row a0)
+            double wm, em, sx;
+            double2 s2;
+            ld_c(a0 - 2, wm, em);
+            ld_c(a0 - 1, w0, e0);
+            ld_c(a0, w1, e1);
+            ld_c(a0 + 1, w2, e2);
+            ld_c(a0 + 2, w3, e3);
+            ld_s(r0 == 0 ? n - 1 : r0 - 1, s2, sx);
+            pf2_out_row(lane, pf_vert(wm, w0, w1, w2), pf_vert(em, e0, e1, e2), s2, sx, bsh, up, hl_c, hr_c);
+            ld_s(r0, s2, sx);
+            pf2_out_row(lane, w1, e1, s2, sx, bsh, cur, hl_c, hr_c);
+        }
+        // operands of iteration a: S rows 2a + 1, 2a + 2 (the last one of the grid wraps to row 0), p and f rows
+        // 2a, 2a + 1, coarse row a + 3
+        double2 nS1, nS2, nP0, nP1, nF0, nF1;
+        double nX1, nX2, nCw, nCe;
+        auto prefetch = [&](int a) {
+            const int i = 2 * a;
+            ld_s(i + 1, nS1, nX1);
+            ld_s(i + 2 >= n ? 0 : i + 2, nS2, nX2);
+            const int64_t o = int64_t(i) * n + c0;
+            nP0 = *reinterpret_cast<const double2 *>(p + o);
+            nP1 = *reinterpret_cast<const double2 *>(p + o + n);
+            nF0 = __ldg(reinterpret_cast<const double2 *>(f + o));
+            nF1 = __ldg(reinterpret_cast<const double2 *>(f + o + n));
+            ld_c(a + 3, nCw, nCe);
+        };
+        prefetch(a0);
+#pragma unroll 1
+        for (int a = a0; a < a1; ++a) {
+            const double2 s1 = nS1, s2 = nS2, p0 = nP0, p1 = nP1, f0 = nF0, f1 = nF1;
+            const double x1 = nX1, x2 = nX2, cw = nCw, ce = nCe;
+            if (a + 1 < a1) prefetch(a + 1);
+            double *const prow = p + int64_t(2 * a) * n + c0;
+            pf2_out_row(lane, pf_vert(w0, w1, w2, w3), pf_vert(e0, e1, e2, e3), s1, x1, bsh, dn, hl_d, hr_d);
+            pf2_finalize(up, cur, dn, hl_c, hr_c, p0, f0, m, inv_h2, prow, v);
+            pf2_out_row(lane, w2, e2, s2, x2, bsh, dn2, hl_e, hr_e);
+            pf2_finalize(cur, dn, dn2, hl_d, hr_d, p1, f1, m, inv_h2, prow + n, v);
+            up = dn;
+            cur = dn2;
+            hl_c = hl_e;
+            hr_c = hr_e;
+            w0 = w1; w1 = w2; w2 = w3; w3 = cw;
+            e0 = e1; e1 = e2; e2 = e3; e3 = ce;
+        }
+    }
+    double *const outs[3] = {acc_out, acc_out + 1, acc_out + 2};
+    const double inv = 1.0 / (double(n) * double(n));
+    const double scales[3] = {inv, inv, inv};
+    if (grid_reduce_to<3>(v, slot, outs, scales)) {
+        stats[0] = sqrt(acc_out[0]);
+        const double var = acc_out[2] - acc_out[1] * acc_out[1];
+        stats[1] = sqrt(var > 0.0 ? var : 0.0);
+    }
+}
+
 // k_prolong_finalize_rows with its operands staged by the bulk-copy engine (same per-cell arithmetic, same
 // launch geometry, so bitwise identical results).  The register-prefetch form keeps one fine row of S, p, f
 // and one coarse row in flight per thread: ~28 KB per SM against the ~35 KB the HBM latency-bandwidth
@@ -1801,10 +1941,18 @@ int launch_prolong_finalize(const double *S, const double *bshift, const double 
     const int gx = nc / 256;
     int strips = (2 * num_sms()) / gx;   // one wave at 2 CTAs per SM
     strips = strips < 1 ? 1 : (strips > n ? n : strips);
-    const int rows = (n + strips - 1) / strips;
+    const int rows = (((n + strips - 1) / strips) + 1) & ~1;   // even: the strips start on even fine rows
     const dim3 g(gx, (n + rows - 1) / rows);
     if (int64_t(g.x) * g.y > kRedMaxBlocks) { set_error("prolong_finalize grid too large"); return MGSR_E_UNSUPPORTED; }
-    static const bool tma = std::getenv("MGSR_FUSED_TOP_TMA") != nullptr;   // A/B: the bulk-copy staged form
+    // A/B: MGSR_FUSED_TOP=rows (one fine row per iteration) | tma (the bulk-copy staged form); default: row pairs
+    static const char *variant = std::getenv("MGSR_FUSED_TOP");
+    static const bool tma = variant && !std::strcmp(variant, "tma"), by_rows = variant && !std::strcmp(variant, "rows");
+    if (!tma && !by_rows && fs.shift == nullptr) {
+        k_prolong_finalize_pairs<<<g, 256, 0, st>>>(S, bshift, c, nc, out_mean, p, fs.f, 1.0 / (h * h), sl, acc3,
+                                                    stats2, rows);
+        MGSR_LAUNCH_CHECK();
+        return MGSR_OK;
+    }
     if (!tma) {
         k_prolong_finalize_rows<<<g, 256, 0, st>>>(S, bshift, c, nc, out_mean, p, fs, 1.0 / (h * h), sl, acc3, stats2,
                                                    rows);
