@@ -15,6 +15,9 @@ struct mgsr_gen {
     float *post_w = nullptr, *post_s = nullptr, *post_b = nullptr;
     float *up_w = nullptr, *up_a = nullptr;  // 256x64x3x3, 64
     float *tail_w = nullptr, *tail_b = nullptr;  // 3x64x9x9, 3
+    // the same conv weights as [C][taps][O] (tail: O padded to 4) for the row-tiled fp32 kernels
+    float *head_t = nullptr, *post_t = nullptr, *up_t = nullptr, *tail_t = nullptr;
+    std::vector<float *> c1_t, c2_t;
     // tensor-core path: packed weights / constants (one device blob), see generator_tc.cu
     void *tc_blob = nullptr;
     size_t tc_bytes = 0;

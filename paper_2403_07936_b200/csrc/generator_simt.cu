@@ -199,6 +199,311 @@ __global__ void __launch_bounds__(kConv2Threads) k_conv_rt(const float *__restri
     }
 }
 
+// Row-tiled form for the window sides the SR passes use (H = 6 and 12) and 64-wide output blocks:
+// thread = one 6-pixel row segment of one window x 8 output channels (48 accumulators).  Per input
+// channel and kernel row it reads <= 12 staged inputs and K x 8 weights for K x 48 FMAs (~0.22 shared-
+// memory words per FMA; k_conv_rt's one pixel x 16 channels needed 1.06 and was LSU-bound).
+//   * The input planes are staged RAW (a window's cc channels are contiguous in (N, C, H, H): straight
+//     16-byte copies, no index arithmetic); the replicate padding is resolved when a row is read: the
+//     clamped row index per dy, and a compile-time column map per segment (rows_load).
+//   * Weights come pre-transposed ([c][tap][O], mgsr_gen::*_t): staging is 16-byte copies and a warp's
+//     weight read is one conflict-free 128-byte line.
+//   * The epilogue goes through shared memory: every value is placed at its offset inside the CTA's
+//     contiguous output block (64 channels x H x H per window; for the pixel shuffle 16 planes of
+//     2H x 2H), then the block is written (and the residual read) with coalesced 16-byte accesses.
+// Per output the accumulation order is unchanged (c ascending, dy, dx, fmaf) and so are the epilogue
+// expressions: bitwise identical to k_conv_simt / k_conv_rt.
+constexpr int kRowThreads = 192;
+#ifndef MGSR_ROW_CC
+#define MGSR_ROW_CC 8
+#endif
+template <int K> struct RowCfg { static constexpr int CC = K == 3 ? MGSR_ROW_CC : 1; };   // C must be a multiple
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(uint32_t(__cvta_generic_to_shared(smem))), "l"(gmem)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+// v[j] = row[clamp(6 * SEG + j - P, 0, H - 1)], j < K + 5, from the fewest aligned vector loads
+template <int K, int H, int SEG>
+__device__ __forceinline__ void rows_load(const float *row, float (&v)[K + 5]) {
+    constexpr int P = K / 2;
+    constexpr int BASE = (H == 12 && K == 3) ? 4 * SEG : 0;
+    constexpr int L = H == 6 ? 6 : (K == 3 ? 8 : 12);
+    float b[L];
+    if constexpr (H == 6) {
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            const float2 t = *reinterpret_cast<const float2 *>(row + 2 * j);
+            b[2 * j] = t.x;
+            b[2 * j + 1] = t.y;
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < L / 4; ++j) {
+            const float4 t = *reinterpret_cast<const float4 *>(row + BASE + 4 * j);
+            b[4 * j] = t.x;
+            b[4 * j + 1] = t.y;
+            b[4 * j + 2] = t.z;
+            b[4 * j + 3] = t.w;
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < K + 5; ++j) {
+        int col = 6 * SEG + j - P;
+        col = col < 0 ? 0 : (col > H - 1 ? H - 1 : col);
+        v[j] = b[col - BASE];
+    }
+}
+
+template <int K, int H, int SEG>
+__device__ __forceinline__ void rows_chunk(const float *s_win, const float *sw, int cc, int y, float (&acc)[6][8]) {
+    constexpr int P = K / 2, HW = H * H;
+    int yo[K];
+#pragma unroll
+    for (int dy = 0; dy < K; ++dy) yo[dy] = min(max(y + dy - P, 0), H - 1) * H;
+    for (int c = 0; c < cc; ++c) {
+        const float *si = s_win + c * HW;
+#pragma unroll
+        for (int dy = 0; dy < K; ++dy) {
+            float v[K + 5];
+            rows_load<K, H, SEG>(si + yo[dy], v);
+#pragma unroll
+            for (int dx = 0; dx < K; ++dx) {
+                const float4 wa = *reinterpret_cast<const float4 *>(sw + ((c * K + dy) * K + dx) * 64);
+                const float4 wb = *reinterpret_cast<const float4 *>(sw + ((c * K + dy) * K + dx) * 64 + 32);
+#pragma unroll
+                for (int i = 0; i < 6; ++i) {
+                    const float a = v[i + dx];
+                    acc[i][0] = fmaf(a, wa.x, acc[i][0]);
+                    acc[i][1] = fmaf(a, wa.y, acc[i][1]);
+                    acc[i][2] = fmaf(a, wa.z, acc[i][2]);
+                    acc[i][3] = fmaf(a, wa.w, acc[i][3]);
+                    acc[i][4] = fmaf(a, wb.x, acc[i][4]);
+                    acc[i][5] = fmaf(a, wb.y, acc[i][5]);
+                    acc[i][6] = fmaf(a, wb.z, acc[i][6]);
+                    acc[i][7] = fmaf(a, wb.w, acc[i][7]);
+                }
+            }
+        }
+    }
+}
+
+template <int K, int OP, int H>
+__global__ void __maxnreg__(112) k_conv_rows(const float *__restrict__ in, int N, int C,
+                                                              const float *__restrict__ wt, int O,
+                                                              float *__restrict__ out, Epi ep) {
+    extern __shared__ __align__(16) float smr[];
+    constexpr int KK = K * K, CC = RowCfg<K>::CC, HW = H * H, NSEG = H / 6;
+    constexpr int NW = kRowThreads / 8 / (H * NSEG);   // windows per CTA: 4 (H = 6), 1 (H = 12)
+    constexpr int RPS = NW * H;                        // row slots per segment (a multiple of 4: warp-uniform SEG)
+    constexpr int STAGE = CC * KK * 64 + NW * CC * HW;   // floats per stage: weights [cc][KK][64] + raw planes [NW][cc][H][H]
+    const int tid = threadIdx.x, o8 = tid & 7, rs = tid >> 3;
+    const int seg = rs / RPS, r2 = rs - seg * RPS, wl = r2 / H, y = r2 - wl * H, x0 = 6 * seg;
+    const int n0 = blockIdx.x * NW, ob = blockIdx.y * 64;
+    const bool act = n0 + wl < N;
+    float acc[6][8];
+#pragma unroll
+    for (int i = 0; i < 6; ++i)
+#pragma unroll
+        for (int o = 0; o < 8; ++o) acc[i][o] = 0.f;
+    // chunk c0 of the input channels -> stage buffer `st` (asynchronous 16-byte copies; windows past N are skipped:
+    // their threads never compute)
+    // The address arithmetic is hoisted: a thread's weight pieces sit (tid & 15) + 16 * ((tid >> 4) + 12 j) apart,
+    // its plane pieces are window-contiguous.
+    const float4 *w_src = reinterpret_cast<const float4 *>(wt) + ob / 4 + (tid & 15) + int64_t(tid >> 4) * (O / 4);
+    const int w_step = 12 * (O / 4);
+    auto stage = [&](int c0, int st) {
+        float *s_w = smr + st * STAGE, *s_in = s_w + CC * KK * 64;
+        constexpr int per = CC * HW / 4;   // 16-byte pieces per window (HW is a multiple of 4)
+#pragma unroll
+        for (int j = 0; j < (NW * per + kRowThreads - 1) / kRowThreads; ++j) {
+            const int idx = tid + j * kRowThreads;
+            const int wi = idx / per, k = idx - wi * per, n = n0 + wi;
+            if (idx < NW * per && n < N)
+                cp_async16(reinterpret_cast<float4 *>(s_in) + idx,
+                           reinterpret_cast<const float4 *>(in + (int64_t(n) * C + c0) * HW) + k);
+        }
+        const float4 *src = w_src + int64_t(c0) * KK * (O / 4);
+#pragma unroll
+        for (int j = 0; j < (CC * KK * 16 + kRowThreads - 1) / kRowThreads; ++j) {
+            const int idx = tid + j * kRowThreads;
+            if (idx < CC * KK * 16) cp_async16(reinterpret_cast<float4 *>(s_w) + idx, src + j * w_step);
+        }
+        cp_async_commit();
+    };
+    stage(0, 0);
+    int st = 0;
+    for (int c0 = 0; c0 < C; c0 += CC, st ^= 1) {
+        constexpr int cc = CC;
+        cp_async_wait_all();
+        __syncthreads();   // chunk c0 landed for every thread; everyone is done with the other buffer
+        if (c0 + CC < C) stage(c0 + CC, st ^ 1);
+        if (act) {
+            const float *s_w = smr + st * STAGE, *s_win = s_w + CC * KK * 64 + wl * cc * HW;
+            if (NSEG == 1 || seg == 0) rows_chunk<K, H, 0>(s_win, s_w + o8 * 4, cc, y, acc);
+            else rows_chunk<K, H, NSEG - 1>(s_win, s_w + o8 * 4, cc, y, acc);
+        }
+    }
+    // epilogue through shared memory: tile[w][offset inside the window's contiguous output block]
+    __syncthreads();
+    float *tile = smr;
+    if (act) {
+#pragma unroll
+        for (int oo = 0; oo < 8; ++oo) {
+            const int ol = (oo >> 2) * 32 + o8 * 4 + (oo & 3), o = ob + ol;
+            float sc = 1.f, sh = 0.f, al = 0.f;
+            if (OP == OP_BN_PRELU || OP == OP_BN_RES) { sc = ep.scale[o]; sh = ep.shift[o]; }
+            if (OP == OP_PRELU || OP == OP_BN_PRELU) al = ep.alpha[o];
+            if (OP == OP_SHUF_PRELU) al = ep.alpha[o >> 2];
+#pragma unroll
+            for (int i = 0; i < 6; ++i) {
+                const int x = x0 + i;
+                float v = acc[i][oo];
+                int off;
+                if (OP == OP_SHUF_PRELU) {
+                    v = v > 0.f ? v : al * v;
+                    off = (ol >> 2) * 4 * HW + (2 * y + ((ol >> 1) & 1)) * 2 * H + 2 * x + (ol & 1);
+                } else {
+                    if (OP != OP_PRELU) v = fmaf(v, sc, sh);
+                    if (OP != OP_BN_RES) v = v > 0.f ? v : al * v;
+                    off = ol * HW + y * H + x;
+                }
+                tile[wl * 64 * HW + off] = v;
+            }
+        }
+    }
+    {
+        // non-shuffle: channels ob .. ob + 63 of (N, O, H, H); shuffle: planes ob/4 .. ob/4 + 15 of (N, O/4, 2H, 2H):
+        // either way the window's block starts at (n O + ob) H H.  The residual is requested before the barrier.
+        constexpr int per = 16 * HW, NP = NW * per / kRowThreads;   // 16-byte pieces per window block / per thread
+        static_assert(NW * per % kRowThreads == 0, "whole pieces per thread");
+        float4 r[OP == OP_BN_RES ? NP : 1];
+        if (OP == OP_BN_RES) {
+#pragma unroll
+            for (int j = 0; j < NP; ++j) {
+                const int idx = tid + j * kRowThreads, wi = idx / per, k = idx - wi * per, n = n0 + wi;
+                if (n < N) r[j] = *(reinterpret_cast<const float4 *>(ep.res + (int64_t(n) * O + ob) * HW) + k);
+            }
+        }
+        __syncthreads();
+        const float4 *t4 = reinterpret_cast<const float4 *>(tile);
+#pragma unroll
+        for (int j = 0; j < NP; ++j) {
+            const int idx = tid + j * kRowThreads, wi = idx / per, k = idx - wi * per, n = n0 + wi;
+            if (n >= N) break;
+            float4 t = t4[idx];
+            if (OP == OP_BN_RES) {
+                t.x = r[j].x + t.x;
+                t.y = r[j].y + t.y;
+                t.z = r[j].z + t.z;
+                t.w = r[j].w + t.w;
+            }
+            *(reinterpret_cast<float4 *>(out + (int64_t(n) * O + ob) * HW) + k) = t;
+        }
+    }
+}
+
+// The 9x9 64 -> 3 tail on 12- or 24-wide images: thread = one 12-pixel row segment x the 3 outputs
+// (36 accumulators); per input channel and kernel row 12 or 16 staged inputs (raw planes, replicate
+// padding resolved by the compile-time column map) and 9 x 4 weights ([c][tap][4], one broadcast float4
+// per tap) for 324 FMAs.  Same accumulation order and epilogue expression as the other forms.
+constexpr int kTailCC = 2;
+
+template <int H, int SEG>
+__device__ __forceinline__ void tail_chunk(const float *s_win, const float4 *sw, int cc, int y, float (&acc)[12][3]) {
+    constexpr int K = 9, P = 4, HW = H * H;
+    constexpr int BASE = H == 12 ? 0 : 8 * SEG, L = H == 12 ? 12 : 16;
+    for (int c = 0; c < cc; ++c) {
+        const float *si = s_win + c * HW;
+#pragma unroll 3
+        for (int dy = 0; dy < K; ++dy) {
+            float b[L], v[20];
+            const int yo = min(max(y + dy - P, 0), H - 1) * H;
+#pragma unroll
+            for (int j = 0; j < L / 4; ++j) {
+                const float4 t = *reinterpret_cast<const float4 *>(si + yo + BASE + 4 * j);
+                b[4 * j] = t.x;
+                b[4 * j + 1] = t.y;
+                b[4 * j + 2] = t.z;
+                b[4 * j + 3] = t.w;
+            }
+#pragma unroll
+            for (int j = 0; j < 20; ++j) {
+                int col = 12 * SEG + j - P;
+                col = col < 0 ? 0 : (col > H - 1 ? H - 1 : col);
+                v[j] = b[col - BASE];
+            }
+#pragma unroll
+            for (int dx = 0; dx < K; ++dx) {
+                const float4 w4 = sw[(c * K + dy) * K + dx];
+#pragma unroll
+                for (int i = 0; i < 12; ++i) {
+                    acc[i][0] = fmaf(v[i + dx], w4.x, acc[i][0]);
+                    acc[i][1] = fmaf(v[i + dx], w4.y, acc[i][1]);
+                    acc[i][2] = fmaf(v[i + dx], w4.z, acc[i][2]);
+                }
+            }
+        }
+    }
+}
+
+template <int H>
+__global__ void __maxnreg__(112) k_conv_tail_rows(const float *__restrict__ in, int N, int C,
+                                                                   const float *__restrict__ wt,
+                                                                   float *__restrict__ out, Epi ep) {
+    extern __shared__ __align__(16) float smr[];
+    constexpr int KK = 81, HW = H * H, NSEG = H / 12, NW = kRowThreads / (H * NSEG), RPS = NW * H;
+    constexpr int STAGE = kTailCC * KK * 4 + NW * kTailCC * HW;   // weights [cc][81][4] + raw planes [NW][cc][H][H]
+    const int tid = threadIdx.x;
+    const int seg = tid / RPS, r2 = tid - seg * RPS, wl = r2 / H, y = r2 - wl * H, x0 = 12 * seg;
+    const int n0 = blockIdx.x * NW;
+    const bool act = n0 + wl < N;
+    float acc[12][3];
+#pragma unroll
+    for (int i = 0; i < 12; ++i) acc[i][0] = acc[i][1] = acc[i][2] = 0.f;
+    auto stage = [&](int c0, int st) {
+        const int cc = min(kTailCC, C - c0);
+        float *s_w = smr + st * STAGE, *s_in = s_w + kTailCC * KK * 4;
+        const int per = cc * HW / 4;
+        for (int idx = tid; idx < NW * per; idx += kRowThreads) {
+            const int wi = idx / per, k = idx - wi * per, n = n0 + wi;
+            if (n < N) cp_async16(reinterpret_cast<float4 *>(s_in) + idx,
+                                  reinterpret_cast<const float4 *>(in + (int64_t(n) * C + c0) * HW) + k);
+        }
+        for (int idx = tid; idx < cc * KK; idx += kRowThreads)
+            cp_async16(reinterpret_cast<float4 *>(s_w) + idx, reinterpret_cast<const float4 *>(wt) + int64_t(c0) * KK + idx);
+        cp_async_commit();
+    };
+    stage(0, 0);
+    int st = 0;
+    for (int c0 = 0; c0 < C; c0 += kTailCC, st ^= 1) {
+        const int cc = min(kTailCC, C - c0);
+        cp_async_wait_all();
+        __syncthreads();
+        if (c0 + kTailCC < C) stage(c0 + kTailCC, st ^ 1);
+        if (act) {
+            const float *s_w = smr + st * STAGE, *s_win = s_w + kTailCC * KK * 4 + wl * cc * HW;
+            const float4 *sw = reinterpret_cast<const float4 *>(s_w);
+            if (NSEG == 1 || seg == 0) tail_chunk<H, 0>(s_win, sw, cc, y, acc);
+            else tail_chunk<H, NSEG - 1>(s_win, sw, cc, y, acc);
+        }
+    }
+    if (!act) return;
+    const int n = n0 + wl;
+    const float sc = ep.tanh_s;
+#pragma unroll
+    for (int o = 0; o < 3; ++o) {
+        float4 *dst = reinterpret_cast<float4 *>(out + (int64_t(n) * 3 + o) * HW + y * H + x0);
+#pragma unroll
+        for (int q = 0; q < 3; ++q)
+            dst[q] = make_float4(sc * tanhf((acc[4 * q][o] + ep.bias[o]) / sc), sc * tanhf((acc[4 * q + 1][o] + ep.bias[o]) / sc),
+                                 sc * tanhf((acc[4 * q + 2][o] + ep.bias[o]) / sc), sc * tanhf((acc[4 * q + 3][o] + ep.bias[o]) / sc));
+    }
+}
+
 // Direct form for large images (generator_forward on sides whose per-CTA tiles exceed shared memory):
 // one thread per output value, replicate-clamped taps read through the read-only cache, the same
 // accumulation order (c ascending, dy, dx, fmaf) and epilogues as k_conv_simt.
@@ -243,8 +548,37 @@ __global__ void __launch_bounds__(256) k_conv_direct(const float *__restrict__ i
 }
 
 template <int K, int OP>
-static int conv(const float *in, int N, int C, int H, const float *w, int O, float *out, const Epi &ep,
-                cudaStream_t st) {
+static int conv(const float *in, int N, int C, int H, const float *w, const float *wt, int O, float *out,
+                const Epi &ep, cudaStream_t st) {
+    if constexpr (OP == OP_TAIL) {
+        if (wt && K == 9 && O == 3 && (H == 12 || H == 24)) {
+            auto go = [&](auto kern, int nw) {
+                const size_t smem = 2 * sizeof(float) * (size_t(kTailCC) * 81 * 4 + size_t(nw) * kTailCC * H * H);
+                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+                kern<<<(N + nw - 1) / nw, kRowThreads, smem, st>>>(in, N, C, wt, out, ep);
+            };
+            if (H == 12) go(k_conv_tail_rows<12>, kRowThreads / 12);
+            else go(k_conv_tail_rows<24>, kRowThreads / 48);
+            MGSR_LAUNCH_CHECK();
+            return MGSR_OK;
+        }
+    } else {
+        if (wt && O % 64 == 0 && C % RowCfg<K>::CC == 0 && (H == 6 || H == 12)) {
+            constexpr int CC = RowCfg<K>::CC;
+            auto go = [&](auto kern, int nw) {
+                // main loop: two stages of (weights + raw planes of a chunk); epilogue: the 64-channel output blocks
+                size_t smem = 2 * sizeof(float) * (size_t(CC) * K * K * 64 + size_t(nw) * CC * H * H);
+                const size_t epi = sizeof(float) * size_t(nw) * 64 * H * H;
+                if (epi > smem) smem = epi;
+                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+                kern<<<dim3((N + nw - 1) / nw, O / 64), kRowThreads, smem, st>>>(in, N, C, wt, O, out, ep);
+            };
+            if (H == 6) go(k_conv_rows<K, OP, 6>, kRowThreads / 8 / 6);
+            else go(k_conv_rows<K, OP, 12>, kRowThreads / 8 / 24);
+            MGSR_LAUNCH_CHECK();
+            return MGSR_OK;
+        }
+    }
     {
         const int HW = H * H, HP = H + K - 1;
         const int nw = HW <= kConv2Threads ? kConv2Threads / HW : 1;
@@ -301,20 +635,20 @@ static int gen_forward_f32(const mgsr_gen *g, const float *x, int N, int H, floa
     Epi ep{};
     int r;
     ep.alpha = g->head_a;
-    if ((r = conv<9, OP_PRELU>(x, N, 3, H, g->head_w, 64, S, ep, st))) return r;
+    if ((r = conv<9, OP_PRELU>(x, N, 3, H, g->head_w, g->head_t, 64, S, ep, st))) return r;
     MGSR_CUDA_TRY(cudaMemcpyAsync(Y, S, sizeof(float) * t64, cudaMemcpyDeviceToDevice, st));
     for (int b = 0; b < g->blocks; ++b) {
         Epi e1{g->bn1s[b], g->bn1b[b], g->pa[b], nullptr, nullptr, 1.f};
-        if ((r = conv<3, OP_BN_PRELU>(Y, N, 64, H, g->c1[b], 64, Z, e1, st))) return r;
+        if ((r = conv<3, OP_BN_PRELU>(Y, N, 64, H, g->c1[b], g->c1_t[b], 64, Z, e1, st))) return r;
         Epi e2{g->bn2s[b], g->bn2b[b], nullptr, nullptr, Y, 1.f};
-        if ((r = conv<3, OP_BN_RES>(Z, N, 64, H, g->c2[b], 64, Y, e2, st))) return r;
+        if ((r = conv<3, OP_BN_RES>(Z, N, 64, H, g->c2[b], g->c2_t[b], 64, Y, e2, st))) return r;
     }
     Epi ep_post{g->post_s, g->post_b, nullptr, nullptr, S, 1.f};
-    if ((r = conv<3, OP_BN_RES>(Y, N, 64, H, g->post_w, 64, Z, ep_post, st))) return r;
+    if ((r = conv<3, OP_BN_RES>(Y, N, 64, H, g->post_w, g->post_t, 64, Z, ep_post, st))) return r;
     Epi ep_up{nullptr, nullptr, g->up_a, nullptr, nullptr, 1.f};
-    if ((r = conv<3, OP_SHUF_PRELU>(Z, N, 64, H, g->up_w, 256, U, ep_up, st))) return r;
+    if ((r = conv<3, OP_SHUF_PRELU>(Z, N, 64, H, g->up_w, g->up_t, 256, U, ep_up, st))) return r;
     Epi ep_t{nullptr, nullptr, nullptr, g->tail_b, nullptr, float(g->tanh_scale)};
-    return conv<9, OP_TAIL>(U, N, 64, 2 * H, g->tail_w, 3, y, ep_t, st);
+    return conv<9, OP_TAIL>(U, N, 64, 2 * H, g->tail_w, g->tail_t, 3, y, ep_t, st);
 }
 
 // ---------------------------------------------------------------------------
@@ -404,7 +738,9 @@ __global__ void k_f32_to_f64(const float *__restrict__ a, double *__restrict__ b
         b[t] = double(a[t]);
 }
 
-constexpr int kSrChunk = 4096;   // windows per fp32 chunk
+// windows per fp32 chunk: a multiple of 444 x 4 (148 SMs x 3 resident CTAs of the row-tiled kernels x 4 windows
+// per CTA at side 6), so a full chunk's launches are whole waves
+constexpr int kSrChunk = 3552;
 
 static size_t pass_ws_floats(int apps) {
     // input X (3*36) + generator scratch for the largest application + outputs
@@ -544,6 +880,15 @@ int upload(mgsr_gen *g, const float *host, size_t count, float **dst) {
     return MGSR_OK;
 }
 
+// OIHW weights -> [C][taps][Opad] for the row-tiled kernels (zero-filled pad channels)
+int upload_transposed(mgsr_gen *g, const float *host, int O, int C, int KK, int Opad, float **dst) {
+    std::vector<float> t(size_t(C) * KK * Opad, 0.f);
+    for (int o = 0; o < O; ++o)
+        for (int c = 0; c < C; ++c)
+            for (int k = 0; k < KK; ++k) t[(size_t(c) * KK + k) * Opad + o] = host[(size_t(o) * C + c) * KK + k];
+    return upload(g, t.data(), t.size(), dst);
+}
+
 // BN(x) = gamma (x - mean)/sqrt(var + 1e-5) + beta  ->  x*scale + shift (srmodel.py:313-318)
 int upload_bn(mgsr_gen *g, const float *gamma, const float *beta, const float *mean, const float *var, float **s,
               float **b) {
@@ -571,24 +916,31 @@ extern "C" int mgsr_generator_create(const float *const *t, int32_t num_tensors,
     g->tanh_scale = tanh_scale;
     int i = 0, r = 0;
 #define UP(cnt, dst) if ((r = upload(g, t[i++], (cnt), (dst)))) goto fail;
+    if ((r = upload_transposed(g, t[i], 64, 3, 81, 64, &g->head_t))) goto fail;
     UP(64 * 3 * 81, &g->head_w);
     UP(64, &g->head_a);
     g->c1.resize(blocks); g->c2.resize(blocks); g->bn1s.resize(blocks); g->bn1b.resize(blocks);
     g->bn2s.resize(blocks); g->bn2b.resize(blocks); g->pa.resize(blocks);
+    g->c1_t.resize(blocks); g->c2_t.resize(blocks);
     for (int b = 0; b < blocks; ++b) {
+        if ((r = upload_transposed(g, t[i], 64, 64, 9, 64, &g->c1_t[b]))) goto fail;
         UP(64 * 64 * 9, &g->c1[b]);
         if ((r = upload_bn(g, t[i], t[i + 1], t[i + 2], t[i + 3], &g->bn1s[b], &g->bn1b[b]))) goto fail;
         i += 4;
         UP(64, &g->pa[b]);
+        if ((r = upload_transposed(g, t[i], 64, 64, 9, 64, &g->c2_t[b]))) goto fail;
         UP(64 * 64 * 9, &g->c2[b]);
         if ((r = upload_bn(g, t[i], t[i + 1], t[i + 2], t[i + 3], &g->bn2s[b], &g->bn2b[b]))) goto fail;
         i += 4;
     }
+    if ((r = upload_transposed(g, t[i], 64, 64, 9, 64, &g->post_t))) goto fail;
     UP(64 * 64 * 9, &g->post_w);
     if ((r = upload_bn(g, t[i], t[i + 1], t[i + 2], t[i + 3], &g->post_s, &g->post_b))) goto fail;
     i += 4;
+    if ((r = upload_transposed(g, t[i], 256, 64, 9, 256, &g->up_t))) goto fail;
     UP(256 * 64 * 9, &g->up_w);
     UP(64, &g->up_a);
+    if ((r = upload_transposed(g, t[i], 3, 64, 81, 4, &g->tail_t))) goto fail;
     UP(3 * 64 * 81, &g->tail_w);
     UP(3, &g->tail_b);
 #undef UP
