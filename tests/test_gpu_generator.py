@@ -45,6 +45,23 @@ def test_sr_prolong_fp32_golden(cuda, golden):
     assert rel(out.data, golden["srnn2_out"]) < 1e-5
 
 
+@pytest.mark.parametrize("s,nc", [(2, 46), (4, 22)])
+def test_fp32_row_tiled_kernels_bitwise_equal_one_pixel_kernels(cuda, monkeypatch, s, nc):
+    """The row-tiled fp32 kernels (k_conv_rows / k_conv_tail_rows, sides 6 and 12) keep the accumulation
+    order of the one-pixel kernels they replaced: the whole pass is bitwise identical (partial CTAs included:
+    441 and 81 windows are not multiples of the windows per CTA)."""
+    from paper_2403_07936_b200 import srmodel
+    from paper_2403_07936_b200.grid import Grid, NormBounds
+    rng = np.random.default_rng(7)
+    c = (10.0 ** rng.uniform(-7, -3.5, (nc, nc))) * np.where(rng.random((nc, nc)) < 0.5, -1, 1)
+    c -= c.mean()
+    w = srmodel.random_weights(2, 5)
+    new = srmodel.sr_prolong(Grid(c), w, NormBounds(), s, precision="fp32").data
+    monkeypatch.setenv("MGSR_F32_LEGACY", "1")
+    old = srmodel.sr_prolong(Grid(c), w, NormBounds(), s, precision="fp32").data
+    assert np.array_equal(new, old)
+
+
 @pytest.mark.parametrize("s", [8, 16])
 def test_sr_prolong_two_pass_ratios(cuda, orc, s):
     from paper_2403_07936_b200 import srmodel
