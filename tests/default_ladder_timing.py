@@ -20,8 +20,8 @@ def main():
     w = srmodel.load_weights(os.path.join(ROOT, "artifacts", "trained_b8.mgsr"))
     cfg = solver.RunConfig(N_step=4, r_min=12, N_smooth=20)
     rows = []
-    for n, runs in [(192, [("spline", "fp16"), ("sr", "fp16"), ("sr", "fp32")]),
-                    (3072, [("spline", "fp16"), ("sr", "fp16"), ("sr", "fp32")])]:
+    for n, runs in [(192, [("spline", "fp16"), ("sr", "fp16"), ("sr", "mixed"), ("sr", "fp32")]),
+                    (3072, [("spline", "fp16"), ("sr", "fp16"), ("sr", "mixed"), ("sr", "fp32")])]:
         f = torch.from_numpy(datagen.scale_to_p_rms(datagen.grf_blobs_rhs(n, seed=0, kmax=n / 8), 1e-4)).cuda()
         for op, pr in runs:
             plan = solver.VCyclePlan(n, cfg, w, precision=pr)

@@ -90,7 +90,7 @@ int main() {
     cudaFuncSetAttribute(k_bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     const int iters = 4096;
     for (int mode = 0; mode < 3; ++mode)
-        for (int n : {16, 64, 128, 256}) {
+        for (int n : {16, 64, 128, 192, 256}) {
             k_bench<<<148, 128, 160 * 1024>>>(n, mode, iters, d);
             cudaError_t e = cudaDeviceSynchronize();
             long long h[148];
