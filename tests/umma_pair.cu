@@ -103,7 +103,7 @@ int main() {
     cfg.numAttrs = 1;
     const int iters = 4096;
     for (int mode = 0; mode < 2; ++mode)
-        for (int n : {64, 128, 192, 256}) {
+        for (int n : {64, 96, 128, 192, 256}) {
             cudaLaunchKernelEx(&cfg, k_pair, n, mode, iters, d);
             cudaError_t e = cudaDeviceSynchronize();
             long long h[148];
