@@ -173,12 +173,6 @@ constexpr int OFF_CONST = OFF_BAR + BAR_BYTES;
 constexpr int COL_ACC = 0, ACC_COLS = 192, COL_SKIP = 384;
 constexpr int COL_Z = COL_SKIP;   // tail accumulators (32 per Z tile, <= 4 tiles) reuse the skip columns + the spare 32
 
-// MGSR_SPLIT_N: a 3x3 unit's kernel-row MMAs are issued as two N = 96 halves (the 16-channel quarters {0, 2},
-// then {1, 3}) with a commit each, so the two halves of the epilogue warps start half a tile apart instead of
-// passing through the same phases together
-#ifndef MGSR_SPLIT_N
-#define MGSR_SPLIT_N 0
-#endif
 constexpr int NEPI = 16;                       // epilogue warps
 constexpr int NTHREADS = 64 + 32 * NEPI;       // 576
 constexpr int UP_QUARTERS = 4;
@@ -507,8 +501,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
     const uint32_t b_tw_peerfull = smem_u32(bars + BB + 21);   // [4] (leader) the peer's landed
     const uint32_t b_tw_empty = smem_u32(bars + BB + 25);   // [4] (both) tail MMAs of the quarter done
     const uint32_t b_post_done = smem_u32(bars + BB + 29);  // (both) post layer's MMAs done: buffer 0 free
-    const uint32_t b_acc_full2 = smem_u32(bars + BB + 30);  // [2] (both) MGSR_SPLIT_N: the second half's commit
-    static_assert((BB + 32) * 8 <= BAR_BYTES - 8, "barriers");
+    static_assert((BB + 30) * 8 <= BAR_BYTES - 8, "barriers");
     const uint32_t rank = cluster_rank();
     const bool leader = rank == 0;
     const int pair = int(blockIdx.x >> 1), npairs = int(gridDim.x >> 1);
@@ -538,7 +531,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
         }
         for (int b2 = 0; b2 < 2; ++b2) {
             mbar_init(b_acc_full + 8 * b2, 1);
-            mbar_init(b_acc_full2 + 8 * b2, 1);
             mbar_init(b_drained + 8 * b2, 2 * NEPI);
         }
         for (int t = 0; t < T; ++t) mbar_init(b_act_ready + 8 * t, 2 * NEPI);
@@ -644,8 +636,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
         const uint32_t act_base = smem_u32(act), ring_base = smem_u32(ring);
         const uint32_t i2c_base = smem_u32(i2c), u_base = smem_u32(ubuf);
         const uint32_t id192 = F16 ? idesc_f16(192) : idesc_bf16(192);
-        const uint32_t id96 = F16 ? idesc_f16(96) : idesc_bf16(96);
-        (void)id96;
         Tracer<INSTR> tr{nullptr, 0};
         // the accumulator buffer of the next unit was read by the epilogue of the unit two before
         auto acquire_acc = [&] {
@@ -684,29 +674,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
                         }
                         const uint64_t a = a_t + uint64_t(int64_t((dy - 1) * RPY));
                         const uint64_t b = make_desc(ring_base + s * UNIT_BYTES, 128, 1024);   // 12 n-groups of 8
-#if MGSR_SPLIT_N
-                        // half h: this CTA's n-groups 6 h .. 6 h + 5 (quarter h of its 32 channels x 3 dx) -> columns 96 h ..
-#pragma unroll
-                        for (int h = 0; h < 2; ++h) {
-#pragma unroll
-                            for (int ks = 0; ks < 4; ++ks)
-                                mma_bf16(d + 96 * h, a + uint64_t(ks * (2 * ACT_PLANE / 16)),
-                                         b + uint64_t(h * (6 * 1024 / 16) + ks * (256 / 16)), id96, (dy | ks) > 0);
-                            if (dy == 2 && h == 0) umma_commit(b_acc_full + 8 * vb);
-                        }
-#else
 #pragma unroll
                         for (int ks = 0; ks < 4; ++ks)
                             mma_bf16(d, a + uint64_t(ks * (2 * ACT_PLANE / 16)), b + uint64_t(ks * (256 / 16)), id192,
                                      (dy | ks) > 0);
-#endif
                         if (t == T - 1) umma_commit(b_empty + 8 * s);
                     }
-#if MGSR_SPLIT_N
-                    umma_commit(b_acc_full2 + 8 * vb);
-#else
                     umma_commit(b_acc_full + 8 * vb);
-#endif
                     if (lid == NLAYERS && t == T - 1) umma_commit(b_post_done);   // buffer 0 no longer read
                 }
                 __syncwarp();
@@ -783,10 +757,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
                             mma_bf16(d, a, b, idesc_f16(64), (kq | ks) > 0);
                         }
                         if (t == T - 1 && (V != 2 || (kq & 1) == 1)) umma_commit(b_empty + 8 * s);
-                        if (kq == G::NBUILD - 1) {
-                            umma_commit(b_acc_full + 8 * vb);
-                            if (MGSR_SPLIT_N) umma_commit(b_acc_full2 + 8 * vb);
-                        }
+                        if (kq == G::NBUILD - 1) umma_commit(b_acc_full + 8 * vb);
                         umma_commit(b_i2c_empty + 8 * ib);
                     }
                     __syncwarp();
@@ -835,7 +806,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
             for (int b2 = 0; b2 < 2; ++b2) mbar_arrive_leader(b_drained + 8 * b2);   // both buffers start free
         // wait for the next accumulator unit; returns this lane's TMEM address of its buffer
         auto acc_wait = [&]() -> uint32_t {
-            mbar_wait((MGSR_SPLIT_N && (cq & 1) ? b_acc_full2 : b_acc_full) + 8 * vb, (af_ph >> vb) & 1u);
+            mbar_wait(b_acc_full + 8 * vb, (af_ph >> vb) & 1u);
             af_ph ^= 1u << vb;
             tc_fence_after();
             return tmem + lane_addr + COL_ACC + ACC_COLS * vb;
@@ -854,7 +825,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_gen_tc(Params P) {
         // shuffle per partial.
         const int src_l = (px == 1 || !interior) ? lane : lane - 1, src_r = (px == G::WS || !interior) ? lane : lane + 1;
         auto load_dx3 = [&](float (&y)[16]) {
-            const uint32_t c = acc_wait() + (MGSR_SPLIT_N ? (cq & 1) * 96 + (cq >> 1) * 48 : (cq >> 1) * 96 + (cq & 1) * 48);
+            const uint32_t c = acc_wait() + (cq >> 1) * 96 + (cq & 1) * 48;
             uint32_t v01[32], v2[16];
             TMEM_LD32(c, v01);
             TMEM_LD16(c + 32, v2);
