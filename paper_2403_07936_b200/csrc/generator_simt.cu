@@ -235,6 +235,24 @@ __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
+#ifndef MGSR_ROW_FFMA2
+#define MGSR_ROW_FFMA2 1
+#endif
+#ifndef MGSR_TAIL_FFMA2
+#define MGSR_TAIL_FFMA2 1
+#endif
+__device__ __forceinline__ unsigned long long pack2f(float lo, float hi) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+// (lo, hi) = a * b + (lo, hi) on packed pairs
+__device__ __forceinline__ void ffma2(float &lo, float &hi, unsigned long long a, unsigned long long b) {
+    unsigned long long d = pack2f(lo, hi);
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(d) : "l"(a), "l"(b));
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(d));
+}
+
 // v[j] = row[clamp(6 * SEG + j - P, 0, H - 1)], j < K + 5, from the fewest aligned vector loads
 template <int K, int H, int SEG>
 __device__ __forceinline__ void rows_load(const float *row, float (&v)[K + 5]) {
@@ -283,6 +301,20 @@ __device__ __forceinline__ void rows_chunk(const float *s_win, const float *sw, 
             for (int dx = 0; dx < K; ++dx) {
                 const float4 wa = *reinterpret_cast<const float4 *>(sw + ((c * K + dy) * K + dx) * 64);
                 const float4 wb = *reinterpret_cast<const float4 *>(sw + ((c * K + dy) * K + dx) * 64 + 32);
+#if MGSR_ROW_FFMA2
+                // two FMAs per instruction (sm_100 FFMA2, each half an IEEE fma: bitwise the scalar result); the
+                // activation is the scalar-broadcast operand, a weight pair and an accumulator pair the packed ones
+                const unsigned long long w0 = pack2f(wa.x, wa.y), w1 = pack2f(wa.z, wa.w), w2 = pack2f(wb.x, wb.y),
+                                         w3 = pack2f(wb.z, wb.w);
+#pragma unroll
+                for (int i = 0; i < 6; ++i) {
+                    const unsigned long long a2 = pack2f(v[i + dx], v[i + dx]);
+                    ffma2(acc[i][0], acc[i][1], a2, w0);
+                    ffma2(acc[i][2], acc[i][3], a2, w1);
+                    ffma2(acc[i][4], acc[i][5], a2, w2);
+                    ffma2(acc[i][6], acc[i][7], a2, w3);
+                }
+#else
 #pragma unroll
                 for (int i = 0; i < 6; ++i) {
                     const float a = v[i + dx];
@@ -295,6 +327,7 @@ __device__ __forceinline__ void rows_chunk(const float *s_win, const float *sw, 
                     acc[i][6] = fmaf(a, wb.z, acc[i][6]);
                     acc[i][7] = fmaf(a, wb.w, acc[i][7]);
                 }
+#endif
             }
         }
     }
@@ -448,12 +481,23 @@ __device__ __forceinline__ void tail_chunk(const float *s_win, const float4 *sw,
 #pragma unroll
             for (int dx = 0; dx < K; ++dx) {
                 const float4 w4 = sw[(c * K + dy) * K + dx];
+#if MGSR_TAIL_FFMA2
+                // outputs 0 and 1 as a packed pair (weights (w.x, w.y) as loaded, the pixel as the broadcast operand),
+                // output 2 scalar
+                const unsigned long long w01 = pack2f(w4.x, w4.y);
+#pragma unroll
+                for (int i = 0; i < 12; ++i) {
+                    ffma2(acc[i][0], acc[i][1], pack2f(v[i + dx], v[i + dx]), w01);
+                    acc[i][2] = fmaf(v[i + dx], w4.z, acc[i][2]);
+                }
+#else
 #pragma unroll
                 for (int i = 0; i < 12; ++i) {
                     acc[i][0] = fmaf(v[i + dx], w4.x, acc[i][0]);
                     acc[i][1] = fmaf(v[i + dx], w4.y, acc[i][1]);
                     acc[i][2] = fmaf(v[i + dx], w4.z, acc[i][2]);
                 }
+#endif
             }
         }
     }
